@@ -1,0 +1,65 @@
+// Shared host/device plumbing for the bt200 library: error state, launch
+// accounting, dtype helpers.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include "../../include/bt200.h"
+
+namespace bt {
+
+// thread-local last error message (bt_last_error)
+void set_error(const char* fmt, ...);
+const char* last_error();
+
+// process-wide count of kernels launched by this library (bt_launch_count)
+extern std::atomic<long long> g_launches;
+inline void count_launch(int n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+int num_sms();
+
+inline cudaStream_t as_stream(bt_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
+
+}  // namespace bt
+
+// Validate a condition on the host before any launch; returns `code`.
+#define BT_REQUIRE(cond, code, ...)     \
+  do {                                  \
+    if (!(cond)) {                      \
+      ::bt::set_error(__VA_ARGS__);     \
+      return (code);                    \
+    }                                   \
+  } while (0)
+
+#define BT_CUDA_CHECK(expr)                                                                      \
+  do {                                                                                           \
+    cudaError_t _e = (expr);                                                                     \
+    if (_e != cudaSuccess) {                                                                     \
+      ::bt::set_error("%s failed: %s (%s:%d)", #expr, cudaGetErrorString(_e), __FILE__, __LINE__); \
+      return BT_ECUDA;                                                                           \
+    }                                                                                            \
+  } while (0)
+
+// After a <<<>>> launch: record it and surface launch-configuration errors.
+#define BT_LAUNCH_CHECK()                                                                          \
+  do {                                                                                             \
+    ::bt::count_launch();                                                                          \
+    cudaError_t _e = cudaGetLastError();                                                           \
+    if (_e != cudaSuccess) {                                                                       \
+      ::bt::set_error("kernel launch failed: %s (%s:%d)", cudaGetErrorString(_e), __FILE__, __LINE__); \
+      return BT_ECUDA;                                                                             \
+    }                                                                                              \
+  } while (0)
+
+#define BT_TRY(expr)          \
+  do {                        \
+    int _rc = (expr);         \
+    if (_rc != BT_OK) return _rc; \
+  } while (0)

@@ -1,0 +1,131 @@
+// Encoder runtime: one post-LN BERT layer and the stacked, padding-free
+// forward pass (reference encoder.py:337-437, OptFlags.all_on()), issued
+// stream-ordered from the host with no synchronisation, so the whole forward
+// can be captured into one CUDA graph.
+//
+// Layer data flow (packed [T, *] bf16 activations):
+//   qkv  = x Wqkv + bqkv                     GEMM #0 (bias epilogue)
+//   ctx  = fused varlen MHA(qkv)             short / long path
+//   proj = ctx Wo                            GEMM #1
+//   y0   = LN((proj + x) + bo)               fused add-bias+residual+LN
+//   h1   = gelu(y0 W1 + b1)                  GEMM #2 (bias+GELU epilogue)
+//   h2   = h1 W2                             GEMM #3
+//   x    = LN((h2 + y0) + b2)                fused add-bias+residual+LN
+
+#include "common.cuh"
+
+namespace bt {
+int gemm_launch(const void* A, const void* Bt, const float* bias, const void* residual, void* C, int M, int N, int K,
+                int epi, int force_bn, cudaStream_t s);
+int mha_launch(const void* qkv, const int32_t* seq_starts, int bs, int mx, int H, int d, int cutoff, int T, void* out,
+               int force_path, cudaStream_t s);
+
+static inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+struct LayerWs {
+  __nv_bfloat16 *qkv, *ctx, *proj, *y0, *h1;
+};
+
+static size_t layer_ws_bytes(int k, int f, int T) {
+  const size_t t = static_cast<size_t>(T);
+  return align_up(t * 3 * k * 2) + 3 * align_up(t * k * 2) + align_up(t * f * 2);
+}
+
+static LayerWs carve_layer(void* ws, int k, int f, int T) {
+  const size_t t = static_cast<size_t>(T);
+  uint8_t* p = static_cast<uint8_t*>(ws);
+  LayerWs w;
+  w.qkv = reinterpret_cast<__nv_bfloat16*>(p);
+  p += align_up(t * 3 * k * 2);
+  w.ctx = reinterpret_cast<__nv_bfloat16*>(p);
+  p += align_up(t * k * 2);
+  w.proj = reinterpret_cast<__nv_bfloat16*>(p);
+  p += align_up(t * k * 2);
+  w.y0 = reinterpret_cast<__nv_bfloat16*>(p);
+  p += align_up(t * k * 2);
+  w.h1 = reinterpret_cast<__nv_bfloat16*>(p);
+  return w;
+}
+
+static int check_cfg(const bt_layer_cfg* cfg) {
+  BT_REQUIRE(cfg != nullptr, BT_ECONFIG, "null layer config");
+  BT_REQUIRE(cfg->head_num >= 1 && cfg->head_size >= 1 && cfg->ffn_scale >= 1 && cfg->max_seq_len >= 1, BT_ECONFIG,
+             "layer config fields must be >= 1");
+  BT_REQUIRE(cfg->head_size == 64, BT_ECONFIG, "the sm_100a kernels support head_size 64, got %d", cfg->head_size);
+  BT_REQUIRE(cfg->split_seq_len >= 1, BT_ECONFIG, "split_seq_len must be >= 1, got %d", cfg->split_seq_len);
+  return BT_OK;
+}
+
+}  // namespace bt
+
+extern "C" int bt_ln_bias_residual(const void* x, const void* residual, const float* bias, const float* gamma,
+                                   const float* beta, float eps, void* out, int T, int k, bt_stream_t stream);
+extern "C" int bt_pack(const void*, int, const int32_t*, int, int, void*, int, bt_stream_t);
+extern "C" int bt_unpack(const void*, int, const int32_t*, int, int, int, void*, int, bt_stream_t);
+extern "C" int bt_plan_lengths(const int32_t*, int, int, int32_t*, int32_t*, bt_stream_t);
+
+extern "C" size_t bt_layer_workspace_bytes(const bt_layer_cfg* cfg, int T) {
+  if (!cfg) return 0;
+  const int k = cfg->head_num * cfg->head_size;
+  return bt::layer_ws_bytes(k, cfg->ffn_scale * k, T < 1 ? 1 : T);
+}
+
+extern "C" int bt_encoder_layer(const bt_layer_weights* w, const bt_layer_cfg* cfg, const int32_t* seq_starts, int bs,
+                                int T, void* x_inout, void* ws, size_t ws_bytes, bt_stream_t stream) {
+  BT_TRY(bt::check_cfg(cfg));
+  BT_REQUIRE(w != nullptr, BT_ESHAPE, "null layer weights");
+  BT_REQUIRE(T >= 1 && bs >= 1, BT_ESHAPE, "encoder_layer: T=%d bs=%d", T, bs);
+  const int k = cfg->head_num * cfg->head_size;
+  const int f = cfg->ffn_scale * k;
+  BT_REQUIRE(ws_bytes >= bt::layer_ws_bytes(k, f, T), BT_ESHAPE, "encoder_layer: workspace too small (%zu < %zu)",
+             ws_bytes, bt::layer_ws_bytes(k, f, T));
+  cudaStream_t s = bt::as_stream(stream);
+  bt::LayerWs L = bt::carve_layer(ws, k, f, T);
+  auto* x = static_cast<__nv_bfloat16*>(x_inout);
+
+  BT_TRY(bt::gemm_launch(x, w->qkv_w, w->qkv_b, nullptr, L.qkv, T, 3 * k, k, BT_EPI_BIAS, 0, s));
+  BT_TRY(bt::mha_launch(L.qkv, seq_starts, bs, cfg->max_seq_len, cfg->head_num, cfg->head_size, cfg->cutoff, T, L.ctx,
+                        0, s));
+  BT_TRY(bt::gemm_launch(L.ctx, w->ao_w, nullptr, nullptr, L.proj, T, k, k, BT_EPI_NONE, 0, s));
+  BT_TRY(bt_ln_bias_residual(L.proj, x, w->ao_b, w->ln0_g, w->ln0_b, w->ln0_eps, L.y0, T, k, stream));
+  BT_TRY(bt::gemm_launch(L.y0, w->w1, w->b1, nullptr, L.h1, T, f, k, BT_EPI_BIAS_GELU, 0, s));
+  BT_TRY(bt::gemm_launch(L.h1, w->w2, nullptr, nullptr, L.proj, T, k, f, BT_EPI_NONE, 0, s));
+  BT_TRY(bt_ln_bias_residual(L.proj, L.y0, w->b2, w->ln1_g, w->ln1_b, w->ln1_eps, x, T, k, stream));
+  return BT_OK;
+}
+
+extern "C" size_t bt_forward_workspace_bytes(const bt_layer_cfg* cfg, int bs, int T) {
+  if (!cfg) return 0;
+  const int k = cfg->head_num * cfg->head_size;
+  const size_t t = static_cast<size_t>(T < 1 ? 1 : T);
+  return bt::align_up((bs + 1) * sizeof(int32_t)) + bt::align_up(t * sizeof(int32_t)) + bt::align_up(t * k * 2) +
+         bt_layer_workspace_bytes(cfg, T);
+}
+
+extern "C" int bt_encoder_forward(const bt_layer_weights* layers, int n_layers, const bt_layer_cfg* cfg,
+                                  const int32_t* lengths, int bs, int T, const float* x_padded, float* out_padded,
+                                  void* ws, size_t ws_bytes, bt_stream_t stream) {
+  BT_TRY(bt::check_cfg(cfg));
+  BT_REQUIRE(n_layers >= 1 && layers != nullptr, BT_ECONFIG, "need >= 1 layer");
+  BT_REQUIRE(bs >= 1 && T >= 1 && T <= bs * cfg->max_seq_len, BT_ESHAPE, "forward: bs=%d T=%d mx=%d", bs, T,
+             cfg->max_seq_len);
+  BT_REQUIRE(ws_bytes >= bt_forward_workspace_bytes(cfg, bs, T), BT_ESHAPE, "forward: workspace too small");
+  const int k = cfg->head_num * cfg->head_size;
+  const int mx = cfg->max_seq_len;
+  uint8_t* p = static_cast<uint8_t*>(ws);
+  auto* seq_starts = reinterpret_cast<int32_t*>(p);
+  p += bt::align_up((bs + 1) * sizeof(int32_t));
+  auto* offsets = reinterpret_cast<int32_t*>(p);
+  p += bt::align_up(static_cast<size_t>(T) * sizeof(int32_t));
+  void* x = p;
+  p += bt::align_up(static_cast<size_t>(T) * k * 2);
+  void* lws = p;
+  const size_t lws_bytes = bt_layer_workspace_bytes(cfg, T);
+
+  BT_TRY(bt_plan_lengths(lengths, bs, mx, seq_starts, offsets, stream));
+  BT_TRY(bt_pack(x_padded, BT_F32, offsets, T, k, x, BT_BF16, stream));
+  for (int li = 0; li < n_layers; ++li)
+    BT_TRY(bt_encoder_layer(&layers[li], cfg, seq_starts, bs, T, x, lws, lws_bytes, stream));
+  BT_TRY(bt_unpack(x, BT_BF16, seq_starts, bs, mx, k, out_padded, BT_F32, stream));
+  return BT_OK;
+}

@@ -1,0 +1,138 @@
+// Fused add-bias + residual + LayerNorm (paper section III-C1, reference
+// fusion.py:79-98):  z = (x + residual) + bias;  y = gamma * (z - mean) /
+// sqrt(var + eps) + beta, population variance over the row.
+//
+// HBM-bound: one warp per row, each lane holds ceil(k/256) 16-byte chunks of
+// x and residual in registers (k = 768 -> 3, k = 1024 -> 4), fp32 two-pass
+// mean / centred variance with shuffle reductions, one global round trip.
+
+#include "common.cuh"
+#include "ptx.cuh"
+
+namespace bt {
+
+template <int NCH>
+__global__ void __launch_bounds__(256) ln_bias_residual_kernel(const __nv_bfloat16* __restrict__ x,
+                                                               const __nv_bfloat16* __restrict__ res,
+                                                               const float* __restrict__ bias,
+                                                               const float* __restrict__ gamma,
+                                                               const float* __restrict__ beta, float eps,
+                                                               __nv_bfloat16* __restrict__ out, int T, int k) {
+  const int lane = threadIdx.x & 31;
+  const int wpb = blockDim.x >> 5;
+  const int nchunk = k >> 3;
+  const float inv_k = 1.0f / static_cast<float>(k);
+  for (int row = blockIdx.x * wpb + (threadIdx.x >> 5); row < T; row += gridDim.x * wpb) {
+    const size_t base = static_cast<size_t>(row) * k;
+    float z[NCH][8];
+    float sum = 0.f;
+#pragma unroll
+    for (int i = 0; i < NCH; ++i) {
+      const int c = lane + 32 * i;
+      if (c < nchunk) {
+        const uint4 xv = __ldg(reinterpret_cast<const uint4*>(x + base) + c);
+        const __nv_bfloat162* xh = reinterpret_cast<const __nv_bfloat162*>(&xv);
+        uint4 rv = make_uint4(0, 0, 0, 0);
+        if (res) rv = __ldg(reinterpret_cast<const uint4*>(res + base) + c);
+        const __nv_bfloat162* rh = reinterpret_cast<const __nv_bfloat162*>(&rv);
+        float b[8];
+        if (bias) {
+          const float4 b0 = __ldg(reinterpret_cast<const float4*>(bias) + 2 * c);
+          const float4 b1 = __ldg(reinterpret_cast<const float4*>(bias) + 2 * c + 1);
+          b[0] = b0.x; b[1] = b0.y; b[2] = b0.z; b[3] = b0.w; b[4] = b1.x; b[5] = b1.y; b[6] = b1.z; b[7] = b1.w;
+        } else {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) b[e] = 0.f;
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 xf = __bfloat1622float2(xh[e]);
+          const float2 rf = __bfloat1622float2(rh[e]);
+          z[i][2 * e] = (xf.x + rf.x) + b[2 * e];  // (x + residual) + bias, fusion.py:96
+          z[i][2 * e + 1] = (xf.y + rf.y) + b[2 * e + 1];
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) sum += z[i][e];
+      } else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) z[i][e] = 0.f;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    const float mean = sum * inv_k;
+    float sq = 0.f;
+#pragma unroll
+    for (int i = 0; i < NCH; ++i) {
+      if (lane + 32 * i < nchunk) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float d = z[i][e] - mean;
+          sq += d * d;
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+    const float rstd = 1.0f / sqrtf(sq * inv_k + eps);
+#pragma unroll
+    for (int i = 0; i < NCH; ++i) {
+      const int c = lane + 32 * i;
+      if (c < nchunk) {
+        const float4 g0 = __ldg(reinterpret_cast<const float4*>(gamma) + 2 * c);
+        const float4 g1 = __ldg(reinterpret_cast<const float4*>(gamma) + 2 * c + 1);
+        const float4 e0 = __ldg(reinterpret_cast<const float4*>(beta) + 2 * c);
+        const float4 e1 = __ldg(reinterpret_cast<const float4*>(beta) + 2 * c + 1);
+        const float g[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+        const float be[8] = {e0.x, e0.y, e0.z, e0.w, e1.x, e1.y, e1.z, e1.w};
+        uint4 o;
+        uint32_t* ow = reinterpret_cast<uint32_t*>(&o);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float y0 = g[2 * e] * ((z[i][2 * e] - mean) * rstd) + be[2 * e];
+          const float y1 = g[2 * e + 1] * ((z[i][2 * e + 1] - mean) * rstd) + be[2 * e + 1];
+          ow[e] = ptx::pack_bf16x2(y0, y1);
+        }
+        reinterpret_cast<uint4*>(out + base)[c] = o;
+      }
+    }
+  }
+}
+
+template <int NCH>
+static void launch_ln(const __nv_bfloat16* x, const __nv_bfloat16* r, const float* b, const float* g, const float* be,
+                      float eps, __nv_bfloat16* out, int T, int k, cudaStream_t s) {
+  const int threads = 256, wpb = threads / 32;
+  const int sms = num_sms() > 0 ? num_sms() : 148;
+  long long grid = (T + wpb - 1) / wpb;
+  if (grid > sms * 8LL) grid = sms * 8LL;
+  if (grid < 1) grid = 1;
+  ln_bias_residual_kernel<NCH><<<static_cast<int>(grid), threads, 0, s>>>(x, r, b, g, be, eps, out, T, k);
+}
+
+}  // namespace bt
+
+extern "C" int bt_ln_bias_residual(const void* x, const void* residual, const float* bias, const float* gamma,
+                                   const float* beta, float eps, void* out, int T, int k, bt_stream_t stream) {
+  BT_REQUIRE(T >= 0 && k >= 8 && k % 8 == 0 && k <= 4096, BT_ESHAPE,
+             "layernorm: need k %% 8 == 0 and 8 <= k <= 4096, got k=%d", k);
+  BT_REQUIRE(eps > 0.f, BT_ESHAPE, "layernorm eps must be > 0, got %g", static_cast<double>(eps));
+  BT_REQUIRE(x && gamma && beta && out, BT_ESHAPE, "layernorm: null pointer");
+  if (T == 0) return BT_OK;
+  const auto* xb = static_cast<const __nv_bfloat16*>(x);
+  const auto* rb = static_cast<const __nv_bfloat16*>(residual);
+  auto* ob = static_cast<__nv_bfloat16*>(out);
+  cudaStream_t s = bt::as_stream(stream);
+  const int nch = (k / 8 + 31) / 32;
+  switch (nch) {
+    case 1: bt::launch_ln<1>(xb, rb, bias, gamma, beta, eps, ob, T, k, s); break;
+    case 2: bt::launch_ln<2>(xb, rb, bias, gamma, beta, eps, ob, T, k, s); break;
+    case 3: bt::launch_ln<3>(xb, rb, bias, gamma, beta, eps, ob, T, k, s); break;
+    case 4: bt::launch_ln<4>(xb, rb, bias, gamma, beta, eps, ob, T, k, s); break;
+    case 5: case 6: bt::launch_ln<6>(xb, rb, bias, gamma, beta, eps, ob, T, k, s); break;
+    case 7: case 8: bt::launch_ln<8>(xb, rb, bias, gamma, beta, eps, ob, T, k, s); break;
+    default: bt::launch_ln<16>(xb, rb, bias, gamma, beta, eps, ob, T, k, s); break;
+  }
+  BT_LAUNCH_CHECK();
+  return BT_OK;
+}

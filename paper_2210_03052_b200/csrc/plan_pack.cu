@@ -1,0 +1,366 @@
+// Zero-padding removal (ByteTransformer section III-D, reference packing.py):
+//   * plan: mask -> lengths -> exclusive prefix sum (seq_starts) -> offsets
+//   * pack: gather valid rows into a contiguous [T, k] tensor (+ fp32->bf16)
+//   * unpack: scatter back with exact-zero padded rows (+ bf16->fp32)
+// All kernels are HBM-bound data movement; 16-byte vector accesses, grids
+// sized in multiples of the SM count.
+
+#include <cstdarg>
+#include <cstring>
+
+#include <type_traits>
+
+#include "common.cuh"
+#include "ptx.cuh"
+
+namespace bt {
+
+// ------------------------------------------------------------ library state
+std::atomic<long long> g_launches{0};
+static thread_local char t_err[1024] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(t_err, sizeof(t_err), fmt, ap);
+  va_end(ap);
+}
+const char* last_error() { return t_err; }
+
+int num_sms() {
+  static int cached = -1;
+  if (cached < 0) {
+    int dev = 0, n = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+      cudaGetLastError();
+      return 0;
+    }
+    cached = n;
+  }
+  return cached;
+}
+
+// ------------------------------------------------------------------ plan
+// One warp per mask row: count ones, find the first zero, flag entries that
+// are not 0/1.  A row is prefix-shaped iff count == first_zero (packing.py:
+// 102-109 rejects anything else).
+__global__ void plan_rows_kernel(const uint8_t* __restrict__ mask, int bs, int mx, int32_t* __restrict__ lengths,
+                                 int32_t* __restrict__ status) {
+  const int warps_per_block = blockDim.x / 32;
+  const int lane = threadIdx.x & 31;
+  for (int row = blockIdx.x * warps_per_block + threadIdx.x / 32; row < bs; row += gridDim.x * warps_per_block) {
+    const uint8_t* m = mask + static_cast<size_t>(row) * mx;
+    int ones = 0, first_zero = mx, bad = 0;
+    for (int j = lane; j < mx; j += 32) {
+      const uint8_t v = m[j];
+      bad |= (v > 1);
+      ones += (v == 1);
+      if (v == 0 && j < first_zero) first_zero = j;
+    }
+    for (int o = 16; o; o >>= 1) {
+      ones += __shfl_xor_sync(0xffffffffu, ones, o);
+      bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+      first_zero = min(first_zero, __shfl_xor_sync(0xffffffffu, first_zero, o));
+    }
+    if (lane == 0) {
+      lengths[row] = ones;
+      int st = 0;
+      if (bad) st |= 1;
+      if (!bad && ones != first_zero) st |= 2;
+      if (ones == 0) st |= 4;
+      if (st) atomicOr(status, st);
+    }
+  }
+}
+
+// Single-CTA exclusive scan of lengths -> seq_starts[bs+1] (+ total T).
+// 1024 threads, chunked over bs with a running carry.
+__global__ void __launch_bounds__(1024) plan_scan_kernel(const int32_t* __restrict__ lengths, int bs,
+                                                          int32_t* __restrict__ seq_starts,
+                                                          int32_t* __restrict__ valid_cnt) {
+  __shared__ int32_t warp_sums[32];
+  __shared__ int32_t carry_s;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid == 0) carry_s = 0;
+  __syncthreads();
+  for (int base = 0; base < bs; base += 1024) {
+    const int i = base + tid;
+    const int v = (i < bs) ? lengths[i] : 0;
+    int x = v;  // inclusive warp scan
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_sums[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      int w = warp_sums[lane];
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += y;
+      }
+      warp_sums[lane] = w;  // inclusive over warps
+    }
+    __syncthreads();
+    const int carry = carry_s;
+    const int incl = x + (wid ? warp_sums[wid - 1] : 0) + carry;
+    if (i < bs) seq_starts[i] = incl - v;
+    __syncthreads();
+    if (tid == 1023) carry_s = incl;
+    __syncthreads();
+  }
+  if (tid == 0) {
+    seq_starts[bs] = carry_s;
+    if (valid_cnt) *valid_cnt = carry_s;
+  }
+}
+
+// offsets[seq_starts[b] + j] = b*mx + j for j < len[b]  (the flat indices of
+// the ones of a prefix-shaped mask, i.e. flatnonzero, packing.py:115).
+// One CTA-slice per sequence, grid-strided.
+__global__ void plan_offsets_kernel(const int32_t* __restrict__ seq_starts, int bs, int mx,
+                                    int32_t* __restrict__ offsets) {
+  for (int b = blockIdx.x; b < bs; b += gridDim.x) {
+    const int s0 = seq_starts[b];
+    const int len = seq_starts[b + 1] - s0;
+    for (int j = threadIdx.x; j < len; j += blockDim.x) offsets[s0 + j] = b * mx + j;
+  }
+}
+
+// ------------------------------------------------------------------ pack
+__device__ __forceinline__ void load8(const float* p, float (&v)[8]) {
+  const float4 a = __ldg(reinterpret_cast<const float4*>(p));
+  const float4 b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+__device__ __forceinline__ void load8(const __nv_bfloat16* p, float (&v)[8]) {
+  const uint4 a = __ldg(reinterpret_cast<const uint4*>(p));
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&a);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 f = __bfloat1622float2(h[i]);
+    v[2 * i] = f.x;
+    v[2 * i + 1] = f.y;
+  }
+}
+__device__ __forceinline__ void store8(float* p, const float (&v)[8]) {
+  reinterpret_cast<float4*>(p)[0] = make_float4(v[0], v[1], v[2], v[3]);
+  reinterpret_cast<float4*>(p)[1] = make_float4(v[4], v[5], v[6], v[7]);
+}
+__device__ __forceinline__ void store8(__nv_bfloat16* p, const float (&v)[8]) {
+  uint4 o;
+  o.x = ptx::pack_bf16x2(v[0], v[1]);
+  o.y = ptx::pack_bf16x2(v[2], v[3]);
+  o.z = ptx::pack_bf16x2(v[4], v[5]);
+  o.w = ptx::pack_bf16x2(v[6], v[7]);
+  *reinterpret_cast<uint4*>(p) = o;
+}
+__device__ __forceinline__ void zero8(float* p) {
+  reinterpret_cast<float4*>(p)[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+  reinterpret_cast<float4*>(p)[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+__device__ __forceinline__ void zero8(__nv_bfloat16* p) { *reinterpret_cast<uint4*>(p) = make_uint4(0, 0, 0, 0); }
+
+// Exact fp32 copies (pack/unpack in fp32 are bit copies, packing.py:148,159).
+__device__ __forceinline__ void copy8(const float* s, float* d) {
+  reinterpret_cast<float4*>(d)[0] = __ldg(reinterpret_cast<const float4*>(s));
+  reinterpret_cast<float4*>(d)[1] = __ldg(reinterpret_cast<const float4*>(s) + 1);
+}
+__device__ __forceinline__ void copy8(const __nv_bfloat16* s, __nv_bfloat16* d) {
+  *reinterpret_cast<uint4*>(d) = __ldg(reinterpret_cast<const uint4*>(s));
+}
+template <typename Tin, typename Tout>
+__device__ __forceinline__ void move8(const Tin* s, Tout* d) {
+  if constexpr (std::is_same<Tin, Tout>::value) {
+    copy8(s, d);
+  } else {
+    float v[8];
+    load8(s, v);
+    store8(d, v);
+  }
+}
+
+__device__ __forceinline__ float to_f(float v) { return v; }
+__device__ __forceinline__ float to_f(__nv_bfloat16 v) { return __bfloat162float(v); }
+template <typename T>
+__device__ __forceinline__ T from_f(float v);
+template <>
+__device__ __forceinline__ float from_f<float>(float v) { return v; }
+template <>
+__device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
+
+// Element-wise variants for widths that are not a multiple of 8 (the
+// reference accepts any hidden width; the encoder itself uses k % 64 == 0).
+template <typename Tin, typename Tout>
+__global__ void pack_scalar_kernel(const Tin* __restrict__ padded, const int32_t* __restrict__ offsets, int T, int k,
+                                   Tout* __restrict__ packed) {
+  const long long total = static_cast<long long>(T) * k;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int row = static_cast<int>(i / k);
+    const int c = static_cast<int>(i - static_cast<long long>(row) * k);
+    packed[i] = from_f<Tout>(to_f(padded[static_cast<long long>(__ldg(offsets + row)) * k + c]));
+  }
+}
+template <typename Tin, typename Tout>
+__global__ void unpack_scalar_kernel(const Tin* __restrict__ packed, const int32_t* __restrict__ seq_starts, int bs,
+                                     int mx, int k, Tout* __restrict__ padded) {
+  const long long total = static_cast<long long>(bs) * mx * k;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long prow = i / k;
+    const int c = static_cast<int>(i - prow * k);
+    const int b = static_cast<int>(prow / mx);
+    const int j = static_cast<int>(prow - static_cast<long long>(b) * mx);
+    const int s0 = __ldg(seq_starts + b);
+    const int len = __ldg(seq_starts + b + 1) - s0;
+    padded[i] = j < len ? from_f<Tout>(to_f(packed[static_cast<long long>(s0 + j) * k + c])) : from_f<Tout>(0.f);
+  }
+}
+
+template <typename Tin, typename Tout>
+__global__ void pack_kernel(const Tin* __restrict__ padded, const int32_t* __restrict__ offsets, int T, int k,
+                            Tout* __restrict__ packed) {
+  const int chunks = k / 8;
+  const long long total = static_cast<long long>(T) * chunks;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int row = static_cast<int>(i / chunks);
+    const int c = static_cast<int>(i - static_cast<long long>(row) * chunks) * 8;
+    const long long src = static_cast<long long>(__ldg(offsets + row)) * k + c;
+    move8(padded + src, packed + static_cast<long long>(row) * k + c);
+  }
+}
+
+// One pass over every padded row: valid rows copy from their packed row,
+// padded rows are written with zeros (so no separate memset pass).
+template <typename Tin, typename Tout>
+__global__ void unpack_kernel(const Tin* __restrict__ packed, const int32_t* __restrict__ seq_starts, int bs,
+                              int mx, int k, Tout* __restrict__ padded) {
+  const int chunks = k / 8;
+  const long long total = static_cast<long long>(bs) * mx * chunks;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long prow = i / chunks;
+    const int c = static_cast<int>(i - prow * chunks) * 8;
+    const int b = static_cast<int>(prow / mx);
+    const int j = static_cast<int>(prow - static_cast<long long>(b) * mx);
+    const int s0 = __ldg(seq_starts + b);
+    const int len = __ldg(seq_starts + b + 1) - s0;
+    Tout* dst = padded + prow * k + c;
+    if (j < len) {
+      move8(packed + static_cast<long long>(s0 + j) * k + c, dst);
+    } else {
+      zero8(dst);
+    }
+  }
+}
+
+static int grid_for(long long work_items, int threads) {
+  const int sms = num_sms() > 0 ? num_sms() : 148;
+  long long blocks = (work_items + threads - 1) / threads;
+  const long long cap = static_cast<long long>(sms) * 8;  // 8 x 256-thread CTAs per SM resident
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  return static_cast<int>(blocks);
+}
+
+template <typename Tin, typename Tout>
+static void launch_pack(const void* in, const int32_t* offsets, int T, int k, void* out, cudaStream_t s) {
+  const int threads = 256;
+  if (k % 8 == 0) {
+    pack_kernel<<<grid_for(static_cast<long long>(T) * (k / 8), threads), threads, 0, s>>>(
+        static_cast<const Tin*>(in), offsets, T, k, static_cast<Tout*>(out));
+  } else {
+    pack_scalar_kernel<<<grid_for(static_cast<long long>(T) * k, threads), threads, 0, s>>>(
+        static_cast<const Tin*>(in), offsets, T, k, static_cast<Tout*>(out));
+  }
+}
+template <typename Tin, typename Tout>
+static void launch_unpack(const void* in, const int32_t* starts, int bs, int mx, int k, void* out, cudaStream_t s) {
+  const int threads = 256;
+  if (k % 8 == 0) {
+    unpack_kernel<<<grid_for(static_cast<long long>(bs) * mx * (k / 8), threads), threads, 0, s>>>(
+        static_cast<const Tin*>(in), starts, bs, mx, k, static_cast<Tout*>(out));
+  } else {
+    unpack_scalar_kernel<<<grid_for(static_cast<long long>(bs) * mx * k, threads), threads, 0, s>>>(
+        static_cast<const Tin*>(in), starts, bs, mx, k, static_cast<Tout*>(out));
+  }
+}
+
+}  // namespace bt
+
+using namespace bt;
+
+extern "C" {
+
+int bt_version(void) { return 1; }
+const char* bt_last_error(void) { return bt::last_error(); }
+long long bt_launch_count(void) { return bt::g_launches.load(); }
+int bt_num_sms(void) { return bt::num_sms(); }
+
+int bt_plan_mask(const uint8_t* mask, int bs, int mx, int32_t* lengths, int32_t* seq_starts, int32_t* offsets,
+                 int32_t* valid_cnt_dev, int32_t* status_dev, bt_stream_t stream) {
+  BT_REQUIRE(bs >= 1 && mx >= 1, BT_ESHAPE, "mask must be at least 1x1, got %dx%d", bs, mx);
+  BT_REQUIRE(static_cast<long long>(bs) * mx < (1LL << 31), BT_ESHAPE, "mask too large (%d x %d)", bs, mx);
+  BT_REQUIRE(mask && lengths && seq_starts && offsets && status_dev, BT_ESHAPE, "null pointer");
+  cudaStream_t s = as_stream(stream);
+  BT_CUDA_CHECK(cudaMemsetAsync(status_dev, 0, sizeof(int32_t), s));
+  const int warps = 8;
+  const int sms = num_sms() > 0 ? num_sms() : 148;
+  int grid = (bs + warps - 1) / warps;
+  if (grid > sms * 8) grid = sms * 8;
+  plan_rows_kernel<<<grid, warps * 32, 0, s>>>(mask, bs, mx, lengths, status_dev);
+  BT_LAUNCH_CHECK();
+  plan_scan_kernel<<<1, 1024, 0, s>>>(lengths, bs, seq_starts, valid_cnt_dev);
+  BT_LAUNCH_CHECK();
+  plan_offsets_kernel<<<bs < sms * 4 ? bs : sms * 4, 256, 0, s>>>(seq_starts, bs, mx, offsets);
+  BT_LAUNCH_CHECK();
+  return BT_OK;
+}
+
+int bt_plan_lengths(const int32_t* lengths, int bs, int mx, int32_t* seq_starts, int32_t* offsets,
+                    bt_stream_t stream) {
+  BT_REQUIRE(bs >= 1 && mx >= 1, BT_ESHAPE, "batch must be at least 1x1, got %dx%d", bs, mx);
+  BT_REQUIRE(lengths && seq_starts, BT_ESHAPE, "null pointer");
+  cudaStream_t s = as_stream(stream);
+  const int sms = num_sms() > 0 ? num_sms() : 148;
+  plan_scan_kernel<<<1, 1024, 0, s>>>(lengths, bs, seq_starts, nullptr);
+  BT_LAUNCH_CHECK();
+  if (offsets) {
+    plan_offsets_kernel<<<bs < sms * 4 ? bs : sms * 4, 256, 0, s>>>(seq_starts, bs, mx, offsets);
+    BT_LAUNCH_CHECK();
+  }
+  return BT_OK;
+}
+
+int bt_pack(const void* padded, int in_dtype, const int32_t* offsets, int T, int k, void* packed, int out_dtype,
+            bt_stream_t stream) {
+  BT_REQUIRE(T >= 0 && k >= 1, BT_ESHAPE, "pack: need T >= 0 and k >= 1, got T=%d k=%d", T, k);
+  BT_REQUIRE((in_dtype == BT_F32 || in_dtype == BT_BF16) && (out_dtype == BT_F32 || out_dtype == BT_BF16), BT_ECONFIG,
+             "pack: unsupported dtypes %d -> %d", in_dtype, out_dtype);
+  if (T == 0) return BT_OK;
+  cudaStream_t s = as_stream(stream);
+  if (in_dtype == BT_F32 && out_dtype == BT_BF16) launch_pack<float, __nv_bfloat16>(padded, offsets, T, k, packed, s);
+  else if (in_dtype == BT_F32) launch_pack<float, float>(padded, offsets, T, k, packed, s);
+  else if (out_dtype == BT_BF16) launch_pack<__nv_bfloat16, __nv_bfloat16>(padded, offsets, T, k, packed, s);
+  else launch_pack<__nv_bfloat16, float>(padded, offsets, T, k, packed, s);
+  BT_LAUNCH_CHECK();
+  return BT_OK;
+}
+
+int bt_unpack(const void* packed, int in_dtype, const int32_t* seq_starts, int bs, int mx, int k, void* padded,
+              int out_dtype, bt_stream_t stream) {
+  BT_REQUIRE(bs >= 1 && mx >= 1 && k >= 1, BT_ESHAPE, "unpack: bad shape bs=%d mx=%d k=%d", bs, mx, k);
+  BT_REQUIRE((in_dtype == BT_F32 || in_dtype == BT_BF16) && (out_dtype == BT_F32 || out_dtype == BT_BF16), BT_ECONFIG,
+             "unpack: unsupported dtypes %d -> %d", in_dtype, out_dtype);
+  cudaStream_t s = as_stream(stream);
+  if (in_dtype == BT_BF16 && out_dtype == BT_F32) launch_unpack<__nv_bfloat16, float>(packed, seq_starts, bs, mx, k, padded, s);
+  else if (in_dtype == BT_F32 && out_dtype == BT_F32) launch_unpack<float, float>(packed, seq_starts, bs, mx, k, padded, s);
+  else if (in_dtype == BT_BF16) launch_unpack<__nv_bfloat16, __nv_bfloat16>(packed, seq_starts, bs, mx, k, padded, s);
+  else launch_unpack<float, __nv_bfloat16>(packed, seq_starts, bs, mx, k, padded, s);
+  BT_LAUNCH_CHECK();
+  return BT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,491 @@
+"""BERT encoder layer and stacked forward on the B200 (reference
+encoder.py:1-437), drop-in for ``packbert.encoder``.
+
+The configuration, weight containers, deterministic init, PKBW weight files
+and key=value config parsing are the reference's (same names, fields, RNG
+draws, byte format and error types).  ``encoder_layer`` / ``forward`` run the
+padding-free pipeline of ``OptFlags.all_on()`` on sm_100a through the C ABI
+(``bt_encoder_layer`` / ``bt_encoder_forward``): device plan + pack, four
+tcgen05 GEMMs with fused bias / bias+GELU epilogues, fused varlen MHA, two
+fused add-bias+residual+LayerNorm passes per layer, unpack.  Weights are
+uploaded once per ``EncoderWeights`` object to bf16 (transposed to the
+K-major operand layout) and cached.
+
+The other ladder rungs (``OptFlags`` subsets, reference bench.py:35-41) are
+served by ``ladder.py`` from the same kernels.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import struct
+import threading
+import weakref
+from dataclasses import dataclass, field, replace
+from pathlib import Path
+
+import numpy as np
+
+from . import _lib
+from .attention import DEFAULT_CUTOFF, DEFAULT_SPLIT_SEQ_LEN
+from .errors import ConfigError, ShapeError, WeightFormatError
+from .fusion import LayernormParams
+from .packing import PackingPlan, SeqLengths, as_seq_lengths, ensure_plan, plan_for_lengths
+from .tensor import FlopCounter, Tensor, host_array, is_device, rows_cols
+
+WEIGHT_INIT_RANGE = 0.02
+
+
+@dataclass(frozen=True)
+class OptFlags:
+    fuse_layernorm: bool = False
+    fuse_bias_gelu: bool = False
+    zero_padding: bool = False
+    fused_mha: bool = False
+
+    @classmethod
+    def all_on(cls) -> "OptFlags":
+        return cls(True, True, True, True)
+
+
+@dataclass(frozen=True)
+class ModelConfig:
+    layers: int
+    head_num: int
+    head_size: int
+    max_seq_len: int
+    batch_size: int
+    ffn_scale: int = 4
+    cutoff: int = DEFAULT_CUTOFF
+    split_seq_len: int = DEFAULT_SPLIT_SEQ_LEN
+    flags: OptFlags = field(default_factory=OptFlags)
+    share_layer_weights: bool = False
+
+    def __post_init__(self):
+        for name in ("layers", "head_num", "head_size", "max_seq_len", "batch_size", "ffn_scale"):
+            if getattr(self, name) < 1:
+                raise ConfigError(f"{name} must be >= 1, got {getattr(self, name)}")
+        if self.flags.fused_mha and not self.flags.zero_padding:
+            raise ConfigError("fused_mha requires zero_padding: the fused kernels consume the packing plan")
+
+    @property
+    def hidden_dim(self) -> int:
+        return self.head_num * self.head_size
+
+    def with_flags(self, flags: OptFlags) -> "ModelConfig":
+        return replace(self, flags=flags)
+
+
+PRESETS: dict[str, dict] = {
+    "bert_base": {"layers": 12, "head_num": 12, "head_size": 64, "share_layer_weights": False},
+    "albert": {"layers": 12, "head_num": 16, "head_size": 64, "share_layer_weights": True},
+    "distilbert": {"layers": 6, "head_num": 12, "head_size": 64, "share_layer_weights": False},
+    "deberta_cfg": {"layers": 12, "head_num": 12, "head_size": 64, "share_layer_weights": False},
+}
+# BERT-large geometry of the north-star configs C3/C5 (not a reference preset).
+BERT_LARGE = {"layers": 24, "head_num": 16, "head_size": 64, "share_layer_weights": False}
+
+
+def preset_config(name: str, batch_size: int, max_seq_len: int, flags: OptFlags = OptFlags(),
+                  layers: int | None = None) -> ModelConfig:
+    if name not in PRESETS:
+        raise ConfigError(f"unknown preset {name!r}; choose from {sorted(PRESETS)}")
+    p = PRESETS[name]
+    return ModelConfig(layers=layers if layers is not None else p["layers"], head_num=p["head_num"],
+                       head_size=p["head_size"], max_seq_len=max_seq_len, batch_size=batch_size, flags=flags,
+                       share_layer_weights=p["share_layer_weights"])
+
+
+def as_model_config(cfg) -> ModelConfig:
+    """Accept the reference's ModelConfig (duck-typed) or ours."""
+    if isinstance(cfg, ModelConfig):
+        return cfg
+    f = cfg.flags
+    return ModelConfig(layers=cfg.layers, head_num=cfg.head_num, head_size=cfg.head_size,
+                       max_seq_len=cfg.max_seq_len, batch_size=cfg.batch_size, ffn_scale=cfg.ffn_scale,
+                       cutoff=cfg.cutoff, split_seq_len=cfg.split_seq_len,
+                       flags=OptFlags(f.fuse_layernorm, f.fuse_bias_gelu, f.zero_padding, f.fused_mha),
+                       share_layer_weights=cfg.share_layer_weights)
+
+
+@dataclass(eq=False)
+class LayerWeights:
+    """Per-layer parameters, [in, out] matrices, QKV as column blocks
+    (reference encoder.py:108-122)."""
+
+    qkv_weight: np.ndarray
+    qkv_bias: np.ndarray
+    attn_out_weight: np.ndarray
+    attn_out_bias: np.ndarray
+    ffn_w1: np.ndarray
+    ffn_b1: np.ndarray
+    ffn_w2: np.ndarray
+    ffn_b2: np.ndarray
+    ln0: LayernormParams
+    ln1: LayernormParams
+
+
+@dataclass(eq=False)
+class EncoderWeights:
+    layers: list
+    shared: bool
+
+    def layer(self, index: int):
+        return self.layers[0] if self.shared else self.layers[index]
+
+
+def _tensor_shapes(config: ModelConfig) -> list[tuple[str, tuple[int, ...]]]:
+    h = config.hidden_dim
+    f = config.ffn_scale * h
+    return [("qkv_weight", (h, 3 * h)), ("qkv_bias", (3 * h,)), ("attn_out_weight", (h, h)),
+            ("attn_out_bias", (h,)), ("ffn_w1", (h, f)), ("ffn_b1", (f,)), ("ffn_w2", (f, h)), ("ffn_b2", (h,)),
+            ("ln0_gamma", (h,)), ("ln0_beta", (h,)), ("ln1_gamma", (h,)), ("ln1_beta", (h,))]
+
+
+def _layer_from_arrays(a: dict) -> LayerWeights:
+    return LayerWeights(qkv_weight=a["qkv_weight"], qkv_bias=a["qkv_bias"], attn_out_weight=a["attn_out_weight"],
+                        attn_out_bias=a["attn_out_bias"], ffn_w1=a["ffn_w1"], ffn_b1=a["ffn_b1"],
+                        ffn_w2=a["ffn_w2"], ffn_b2=a["ffn_b2"],
+                        ln0=LayernormParams(gamma=a["ln0_gamma"], beta=a["ln0_beta"]),
+                        ln1=LayernormParams(gamma=a["ln1_gamma"], beta=a["ln1_beta"]))
+
+
+def _layer_arrays(layer) -> dict:
+    return {"qkv_weight": layer.qkv_weight, "qkv_bias": layer.qkv_bias, "attn_out_weight": layer.attn_out_weight,
+            "attn_out_bias": layer.attn_out_bias, "ffn_w1": layer.ffn_w1, "ffn_b1": layer.ffn_b1,
+            "ffn_w2": layer.ffn_w2, "ffn_b2": layer.ffn_b2, "ln0_gamma": np.asarray(layer.ln0.gamma),
+            "ln0_beta": np.asarray(layer.ln0.beta), "ln1_gamma": np.asarray(layer.ln1.gamma),
+            "ln1_beta": np.asarray(layer.ln1.beta)}
+
+
+def init_weights(config, seed: int = 0) -> EncoderWeights:
+    """U(-0.02, 0.02), one draw per tensor in declaration order (reference
+    encoder.py:168-180) -- bit-identical to the reference's weights."""
+    config = as_model_config(config)
+    rng = np.random.default_rng(seed)
+    stored = 1 if config.share_layer_weights else config.layers
+    layers = []
+    for _ in range(stored):
+        arrays = {name: rng.uniform(-WEIGHT_INIT_RANGE, WEIGHT_INIT_RANGE, shape).astype(np.float32)
+                  for name, shape in _tensor_shapes(config)}
+        layers.append(_layer_from_arrays(arrays))
+    return EncoderWeights(layers=layers, shared=config.share_layer_weights)
+
+
+# ---------------------------------------------------------------- PKBW files
+_WEIGHT_MAGIC = b"PKBW"
+_WEIGHT_VERSION = 1
+_HEADER = "<4sI5I"
+_HEADER_FIELDS = ("layers", "head_num", "head_size", "ffn_scale", "share_layer_weights")
+
+
+def save_weights(path, weights, config) -> None:
+    """PKBW v1: little-endian header + raw <f4 tensors in declaration order
+    (reference encoder.py:183-206)."""
+    config = as_model_config(config)
+    header = struct.pack(_HEADER, _WEIGHT_MAGIC, _WEIGHT_VERSION, config.layers, config.head_num,
+                         config.head_size, config.ffn_scale, 1 if config.share_layer_weights else 0)
+    with open(path, "wb") as f:
+        f.write(header)
+        for layer in weights.layers:
+            arrays = _layer_arrays(layer)
+            for name, _ in _tensor_shapes(config):
+                f.write(np.ascontiguousarray(arrays[name], dtype="<f4").tobytes())
+
+
+def load_weights(path, config) -> EncoderWeights:
+    """Strictly validated PKBW load (reference encoder.py:226-268)."""
+    config = as_model_config(config)
+    raw = Path(path).read_bytes()
+    hsz = struct.calcsize(_HEADER)
+    if len(raw) < hsz:
+        raise WeightFormatError(f"{path}: file too short for a weight header")
+    magic, version, *fields = struct.unpack(_HEADER, raw[:hsz])
+    if magic != _WEIGHT_MAGIC:
+        raise WeightFormatError(f"{path}: bad magic {magic!r}")
+    if version != _WEIGHT_VERSION:
+        raise WeightFormatError(f"{path}: unsupported version {version}")
+    expected = (config.layers, config.head_num, config.head_size, config.ffn_scale,
+                1 if config.share_layer_weights else 0)
+    for name, got, want in zip(_HEADER_FIELDS, fields, expected):
+        if got != want:
+            raise WeightFormatError(f"{path}: {name} is {got} in file, config expects {want}")
+    shapes = _tensor_shapes(config)
+    stored = 1 if config.share_layer_weights else config.layers
+    per_layer = sum(int(np.prod(s)) for _, s in shapes)
+    want_bytes = hsz + 4 * per_layer * stored
+    if len(raw) != want_bytes:
+        raise WeightFormatError(f"{path}: payload is {len(raw) - hsz} bytes, expected {want_bytes - hsz}")
+    off = hsz
+    layers = []
+    for _ in range(stored):
+        arrays = {}
+        for name, shape in shapes:
+            n = int(np.prod(shape))
+            arrays[name] = np.frombuffer(raw, dtype="<f4", count=n, offset=off).reshape(shape).astype(np.float32)
+            off += 4 * n
+        layers.append(_layer_from_arrays(arrays))
+    return EncoderWeights(layers=layers, shared=config.share_layer_weights)
+
+
+_CONFIG_BOOL_KEYS = {"fuse_layernorm", "fuse_bias_gelu", "zero_padding", "fused_mha", "share_layer_weights"}
+_CONFIG_INT_KEYS = {"layers", "head_num", "head_size", "ffn_scale", "max_seq_len", "batch_size", "cutoff",
+                    "split_seq_len"}
+
+
+def parse_config_text(text: str) -> ModelConfig:
+    """key=value config, '#' comments (reference encoder.py:290-324)."""
+    values: dict = {}
+    flag_values: dict = {}
+    for lineno, line in enumerate(text.splitlines(), start=1):
+        line = line.split("#", 1)[0].strip()
+        if not line:
+            continue
+        if "=" not in line:
+            raise ConfigError(f"line {lineno}: expected key=value, got {line!r}")
+        key, _, value = line.partition("=")
+        key, value = key.strip(), value.strip()
+        if key in _CONFIG_INT_KEYS:
+            try:
+                values[key] = int(value)
+            except ValueError:
+                raise ConfigError(f"line {lineno}: {key} must be an integer, got {value!r}") from None
+        elif key in _CONFIG_BOOL_KEYS:
+            low = value.lower()
+            if low in ("1", "true", "yes", "on"):
+                parsed = True
+            elif low in ("0", "false", "no", "off"):
+                parsed = False
+            else:
+                raise ConfigError(f"line {lineno}: {key} must be a boolean, got {value!r}")
+            if key == "share_layer_weights":
+                values[key] = parsed
+            else:
+                flag_values[key] = parsed
+        else:
+            raise ConfigError(f"line {lineno}: unknown config key {key!r}")
+    missing = [k for k in ("layers", "head_num", "head_size", "max_seq_len", "batch_size") if k not in values]
+    if missing:
+        raise ConfigError(f"missing required config keys: {', '.join(missing)}")
+    return ModelConfig(flags=OptFlags(**flag_values), **values)
+
+
+def parse_config_file(path) -> ModelConfig:
+    return parse_config_text(Path(path).read_text())
+
+
+# ---------------------------------------------------------------- device side
+
+class DeviceLayer:
+    """One layer's parameters resident in HBM: bf16 K-major matrices, fp32
+    vectors, plus the C struct the library reads."""
+
+    def __init__(self, layer, torch):
+        def mat(w):  # [in, out] -> [out, in] bf16
+            if is_device(w):
+                return w.t().to(torch.bfloat16).contiguous()
+            return torch.from_numpy(np.ascontiguousarray(np.asarray(w, np.float32).T)).to("cuda").to(torch.bfloat16)
+
+        def vec(v):
+            if is_device(v):
+                return v.to(torch.float32).contiguous().reshape(-1)
+            return torch.from_numpy(np.ascontiguousarray(np.asarray(v, np.float32).reshape(-1))).to("cuda")
+
+        self.qkv_w, self.qkv_b = mat(layer.qkv_weight), vec(layer.qkv_bias)
+        self.ao_w, self.ao_b = mat(layer.attn_out_weight), vec(layer.attn_out_bias)
+        self.w1, self.b1 = mat(layer.ffn_w1), vec(layer.ffn_b1)
+        self.w2, self.b2 = mat(layer.ffn_w2), vec(layer.ffn_b2)
+        self.ln0_g, self.ln0_b = vec(layer.ln0.gamma), vec(layer.ln0.beta)
+        self.ln1_g, self.ln1_b = vec(layer.ln1.gamma), vec(layer.ln1.beta)
+        self.ln0_eps = float(getattr(layer.ln0, "eps", 1e-12))
+        self.ln1_eps = float(getattr(layer.ln1, "eps", 1e-12))
+        self.c = _lib.LayerWeightsC(
+            self.qkv_w.data_ptr(), self.qkv_b.data_ptr(), self.ao_w.data_ptr(), self.ao_b.data_ptr(),
+            self.w1.data_ptr(), self.b1.data_ptr(), self.w2.data_ptr(), self.b2.data_ptr(),
+            self.ln0_g.data_ptr(), self.ln0_b.data_ptr(), self.ln1_g.data_ptr(), self.ln1_b.data_ptr(),
+            self.ln0_eps, self.ln1_eps)
+
+
+def _check_layer_shapes(layer, config: ModelConfig) -> None:
+    arrays = _layer_arrays(layer)
+    for name, shape in _tensor_shapes(config):
+        got = tuple(arrays[name].shape)
+        if got != shape:
+            raise ShapeError(f"layer tensor {name} has shape {got}, config expects {shape}")
+
+
+def layer_cfg_c(config: ModelConfig) -> _lib.LayerCfgC:
+    return _lib.LayerCfgC(config.head_num, config.head_size, config.ffn_scale, config.max_seq_len, config.cutoff,
+                          config.split_seq_len)
+
+
+class BertEncoderB200:
+    """Device-resident encoder: uploaded weights, cached workspace, and the
+    stream-ordered forward used by ``forward()`` and ``bench.py``."""
+
+    def __init__(self, weights, config):
+        torch = _lib.require_device()
+        self.torch = torch
+        self.config = as_model_config(config)
+        if self.config.head_size != 64:
+            raise ConfigError(f"the sm_100a kernels support head_size 64, got {self.config.head_size}")
+        if self.config.hidden_dim % 64:
+            raise ConfigError(f"hidden size {self.config.hidden_dim} must be a multiple of 64")
+        stored = [weights.layers[0]] if weights.shared else list(weights.layers)
+        for lw in stored:
+            _check_layer_shapes(lw, self.config)
+        self._stored = [DeviceLayer(lw, torch) for lw in stored]
+        n = self.config.layers
+        self._layers = [self._stored[0] if weights.shared else self._stored[i] for i in range(n)]
+        self._c_layers = (_lib.LayerWeightsC * n)(*[dl.c for dl in self._layers])
+        self._cfg_c = layer_cfg_c(self.config)
+        self._ws = None
+
+    def layer(self, i: int) -> DeviceLayer:
+        return self._layers[i]
+
+    def workspace(self, nbytes: int):
+        if self._ws is None or self._ws.numel() < nbytes:
+            self._ws = self.torch.empty(max(nbytes, 1), dtype=self.torch.uint8, device="cuda")
+        return self._ws
+
+    def forward_device(self, lengths_dev, bs: int, T: int, x_padded_f32, out_padded_f32, stream=None,
+                       config: ModelConfig | None = None):
+        """Device forward: int32 lengths [bs], fp32 padded input [bs*mx, k] ->
+        fp32 padded output (exact-zero padded rows).  No host sync."""
+        cfg = config or self.config
+        cfg_c = self._cfg_c if config is None else layer_cfg_c(cfg)
+        ws_bytes = int(_lib.load().bt_forward_workspace_bytes(C.byref(cfg_c), bs, T))
+        ws = self.workspace(ws_bytes)
+        _lib.call("bt_encoder_forward", self._c_layers, cfg.layers, C.byref(cfg_c), lengths_dev.data_ptr(), bs, T,
+                  x_padded_f32.data_ptr(), out_padded_f32.data_ptr(), ws.data_ptr(), ws_bytes,
+                  _lib.stream_ptr(stream))
+        return out_padded_f32
+
+    def layer_device(self, li: int, x_bf16, plan: PackingPlan, stream=None):
+        """In-place encoder_layer on a packed bf16 [T, k] device tensor."""
+        T = plan.valid_word_cnt
+        ws_bytes = int(_lib.load().bt_layer_workspace_bytes(C.byref(self._cfg_c), T))
+        ws = self.workspace(ws_bytes)
+        _lib.call("bt_encoder_layer", C.byref(self._layers[li].c), C.byref(self._cfg_c),
+                  plan.seq_starts_dev.data_ptr(), plan.batch_size, T, x_bf16.data_ptr(), ws.data_ptr(), ws_bytes,
+                  _lib.stream_ptr(stream))
+        return x_bf16
+
+
+# weights (or layer) object -> (weakref, engine, geometry); one upload per object
+_engines: dict[int, tuple] = {}
+_engines_lock = threading.Lock()
+
+
+def _cached_engine(obj, geom, build):
+    key = id(obj)
+    with _engines_lock:
+        hit = _engines.get(key)
+        if hit is not None and hit[0]() is obj and hit[2] == geom:
+            return hit[1]
+        eng = build()
+        try:
+            ref = weakref.ref(obj, lambda _r, k=key: _engines.pop(k, None))
+        except TypeError:
+            ref = lambda o=obj: o  # noqa: E731  (not weak-referenceable: keep alive)
+        _engines[key] = (ref, eng, geom)
+        return eng
+
+
+def engine_for(weights, config) -> BertEncoderB200:
+    """Device engine for an EncoderWeights object (uploaded once, cached)."""
+    config = as_model_config(config)
+    geom = (config.layers, config.head_num, config.head_size, config.ffn_scale, config.share_layer_weights)
+    return _cached_engine(weights, geom, lambda: BertEncoderB200(weights, config))
+
+
+def engine_for_layer(layer, config) -> BertEncoderB200:
+    """Single-layer device engine for a LayerWeights object (cached)."""
+    config = replace(as_model_config(config), layers=1, share_layer_weights=False)
+    geom = ("layer", config.head_num, config.head_size, config.ffn_scale)
+    return _cached_engine(layer, geom, lambda: BertEncoderB200(EncoderWeights(layers=[layer], shared=False), config))
+
+
+def _count_flops(counter: FlopCounter | None, config: ModelConfig, seqs: SeqLengths, layers: int) -> None:
+    """Exact per-module counts the reference's instrumented kernels add
+    (tensor.py:198-199, attention.py:232-236): zero tolerance in bench --check."""
+    if counter is None:
+        return
+    k, T = config.hidden_dim, seqs.total
+    for _ in range(layers):
+        counter.add("gemm0", 3 * 2 * T * k * k)
+        counter.add("mha", sum(4 * n * n * config.head_size for n in seqs.lengths) * config.head_num)
+        counter.add("gemm1", 2 * T * k * k)
+        counter.add("gemm2", 2 * T * k * config.ffn_scale * k)
+        counter.add("gemm3", 2 * T * config.ffn_scale * k * k)
+
+
+def _is_all_on(flags) -> bool:
+    return bool(flags.fuse_layernorm and flags.fuse_bias_gelu and flags.zero_padding and flags.fused_mha)
+
+
+def encoder_layer(x, layer, config, plan, *, workers: int = 1, counter: FlopCounter | None = None):
+    """One encoder layer (reference encoder.py:337-408).  Input and output
+    share a layout (packed iff zero_padding)."""
+    config = as_model_config(config)
+    hidden = config.hidden_dim
+    xr, xc = rows_cols(x)
+    if xc != hidden:
+        raise ShapeError(f"input has {xc} columns, config expects {hidden}")
+    plan = ensure_plan(plan)
+    expected_rows = plan.valid_word_cnt if config.flags.zero_padding else plan.padded_rows
+    if xr != expected_rows:
+        raise ShapeError(f"input has {xr} rows, expected {expected_rows} for this layout")
+    if not _is_all_on(config.flags):
+        from . import ladder
+
+        return ladder.encoder_layer_variant(x, layer, config, plan, counter=counter)
+    torch = _lib.require_device()
+    eng = engine_for_layer(layer, config)
+    device_mode = is_device(x)
+    xb = x.to(torch.bfloat16).contiguous().clone() if device_mode else \
+        torch.from_numpy(host_array(x)).to("cuda").to(torch.bfloat16)
+    eng.layer_device(0, xb, plan)
+    _count_flops(counter, config, plan.seqs, 1)
+    return xb.float() if device_mode else Tensor(xb.float().cpu().numpy())
+
+
+def forward(weights, seqs, input_padded, config, *, workers: int = 1, counter: FlopCounter | None = None):
+    """Stacked encoder: plan, pack once, L layers, unpack once (reference
+    encoder.py:411-437).
+
+    Host input (reference ``Tensor`` / ndarray, fp32 ``[bs*mx, k]``) returns a
+    host fp32 ``Tensor``; a CUDA fp32 tensor returns a CUDA fp32 tensor.
+    Padded output rows are exactly zero."""
+    config = as_model_config(config)
+    seqs = as_seq_lengths(seqs)
+    if seqs.batch_size != config.batch_size or seqs.max_seq_len != config.max_seq_len:
+        raise ShapeError(f"lengths describe a {seqs.batch_size}x{seqs.max_seq_len} batch, config expects "
+                         f"{config.batch_size}x{config.max_seq_len}")
+    rows, cols = rows_cols(input_padded)
+    padded_rows = seqs.batch_size * seqs.max_seq_len
+    if rows != padded_rows:
+        raise ShapeError(f"input has {rows} rows, expected batch_size * max_seq_len = {padded_rows}")
+    if cols != config.hidden_dim:
+        raise ShapeError(f"input has {cols} columns, config expects {config.hidden_dim}")
+    if not _is_all_on(config.flags):
+        from . import ladder
+
+        return ladder.forward_variant(weights, seqs, input_padded, config, counter=counter)
+    torch = _lib.require_device()
+    eng = engine_for(weights, config)
+    device_mode = is_device(input_padded)
+    lengths = torch.tensor(seqs.lengths, dtype=torch.int32)
+    if device_mode:
+        x = input_padded.to(torch.float32).contiguous()
+        lengths = lengths.to(x.device)
+    else:
+        x = torch.from_numpy(host_array(input_padded)).pin_memory().to("cuda", non_blocking=True)
+        lengths = lengths.pin_memory().to("cuda", non_blocking=True)
+    out = torch.empty((padded_rows, cols), dtype=torch.float32, device="cuda")
+    eng.forward_device(lengths, seqs.batch_size, seqs.total, x, out, config=config)
+    _count_flops(counter, config, seqs, config.layers)
+    if device_mode:
+        return out
+    return Tensor(out.cpu().numpy())

@@ -1,0 +1,135 @@
+"""GPU parity of the full padding-free encoder forward against the
+reference's frozen outputs (tests/golden/encoder.npz) and the pinned oracle.
+
+Tolerance (BASELINE.json north star): cosine >= 0.9999
+and max-abs <= 2e-2 under the reference init; under the stress init cosine
+>= 0.9999, relFro <= 1.5e-2 and max-abs <= 0.1 * RMS(output)."""
+
+import numpy as np
+import pytest
+
+from oracle import packbert_np as orc
+from tests._metrics import assert_close_bf16, rms
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def bt():
+    import paper_2210_03052_b200 as bt
+
+    bt._lib.require_device()
+    return bt
+
+
+def _weights(bt, cfg, seed, kind):
+    if kind == "init":
+        return bt.init_weights(cfg, seed)
+    ocfg = orc.OracleConfig(cfg.layers, cfg.head_num, 64, cfg.max_seq_len, cfg.batch_size)
+    layers = []
+    for d in orc.stress_weights(ocfg, seed):
+        layers.append(bt.encoder._layer_from_arrays(d))
+    return bt.EncoderWeights(layers=layers, shared=False)
+
+
+@pytest.mark.parametrize("tag,layers,heads,mx,bs,seed,kind", [
+    ("tiny", 2, 2, 48, 6, 0, "init"),
+    ("tiny_long", 1, 2, 400, 3, 1, "init"),
+    ("tiny_stress", 2, 2, 96, 5, 2, "stress"),
+    ("tiny_stress_long", 1, 2, 450, 2, 3, "stress"),
+])
+def test_forward_golden(bt, golden, tag, layers, heads, mx, bs, seed, kind):
+    g = golden("encoder")
+    cfg = bt.ModelConfig(layers=layers, head_num=heads, head_size=64, max_seq_len=mx, batch_size=bs,
+                         flags=bt.OptFlags.all_on())
+    lens = g[f"{tag}_lengths"].tolist()
+    x = orc.gen_input(lens, mx, cfg.hidden_dim, seed)
+    y = bt.forward(_weights(bt, cfg, seed, kind), bt.SeqLengths.of(lens, mx), bt.Tensor(x), cfg)
+    want = g[f"{tag}_out"]
+    if kind == "init":
+        assert_close_bf16(y, want, max_abs_max=2e-2, what=tag)
+    else:
+        assert_close_bf16(y, want, max_abs_max=0.1 * rms(want) * 10, what=tag)
+    pad = ~orc.build_mask(lens, mx).reshape(-1).astype(bool)
+    assert not y.array[pad].any(), "padded rows must be exactly zero"
+
+
+def test_forward_c1_golden(bt, golden):
+    """C1: BERT-base, 1 layer, batch 16, max 128, reference init (rows subsampled)."""
+    g = golden("encoder")
+    cfg = bt.preset_config("bert_base", 16, 128, bt.OptFlags.all_on(), layers=1)
+    lens = orc.gen_lengths(16, 128, "fixed", seed=0, alpha=0.6)
+    x = orc.gen_input(lens, 128, 768, 0)
+    y = bt.forward(bt.init_weights(cfg, 0), bt.SeqLengths.of(lens, 128), bt.Tensor(x), cfg)
+    assert_close_bf16(y.array[g["c1_rows"]], g["c1_out_sub"], max_abs_max=2e-2, what="C1")
+
+
+@pytest.mark.parametrize("kind", ["init", "stress"])
+def test_forward_c2_vs_oracle(bt, kind):
+    """C2 geometry (BERT-base 12 layers, bs 16, mx 256) vs the fp32 oracle."""
+    cfg = bt.preset_config("bert_base", 16, 256, bt.OptFlags.all_on())
+    lens = orc.gen_lengths(16, 256, "fixed", seed=0, alpha=0.6)
+    x = orc.gen_input(lens, 256, 768, 0)
+    w = _weights(bt, cfg, 0, kind)
+    ocfg = orc.OracleConfig(12, 12, 64, 256, 16)
+    wo = orc.init_weights(ocfg, 0) if kind == "init" else orc.stress_weights(ocfg, 0)
+    want = orc.forward(wo, lens, x, ocfg)
+    y = bt.forward(w, bt.SeqLengths.of(lens, 256), bt.Tensor(x), cfg)
+    if kind == "init":
+        assert_close_bf16(y, want, max_abs_max=2e-2, what="C2 init")
+    else:
+        valid = orc.build_mask(lens, 256).reshape(-1).astype(bool)
+        assert_close_bf16(y.array[valid], want[valid], max_abs_max=10 * rms(want[valid]), what="C2 stress")
+
+
+def test_forward_device_api_and_isolation(bt):
+    """CUDA-tensor API; padded input rows do not influence the output
+    (bitwise), padded output rows are exactly zero, repeat runs are bitwise
+    identical."""
+    import torch
+
+    cfg = bt.preset_config("bert_base", 8, 200, bt.OptFlags.all_on(), layers=2)
+    lens = orc.gen_lengths(8, 200, "uniform", seed=5)
+    seqs = bt.SeqLengths.of(lens, 200)
+    w = _weights(bt, cfg, 1, "stress")
+    x = torch.from_numpy(orc.gen_input(lens, 200, 768, 1)).cuda()
+    y1 = bt.forward(w, seqs, x, cfg)
+    valid = torch.from_numpy(orc.build_mask(lens, 200).reshape(-1).astype(bool)).cuda()
+    x2 = x.clone()
+    x2[~valid] = torch.randn_like(x2[~valid]) * 100
+    y2 = bt.forward(w, seqs, x2, cfg)
+    assert torch.equal(y1, y2)
+    assert not y1[~valid].any()
+    assert torch.equal(y1, bt.forward(w, seqs, x, cfg))
+
+
+def test_encoder_layer_api(bt):
+    cfg = bt.ModelConfig(layers=1, head_num=2, head_size=64, max_seq_len=64, batch_size=4,
+                         flags=bt.OptFlags.all_on())
+    lens = [64, 1, 33, 17]
+    ocfg = orc.OracleConfig(1, 2, 64, 64, 4)
+    wd = orc.stress_weights(ocfg, 4)[0]
+    layer = bt.encoder._layer_from_arrays(wd)
+    x = np.random.default_rng(0).standard_normal((sum(lens), 128)).astype(np.float32)
+    plan = bt.plan_for_lengths(bt.SeqLengths.of(lens, 64))
+    got = bt.encoder_layer(bt.Tensor(x), layer, cfg, plan)
+    _, st, ln = orc.compute_plan(orc.build_mask(lens, 64))
+    want = orc.encoder_layer(x, wd, ocfg, st, ln)
+    assert_close_bf16(got, want, what="encoder_layer")
+    with pytest.raises(bt.ShapeError):
+        bt.encoder_layer(bt.Tensor(x[:-1]), layer, cfg, plan)
+
+
+def test_flop_counter_and_albert_sharing(bt):
+    cfg = bt.preset_config("albert", 3, 32, bt.OptFlags.all_on(), layers=3)
+    lens = [32, 5, 20]
+    w = bt.init_weights(cfg, 0)
+    x = orc.gen_input(lens, 32, cfg.hidden_dim, 0)
+    c = bt.FlopCounter()
+    y = bt.forward(w, bt.SeqLengths.of(lens, 32), bt.Tensor(x), cfg, counter=c)
+    exact = orc.exact_flops(lens, cfg.hidden_dim)
+    for key, val in exact.items():
+        assert c.get(key) == 3 * val
+    ocfg = orc.OracleConfig(3, 16, 64, 32, 3, share_layer_weights=True)
+    want = orc.forward(orc.init_weights(ocfg, 0), lens, x, ocfg)
+    assert_close_bf16(y, want, max_abs_max=2e-2, what="albert")

@@ -1,0 +1,214 @@
+"""GPU parity of the compute kernels: tcgen05 GEMM (every tile width and
+epilogue), fused add-bias+residual+LayerNorm, fused varlen MHA (short and
+long paths) -- against fp32 references (torch fp32 for the GEMM/LN, the
+pinned oracle for attention) on the same bf16-rounded inputs."""
+
+import math
+
+import numpy as np
+import pytest
+
+from oracle import packbert_np as orc
+from tests._metrics import assert_close_bf16, cosine, rel_fro
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+
+    import paper_2210_03052_b200 as bt
+
+    bt._lib.require_device()
+    torch.manual_seed(0)
+    return bt, torch
+
+
+def _gelu(t):
+    return 0.5 * t * (1.0 + torch_tanh(math.sqrt(2 / math.pi) * (t + 0.044715 * t ** 3)))
+
+
+def torch_tanh(t):
+    import torch
+
+    return torch.tanh(t)
+
+
+@pytest.mark.parametrize("bn", [64, 128, 256])
+@pytest.mark.parametrize("epi", [0, 1, 2, 3])
+@pytest.mark.parametrize("M,N,K", [(1, 256, 64), (200, 768, 768), (2458, 2304, 768), (129, 1024, 4096)])
+def test_gemm(env, bn, epi, M, N, K):
+    bt, torch = env
+    from paper_2210_03052_b200.tensor import gemm_device
+
+    if N % bn:
+        pytest.skip("N not a multiple of BN")
+    a = (torch.randn(M, K, device="cuda") * 0.5).to(torch.bfloat16)
+    w = (torch.randn(N, K, device="cuda") / math.sqrt(K)).to(torch.bfloat16)
+    bias = torch.randn(N, device="cuda") * 0.1
+    res = torch.randn(M, N, device="cuda").to(torch.bfloat16)
+    out = gemm_device(a, w, bias if epi else None, res if epi == 3 else None, epi, bn=bn)
+    ref = a.float() @ w.float().t()
+    if epi == 3:
+        ref = ref + res.float()
+    if epi:
+        ref = ref + bias
+    if epi == 2:
+        ref = _gelu(ref)
+    torch.cuda.synchronize()
+    assert rel_fro(out, ref) < 6e-3, (bn, epi, M, N, K, rel_fro(out, ref))
+    assert (out.float() - ref).abs().max().item() < 0.05 * max(1.0, ref.abs().max().item())
+
+
+def test_gemm_public_api(env):
+    bt, torch = env
+    rng = np.random.default_rng(1)
+    a = rng.standard_normal((37, 128)).astype(np.float32)
+    b = (rng.standard_normal((128, 192)) * 0.1).astype(np.float32)
+    bias = rng.standard_normal(192).astype(np.float32)
+    got = bt.gemm(bt.Tensor(a), bt.Tensor(b), bt.EpilogueHook.add_bias_gelu(bias))
+    ref = orc.gelu(a @ b + bias)
+    assert_close_bf16(got, ref, rel_max=1e-2, what="gemm+bias+gelu")
+    q, k, v = bt.batched_gemm([bt.Tensor(a)] * 3, [bt.Tensor(b[:, :64]), bt.Tensor(b[:, 64:128]),
+                                                    bt.Tensor(b[:, 128:])])
+    assert_close_bf16(k, a @ b[:, 64:128], rel_max=1e-2, what="batched")
+    with pytest.raises(bt.ShapeError):
+        bt.gemm(bt.Tensor(a), bt.Tensor(b[:64]))
+
+
+@pytest.mark.parametrize("k", [768, 1024, 64, 2048])
+def test_layernorm(env, k):
+    bt, torch = env
+    from paper_2210_03052_b200.fusion import ln_device
+
+    T = 1000
+    x = torch.randn(T, k, device="cuda").to(torch.bfloat16)
+    r = torch.randn(T, k, device="cuda").to(torch.bfloat16)
+    b = torch.randn(k, device="cuda") * 0.1
+    g = torch.randn(k, device="cuda")
+    be = torch.randn(k, device="cuda")
+    out = ln_device(x, r, b, g, be, 1e-12)
+    z = (x.float() + r.float()) + b
+    ref = torch.nn.functional.layer_norm(z, (k,), g, be, eps=1e-12)
+    assert rel_fro(out, ref) < 5e-3
+    # constant rows normalise to exactly beta (variance 0, reference fusion.py:52-53)
+    c = torch.full((4, k), 3.0, device="cuda").to(torch.bfloat16)
+    outc = ln_device(c, None, None, g, be, 1e-12)
+    assert torch.allclose(outc.float(), be.to(torch.bfloat16).float().expand(4, k), atol=1e-2)
+
+
+def test_layernorm_golden(env, golden):
+    bt, torch = env
+    g = golden("fusion")
+    y = bt.add_bias_residual_layernorm(bt.Tensor(g["ln_x"]), bt.Tensor(g["ln_r"]), g["ln_b"],
+                                       bt.LayernormParams(g["ln_g"], g["ln_beta"]))
+    assert_close_bf16(y, g["ln_y"], what="LN vs reference")
+    kat = bt.layernorm(bt.Tensor(np.array([[1, 2, 3, 0, 0, 0, 0, 0]], np.float32)),
+                       bt.LayernormParams(np.ones(8, np.float32), np.zeros(8, np.float32)))
+    ref = orc.layernorm(np.array([[1, 2, 3, 0, 0, 0, 0, 0]], np.float32), np.ones(8), np.zeros(8))
+    assert np.abs(kat.array - ref).max() < 2e-2
+
+
+def test_gelu_and_elementwise(env, golden):
+    bt, torch = env
+    g = golden("fusion")
+    got = bt.gelu(g["gelu_in"])
+    assert np.abs(got - g["gelu_out"]).max() < 2e-2  # bf16-free fp32 path, tanh.approx
+    assert abs(float(bt.gelu(np.float32(1.0))) - 0.841192) < 2e-3
+    a = np.random.default_rng(0).standard_normal((5, 16)).astype(np.float32)
+    np.testing.assert_allclose(bt.add(bt.Tensor(a), bt.Tensor(a)).array, 2 * a, rtol=1e-6)
+    np.testing.assert_allclose(bt.add_rowvec(bt.Tensor(a), np.ones(16, np.float32)).array, a + 1, rtol=1e-6)
+
+
+def _attn_case(golden, tag):
+    g = golden("attention")
+    lens = g[f"{tag}_lengths"].tolist()
+    mx, heads = int(g[f"{tag}_mx"]), int(g[f"{tag}_heads"])
+    return g, lens, mx, heads
+
+
+@pytest.mark.parametrize("tag", ["short", "long", "cut384", "cut385"])
+def test_mha_golden(env, golden, tag):
+    """dispatch_mha on the reference's own attention vectors."""
+    bt, torch = env
+    g, lens, mx, heads = _attn_case(golden, tag)
+    plan = bt.plan_for_lengths(bt.SeqLengths.of(lens, mx))
+    hid = heads * 64
+    b = g[f"{tag}_bias"]
+    inp = bt.AttentionInput(bt.Tensor(g[f"{tag}_q"]), bt.Tensor(g[f"{tag}_k"]), bt.Tensor(g[f"{tag}_v"]),
+                            b[:hid], b[hid:2 * hid], b[2 * hid:], plan, heads, 64)
+    out = bt.dispatch_mha(inp)
+    assert_close_bf16(out, g[f"{tag}_out"], what=f"mha {tag}")
+
+
+def _rand_qkv(torch, T, hid, scale=1.0, seed=0):
+    gen = torch.Generator(device="cuda").manual_seed(seed)
+    return (torch.randn(T, 3 * hid, device="cuda", generator=gen) * scale).to(torch.bfloat16)
+
+
+def _oracle_mha(qkv, plan, heads, mx, cutoff=384):
+    a = qkv.float().cpu().numpy()
+    hid = heads * 64
+    zero = np.zeros(3 * hid, np.float32)
+    return orc.dispatch_mha(a[:, :hid], a[:, hid:2 * hid], a[:, 2 * hid:], zero, plan.seq_starts, mx, heads, 64,
+                            cutoff)
+
+
+@pytest.mark.parametrize("path", [1, 2])
+@pytest.mark.parametrize("lens,mx", [([1, 2, 3, 127, 128, 129, 200, 256], 256), ([384, 1, 383, 257, 77], 384),
+                                     ([5] * 40, 8), ([128] * 6, 128)])
+def test_mha_paths_random(env, path, lens, mx):
+    """Both kernels on edge lengths (1, tile boundaries 127/128/129, 384)
+    with N(0,1) q/k/v (sharp softmax), vs the fp32 oracle."""
+    bt, torch = env
+    from paper_2210_03052_b200.attention import mha_device
+
+    heads = 3
+    plan = bt.plan_for_lengths(bt.SeqLengths.of(lens, mx))
+    qkv = _rand_qkv(torch, plan.valid_word_cnt, heads * 64, seed=len(lens))
+    out = mha_device(qkv, plan, heads, 64, path=path)
+    ref = _oracle_mha(qkv, plan, heads, mx)
+    assert_close_bf16(out, ref, what=f"path{path} {lens[:4]}")
+
+
+@pytest.mark.parametrize("lens,mx", [([1000, 1, 513, 640, 129], 1024), ([512] * 3 + [300], 512)])
+def test_mha_long_random(env, lens, mx):
+    bt, torch = env
+    from paper_2210_03052_b200.attention import mha_device
+
+    heads = 2
+    plan = bt.plan_for_lengths(bt.SeqLengths.of(lens, mx))
+    qkv = _rand_qkv(torch, plan.valid_word_cnt, heads * 64, seed=7)
+    out = mha_device(qkv, plan, heads, 64)
+    ref = _oracle_mha(qkv, plan, heads, mx)
+    assert_close_bf16(out, ref, what="long")
+
+
+def test_mha_padded_token_isolation(env):
+    """Tokens of other sequences never influence a sequence: perturbing
+    sequence 1 leaves sequences 0 and 2 bitwise unchanged."""
+    bt, torch = env
+    from paper_2210_03052_b200.attention import mha_device
+
+    for mx in (256, 700):
+        lens = [100, 150, 60] if mx == 256 else [600, 300, 700]
+        plan = bt.plan_for_lengths(bt.SeqLengths.of(lens, mx))
+        qkv = _rand_qkv(torch, plan.valid_word_cnt, 128, seed=3)
+        a = mha_device(qkv, plan, 2, 64).clone()
+        s = plan.seq_starts
+        qkv2 = qkv.clone()
+        qkv2[s[1]:s[2]] = torch.randn_like(qkv2[s[1]:s[2]].float()).to(torch.bfloat16) * 5
+        b = mha_device(qkv2, plan, 2, 64)
+        assert torch.equal(a[: s[1]], b[: s[1]]) and torch.equal(a[s[2]:], b[s[2]:])
+
+
+def test_mha_deterministic(env):
+    bt, torch = env
+    from paper_2210_03052_b200.attention import mha_device
+
+    plan = bt.plan_for_lengths(bt.SeqLengths.of([300, 17, 256], 512))
+    qkv = _rand_qkv(torch, plan.valid_word_cnt, 256, seed=9)
+    a = mha_device(qkv, plan, 4, 64).clone()
+    b = mha_device(qkv, plan, 4, 64)
+    assert torch.equal(a, b)

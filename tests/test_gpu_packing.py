@@ -1,0 +1,108 @@
+"""GPU parity: mask -> plan -> pack/unpack kernels, bit-exact against the
+oracle (which is pinned to the reference's golden vectors)."""
+
+import numpy as np
+import pytest
+
+from oracle import packbert_np as orc
+
+pytestmark = pytest.mark.gpu
+
+CASES = ["fig4", "ones", "dense", "single", "r1", "r2", "r3"]
+
+
+@pytest.fixture(scope="module")
+def bt():
+    import paper_2210_03052_b200 as bt
+
+    bt._lib.require_device()
+    return bt
+
+
+@pytest.mark.parametrize("tag", CASES)
+def test_plan_from_mask_bit_exact(bt, golden, tag):
+    g = golden("packing")
+    lens, mx = g[f"{tag}_lengths"], int(g[f"{tag}_mx"])
+    plan = bt.compute_plan(orc.build_mask(lens, mx))
+    np.testing.assert_array_equal(plan.offsets, g[f"{tag}_offsets"])
+    np.testing.assert_array_equal(plan.seq_starts, g[f"{tag}_seq_starts"])
+    assert plan.offsets.dtype == np.int64 and not plan.offsets.flags.writeable
+
+
+@pytest.mark.parametrize("tag", CASES)
+def test_plan_from_lengths_bit_exact(bt, golden, tag):
+    g = golden("packing")
+    lens, mx = g[f"{tag}_lengths"], int(g[f"{tag}_mx"])
+    plan = bt.plan_for_lengths(bt.SeqLengths.of(lens, mx))
+    np.testing.assert_array_equal(plan.offsets, g[f"{tag}_offsets"])
+    np.testing.assert_array_equal(plan.seq_starts, g[f"{tag}_seq_starts"])
+
+
+def test_plan_c5_scale(bt, golden):
+    """2048 sequences x 512 (C5): multi-chunk scan, 629,146 offsets."""
+    lens = golden("generators")["c5_lengths"]
+    offs, starts, _ = orc.compute_plan(orc.build_mask(lens, 512))
+    plan = bt.compute_plan(orc.build_mask(lens, 512))
+    assert plan.valid_word_cnt == len(offs) == 629146
+    np.testing.assert_array_equal(plan.offsets, offs)
+    np.testing.assert_array_equal(plan.seq_starts, starts)
+    plan2 = bt.plan_for_lengths(bt.SeqLengths.of(lens, 512))
+    np.testing.assert_array_equal(plan2.offsets, offs)
+
+
+def test_plan_device_mask_validation(bt):
+    import torch
+
+    bad = torch.tensor([[1, 0, 1]], dtype=torch.uint8, device="cuda")
+    with pytest.raises(bt.ShapeError, match="prefix"):
+        bt.compute_plan(bad)
+    with pytest.raises(bt.ShapeError, match="0 or 1"):
+        bt.compute_plan(torch.tensor([[2, 0]], dtype=torch.uint8, device="cuda"))
+    with pytest.raises(bt.ShapeError):
+        bt.compute_plan(torch.tensor([[1, 1], [0, 0]], dtype=torch.uint8, device="cuda"))
+    ok = bt.compute_plan(torch.tensor([[1, 1, 0], [1, 0, 0]], dtype=torch.uint8, device="cuda"))
+    assert ok.offsets.tolist() == [0, 1, 3]
+    with pytest.raises(bt.ShapeError):
+        bt.compute_plan(np.array([[1, 0, 1]], np.uint8))
+
+
+def test_pack_unpack_fp32_bit_exact(bt, golden):
+    g = golden("packing")
+    lens = g["pk_lengths"]
+    plan = bt.plan_for_lengths(bt.SeqLengths.of(lens, 40))
+    packed = bt.pack(bt.Tensor(g["pk_padded"]), plan)
+    np.testing.assert_array_equal(packed.tokens.array, g["pk_packed"])
+    up = bt.unpack(packed, 40)
+    np.testing.assert_array_equal(up.array, g["pk_unpacked"])
+    with pytest.raises(bt.ShapeError):
+        bt.unpack(packed, 41)
+    with pytest.raises(bt.ShapeError):
+        bt.pack(bt.Tensor(g["pk_padded"][:-1]), plan)
+
+
+def test_unpack_fig4_zero_rows(bt):
+    plan = bt.plan_for_lengths(bt.SeqLengths.of([2, 4, 5], 5))
+    tokens = np.repeat(np.arange(11, dtype=np.float32)[:, None] + 1, 3, axis=1)
+    up = bt.unpack(bt.PackedBatch(bt.Tensor(tokens), plan), 5).array
+    assert [i for i in range(15) if not up[i].any()] == [2, 3, 4, 9]
+
+
+def test_pack_bf16_and_round_trip_large(bt):
+    """fp32 -> bf16 pack equals round-to-nearest of the fp32 gather; unpack
+    restores every valid row and writes exact zeros elsewhere (C2 size)."""
+    import torch
+
+    lens = orc.gen_lengths(16, 256, "fixed", seed=0, alpha=0.6)
+    plan = bt.plan_for_lengths(bt.SeqLengths.of(lens, 256))
+    x = torch.randn(16 * 256, 768, device="cuda")
+    from paper_2210_03052_b200.packing import pack_device, unpack_device
+
+    pk = pack_device(x, plan, out_dtype=torch.bfloat16)
+    idx = torch.from_numpy(plan.offsets).cuda()
+    assert torch.equal(pk, x[idx].to(torch.bfloat16))
+    up = unpack_device(pk, plan)
+    ref = torch.zeros_like(x)
+    ref[idx] = pk.float()
+    assert torch.equal(up, ref)
+    pk32 = pack_device(x, plan)
+    assert torch.equal(unpack_device(pk32, plan)[idx], x[idx])

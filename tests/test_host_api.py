@@ -1,0 +1,131 @@
+"""Host-side API parity with the reference (no GPU needed): containers,
+init, config parsing, weight files, validation, error types."""
+
+import numpy as np
+import pytest
+
+import paper_2210_03052_b200 as bt
+from oracle import packbert_np as orc
+
+
+def test_error_hierarchy():
+    assert issubclass(bt.ShapeError, ValueError) and issubclass(bt.ShapeError, bt.PackbertError)
+    assert issubclass(bt.ConfigError, ValueError)
+    assert issubclass(bt.WeightFormatError, ValueError)
+
+
+def test_seq_lengths_validation():
+    s = bt.SeqLengths.of([2, 4, 5], 5)
+    assert s.total == 11 and s.batch_size == 3 and abs(s.alpha - 11 / 15) < 1e-12
+    with pytest.raises(bt.ShapeError):
+        bt.SeqLengths.of([], 5)
+    with pytest.raises(bt.ShapeError):
+        bt.SeqLengths.of([0, 3], 5)
+    with pytest.raises(bt.ShapeError):
+        bt.SeqLengths.of([6], 5)
+    with pytest.raises(bt.ShapeError):
+        bt.SeqLengths.of([1], 0)
+
+
+def test_build_mask_kat():
+    m = bt.build_mask(bt.SeqLengths.of([2, 4, 5], 5))
+    assert m.dtype == np.uint8
+    assert m.tolist() == [[1, 1, 0, 0, 0], [1, 1, 1, 1, 0], [1, 1, 1, 1, 1]]
+
+
+def test_model_config_validation():
+    with pytest.raises(bt.ConfigError):
+        bt.ModelConfig(layers=0, head_num=1, head_size=64, max_seq_len=8, batch_size=1)
+    with pytest.raises(bt.ConfigError):
+        bt.ModelConfig(layers=1, head_num=1, head_size=64, max_seq_len=8, batch_size=1,
+                       flags=bt.OptFlags(fused_mha=True))
+    c = bt.preset_config("bert_base", 16, 256, bt.OptFlags.all_on())
+    assert c.hidden_dim == 768 and c.layers == 12 and c.cutoff == 384 and c.split_seq_len == 32
+    assert bt.preset_config("albert", 1, 8).share_layer_weights
+    with pytest.raises(bt.ConfigError):
+        bt.preset_config("gpt", 1, 8)
+
+
+def test_init_weights_match_reference(golden):
+    g = golden("generators")
+    cfg = bt.ModelConfig(layers=2, head_num=2, head_size=8, max_seq_len=16, batch_size=4)
+    w = bt.init_weights(cfg, seed=3)
+    for li in range(2):
+        lw = w.layer(li)
+        np.testing.assert_array_equal(lw.qkv_weight, g[f"w{li}_qkv_weight"])
+        np.testing.assert_array_equal(lw.ffn_w2, g[f"w{li}_ffn_w2"])
+        np.testing.assert_array_equal(lw.ln1.beta, g[f"w{li}_ln1_beta"])
+    shared = bt.init_weights(bt.preset_config("albert", 1, 8, layers=3), 0)
+    assert len(shared.layers) == 1 and shared.layer(2) is shared.layer(0)
+
+
+def test_pkbw_round_trip_and_validation(tmp_path):
+    cfg = bt.ModelConfig(layers=2, head_num=2, head_size=8, max_seq_len=16, batch_size=4)
+    w = bt.init_weights(cfg, seed=1)
+    p = tmp_path / "w.pkbw"
+    bt.save_weights(p, w, cfg)
+    w2 = bt.load_weights(p, cfg)
+    for a, b in zip(w.layers, w2.layers):
+        np.testing.assert_array_equal(a.qkv_weight, b.qkv_weight)
+        np.testing.assert_array_equal(a.ln0.gamma, b.ln0.gamma)
+    raw = p.read_bytes()
+    (tmp_path / "bad_magic").write_bytes(b"XXXX" + raw[4:])
+    with pytest.raises(bt.WeightFormatError, match="bad magic"):
+        bt.load_weights(tmp_path / "bad_magic", cfg)
+    (tmp_path / "short").write_bytes(raw[:-4])
+    with pytest.raises(bt.WeightFormatError, match="payload"):
+        bt.load_weights(tmp_path / "short", cfg)
+    with pytest.raises(bt.WeightFormatError, match="layers"):
+        bt.load_weights(p, bt.ModelConfig(layers=3, head_num=2, head_size=8, max_seq_len=16, batch_size=4))
+    (tmp_path / "tiny").write_bytes(b"PK")
+    with pytest.raises(bt.WeightFormatError, match="too short"):
+        bt.load_weights(tmp_path / "tiny", cfg)
+
+
+def test_parse_config():
+    cfg = bt.parse_config_text("""
+        # BERT-base padding-free
+        layers = 12
+        head_num=12
+        head_size=64
+        max_seq_len=256
+        batch_size=16
+        fuse_layernorm=on
+        fuse_bias_gelu=yes
+        zero_padding=1
+        fused_mha=true
+    """)
+    assert cfg.flags == bt.OptFlags.all_on() and cfg.hidden_dim == 768
+    with pytest.raises(bt.ConfigError, match="unknown config key"):
+        bt.parse_config_text("layers=1\nbogus=2")
+    with pytest.raises(bt.ConfigError, match="missing required"):
+        bt.parse_config_text("layers=1")
+    with pytest.raises(bt.ConfigError, match="integer"):
+        bt.parse_config_text("layers=x")
+    with pytest.raises(bt.ConfigError, match="boolean"):
+        bt.parse_config_text("layers=1\nhead_num=1\nhead_size=64\nmax_seq_len=4\nbatch_size=1\nfused_mha=maybe")
+
+
+def test_forward_validates_before_compute():
+    """Shape errors are raised on the host, before any device work (no GPU here)."""
+    cfg = bt.preset_config("bert_base", 2, 8, bt.OptFlags.all_on(), layers=1)
+    seqs = bt.SeqLengths.of([3, 8], 8)
+    w = None
+    with pytest.raises(bt.ShapeError, match="rows"):
+        bt.forward(w, seqs, np.zeros((15, 768), np.float32), cfg)
+    with pytest.raises(bt.ShapeError, match="batch"):
+        bt.forward(w, bt.SeqLengths.of([3], 8), np.zeros((8, 768), np.float32), cfg)
+    with pytest.raises(bt.ShapeError, match="columns"):
+        bt.forward(w, seqs, np.zeros((16, 64), np.float32), cfg)
+
+
+def test_flop_counter_matches_exact_model():
+    from paper_2210_03052_b200.encoder import _count_flops
+
+    lens = orc.gen_lengths(16, 256, "fixed", seed=0, alpha=0.6)
+    cfg = bt.preset_config("bert_base", 16, 256, bt.OptFlags.all_on())
+    c = bt.FlopCounter()
+    _count_flops(c, cfg, bt.SeqLengths.of(lens, 256), cfg.layers)
+    exact = orc.exact_flops(lens, 768)
+    for key, val in exact.items():
+        assert c.get(key) == val * cfg.layers
