@@ -481,11 +481,25 @@ def forward(weights, seqs, input_padded, config, *, workers: int = 1, counter: F
         x = input_padded.to(torch.float32).contiguous()
         lengths = lengths.to(x.device)
     else:
-        x = torch.from_numpy(host_array(input_padded)).pin_memory().to("cuda", non_blocking=True)
+        x = _host_to_device_f32(input_padded, torch)
         lengths = lengths.pin_memory().to("cuda", non_blocking=True)
     out = torch.empty((padded_rows, cols), dtype=torch.float32, device="cuda")
     eng.forward_device(lengths, seqs.batch_size, seqs.total, x, out, config=config)
     _count_flops(counter, config, seqs, config.layers)
     if device_mode:
         return out
-    return Tensor(out.cpu().numpy())
+    # pinned host result from torch's caching host allocator (reused across
+    # calls once the caller drops it), async D2H, one sync
+    host = torch.empty((padded_rows, cols), dtype=torch.float32, pin_memory=True)
+    host.copy_(out, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    return Tensor(host.numpy())
+
+
+def _host_to_device_f32(x, torch):
+    """Host fp32 input -> device.  A pinned CPU torch tensor is copied
+    asynchronously as is; ndarrays / Tensors go through a pageable copy."""
+    if type(x).__module__.startswith("torch") and not x.is_cuda:
+        t = x if x.dtype == torch.float32 else x.float()
+        return t.contiguous().to("cuda", non_blocking=t.is_pinned())
+    return torch.from_numpy(host_array(x)).to("cuda")

@@ -1,0 +1,40 @@
+"""Run eager forwards of a bench workload (for ncu launch lists / captures).
+
+    python scripts/profile_forward.py --config c2 --iters 2
+"""
+
+import argparse
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--iters", type=int, default=2)
+    a = ap.parse_args()
+    import torch
+
+    import bench
+    import paper_2210_03052_b200 as bt
+    from paper_2210_03052_b200 import harness
+
+    desc, heads, layers, bs, mx, _ = bench.WORKLOADS[a.config]
+    seqs = harness.gen_lengths(bs, mx, "fixed", seed=0, alpha=0.6)
+    cfg = bt.ModelConfig(layers=layers, head_num=heads, head_size=64, max_seq_len=mx, batch_size=bs,
+                         flags=bt.OptFlags.all_on())
+    eng = bt.BertEncoderB200(bt.init_weights(cfg, 0), cfg)
+    x = torch.from_numpy(harness.gen_input(seqs, heads * 64, 0)).cuda()
+    lengths = torch.tensor(seqs.lengths, dtype=torch.int32, device="cuda")
+    out = torch.empty_like(x)
+    for _ in range(a.iters):
+        eng.forward_device(lengths, bs, seqs.total, x, out)
+    torch.cuda.synchronize()
+    print("done", desc)
+
+
+if __name__ == "__main__":
+    main()

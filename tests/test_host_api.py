@@ -129,3 +129,32 @@ def test_flop_counter_matches_exact_model():
     exact = orc.exact_flops(lens, 768)
     for key, val in exact.items():
         assert c.get(key) == val * cfg.layers
+
+
+def test_harness_generators_match_reference(golden):
+    from paper_2210_03052_b200 import harness
+
+    g = golden("generators")
+    for tag, (bs, mx) in {"c1": (16, 128), "c2": (16, 256), "c3": (16, 512), "c5": (2048, 512)}.items():
+        assert list(harness.gen_lengths(bs, mx, "fixed", seed=0, alpha=0.6).lengths) == g[f"{tag}_lengths"].tolist()
+    assert list(harness.gen_lengths(50, 77, "uniform", seed=4).lengths) == g["uniform_lengths"].tolist()
+    seqs = bt.SeqLengths.of(g["input_lengths"].tolist(), 16)
+    np.testing.assert_array_equal(harness.gen_input(seqs, 32, 2), g["input_x"])
+    lens = g["c2_lengths"].tolist()
+    assert harness.layer_flops(lens, 768) == {k: int(g[f"flops_c2_{k}"]) for k in
+                                              ("gemm0", "mha", "gemm1", "gemm2", "gemm3")}
+
+
+def test_token_balanced_partition():
+    from paper_2210_03052_b200 import harness
+    from paper_2210_03052_b200.partition import imbalance, token_balanced_partition
+
+    lens = harness.gen_lengths(2048, 512, "fixed", seed=0, alpha=0.6).lengths
+    for n in (1, 2, 4, 8):
+        sh = token_balanced_partition(lens, n, 1024)
+        assert sh[0].start == 0 and sh[-1].stop == 2048
+        assert all(a.stop == b.start for a, b in zip(sh, sh[1:]))
+        assert sum(s.tokens for s in sh) == sum(lens)
+        assert imbalance(sh) < 1.01
+    with pytest.raises(ValueError):
+        token_balanced_partition([3, 4], 3)
