@@ -179,12 +179,18 @@ BT_API int bt_encoder_forward(const bt_layer_weights* layers, int n_layers, cons
                        void* ws, size_t ws_bytes, bt_stream_t stream);
 
 /* ---- test hooks (exercise every kernel instantiation) ------------------ */
-/* bt_gemm with a forced tile width bn in {64, 128, 256}. */
+/* bt_gemm with a forced tile: bn in {64,128,256} = one CTA 128 x bn, bn in {-64,-128,-192,-256} = SM pair (cta_group::2) 256 x |bn|. */
 BT_API int bt_gemm_bn(const void* A, const void* Bt, const float* bias, const void* residual, void* C, int M, int N,
                       int K, int epilogue, int bn, bt_stream_t stream);
 /* bt_mha_varlen forcing the short (path = 1, mx <= 384) or long (path = 2) kernel. */
 BT_API int bt_mha_varlen_path(const void* qkv, const int32_t* seq_starts, int bs, int mx, int H, int d, void* out,
                               int T, int path, bt_stream_t stream);
+
+/* Debug hook: per-CTA globaltimer event trace of the GEMM kernels (64 u64
+ * slots per CTA, see csrc/gemm_sm100.cu); NULL turns tracing off. */
+BT_API int bt_debug_gemm_trace(unsigned long long* buf);
+/* Debug hook: 0 normal, 1 = GEMMs skip the MMAs, 2 = GEMMs skip the TMA loads (results invalid in 1/2). */
+BT_API int bt_debug_gemm_mode(int mode);
 
 #ifdef __cplusplus
 }

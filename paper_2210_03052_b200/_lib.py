@@ -66,6 +66,8 @@ SIGNATURES = {
     "bt_bias_act": (_I, [_P, _I, _I, _P, _P, _I, _I, _I, _I, _I, _S]),
     "bt_add": (_I, [_P, _P, _P, _I, C.c_longlong, _S]),
     "bt_gemm_bn": (_I, [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _S]),
+    "bt_debug_gemm_trace": (_I, [_P]),
+    "bt_debug_gemm_mode": (_I, [_I]),
     "bt_mha_varlen_path": (_I, [_P, _P, _I, _I, _I, _I, _P, _I, _I, _S]),
 }
 

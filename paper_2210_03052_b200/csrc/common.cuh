@@ -10,6 +10,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <string>
+#include <utility>
 
 #include "../../include/bt200.h"
 
@@ -26,6 +27,40 @@ inline void count_launch(int n = 1) { g_launches.fetch_add(n, std::memory_order_
 int num_sms();
 
 inline cudaStream_t as_stream(bt_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Programmatic dependent launch (PDL) is on unless BT_PDL=0: every kernel is
+// launched with programmatic stream serialisation, runs its prologue
+// (barrier init, TMEM alloc, descriptor / weight prefetch) while the previous
+// kernel drains, and waits on griddepcontrol.wait before touching activations.
+bool pdl_enabled();
+
+// cudaLaunchKernelEx with the PDL attribute (and an optional cluster size).
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, int cluster_x,
+                          Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  int n = 0;
+  if (cluster_x > 1) {
+    attr[n].id = cudaLaunchAttributeClusterDimension;
+    attr[n].val.clusterDim.x = cluster_x;
+    attr[n].val.clusterDim.y = 1;
+    attr[n].val.clusterDim.z = 1;
+    ++n;
+  }
+  if (pdl_enabled()) {
+    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = n;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 }  // namespace bt
 
@@ -56,6 +91,17 @@ inline cudaStream_t as_stream(bt_stream_t s) { return reinterpret_cast<cudaStrea
       ::bt::set_error("kernel launch failed: %s (%s:%d)", cudaGetErrorString(_e), __FILE__, __LINE__); \
       return BT_ECUDA;                                                                             \
     }                                                                                              \
+  } while (0)
+
+// Launch through bt::launch (PDL attribute), record it, surface errors.
+#define BT_LAUNCH(kern, grid, block, smem, stream, cluster, ...)                                        \
+  do {                                                                                                 \
+    cudaError_t _le = ::bt::launch(kern, grid, block, smem, stream, cluster, __VA_ARGS__);             \
+    if (_le != cudaSuccess) {                                                                          \
+      ::bt::set_error("launch of %s failed: %s (%s:%d)", #kern, cudaGetErrorString(_le), __FILE__, __LINE__); \
+      return BT_ECUDA;                                                                                 \
+    }                                                                                                  \
+    ::bt::count_launch();                                                                              \
   } while (0)
 
 #define BT_TRY(expr)          \

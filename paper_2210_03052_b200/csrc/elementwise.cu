@@ -43,6 +43,8 @@ __device__ __forceinline__ void st8(__nv_bfloat16* p, const float (&v)[8]) {
 template <typename Ti, typename To, bool GELU>
 __global__ void bias_act_kernel(const Ti* __restrict__ x, int ldx, const float* __restrict__ bias, To* __restrict__ out,
                                 int ldo, int rows, int cols) {
+  ptx::griddep_launch_dependents();
+  ptx::griddep_wait();
   const int chunks = cols / 8;
   const long long total = static_cast<long long>(rows) * chunks;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
@@ -67,6 +69,8 @@ __global__ void bias_act_kernel(const Ti* __restrict__ x, int ldx, const float* 
 
 template <typename T>
 __global__ void add_kernel(const T* __restrict__ x, const T* __restrict__ y, T* __restrict__ out, long long n8) {
+  ptx::griddep_launch_dependents();
+  ptx::griddep_wait();
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n8;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     float a[8], b[8];
@@ -86,15 +90,16 @@ static int ew_grid(long long items) {
 }
 
 template <typename Ti, typename To>
-static void launch_bias_act(const void* x, int ldx, const float* bias, void* out, int ldo, int rows, int cols, int act,
-                            cudaStream_t s) {
+static int launch_bias_act(const void* x, int ldx, const float* bias, void* out, int ldo, int rows, int cols, int act,
+                           cudaStream_t s) {
   const int g = ew_grid(static_cast<long long>(rows) * (cols / 8));
   if (act)
-    bias_act_kernel<Ti, To, true><<<g, 256, 0, s>>>(static_cast<const Ti*>(x), ldx, bias, static_cast<To*>(out), ldo,
-                                                    rows, cols);
+    BT_LAUNCH((bias_act_kernel<Ti, To, true>), dim3(g), dim3(256), 0, s, 1, static_cast<const Ti*>(x), ldx, bias,
+              static_cast<To*>(out), ldo, rows, cols);
   else
-    bias_act_kernel<Ti, To, false><<<g, 256, 0, s>>>(static_cast<const Ti*>(x), ldx, bias, static_cast<To*>(out), ldo,
-                                                     rows, cols);
+    BT_LAUNCH((bias_act_kernel<Ti, To, false>), dim3(g), dim3(256), 0, s, 1, static_cast<const Ti*>(x), ldx, bias,
+              static_cast<To*>(out), ldo, rows, cols);
+  return BT_OK;
 }
 
 }  // namespace bt
@@ -108,15 +113,10 @@ extern "C" BT_API int bt_bias_act(const void* x, int in_dtype, int ldx, const fl
   if (rows == 0) return BT_OK;
   cudaStream_t s = bt::as_stream(stream);
   if (in_dtype == BT_F32 && out_dtype == BT_F32)
-    bt::launch_bias_act<float, float>(x, ldx, bias, out, ldo, rows, cols, act, s);
-  else if (in_dtype == BT_F32)
-    bt::launch_bias_act<float, __nv_bfloat16>(x, ldx, bias, out, ldo, rows, cols, act, s);
-  else if (out_dtype == BT_F32)
-    bt::launch_bias_act<__nv_bfloat16, float>(x, ldx, bias, out, ldo, rows, cols, act, s);
-  else
-    bt::launch_bias_act<__nv_bfloat16, __nv_bfloat16>(x, ldx, bias, out, ldo, rows, cols, act, s);
-  BT_LAUNCH_CHECK();
-  return BT_OK;
+    return bt::launch_bias_act<float, float>(x, ldx, bias, out, ldo, rows, cols, act, s);
+  if (in_dtype == BT_F32) return bt::launch_bias_act<float, __nv_bfloat16>(x, ldx, bias, out, ldo, rows, cols, act, s);
+  if (out_dtype == BT_F32) return bt::launch_bias_act<__nv_bfloat16, float>(x, ldx, bias, out, ldo, rows, cols, act, s);
+  return bt::launch_bias_act<__nv_bfloat16, __nv_bfloat16>(x, ldx, bias, out, ldo, rows, cols, act, s);
 }
 
 extern "C" BT_API int bt_add(const void* x, const void* y, void* out, int dtype, long long n, bt_stream_t stream) {
@@ -126,12 +126,10 @@ extern "C" BT_API int bt_add(const void* x, const void* y, void* out, int dtype,
   cudaStream_t s = bt::as_stream(stream);
   const int g = bt::ew_grid(n / 8);
   if (dtype == BT_F32)
-    bt::add_kernel<float><<<g, 256, 0, s>>>(static_cast<const float*>(x), static_cast<const float*>(y),
-                                            static_cast<float*>(out), n / 8);
+    BT_LAUNCH(bt::add_kernel<float>, dim3(g), dim3(256), 0, s, 1, static_cast<const float*>(x),
+              static_cast<const float*>(y), static_cast<float*>(out), n / 8);
   else
-    bt::add_kernel<__nv_bfloat16><<<g, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(x),
-                                                    static_cast<const __nv_bfloat16*>(y),
-                                                    static_cast<__nv_bfloat16*>(out), n / 8);
-  BT_LAUNCH_CHECK();
+    BT_LAUNCH(bt::add_kernel<__nv_bfloat16>, dim3(g), dim3(256), 0, s, 1, static_cast<const __nv_bfloat16*>(x),
+              static_cast<const __nv_bfloat16*>(y), static_cast<__nv_bfloat16*>(out), n / 8);
   return BT_OK;
 }

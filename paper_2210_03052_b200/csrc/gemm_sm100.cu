@@ -3,15 +3,26 @@
 //
 //   C[M,N] = epilogue( A[M,K] * Bt[N,K]^T )     bf16 in, fp32 accumulate
 //
-//   warp 0      TMA producer: A/B tiles -> STAGES-deep smem ring (128B swizzle)
+//   warp 0      TMA producer: A/B k-blocks -> STAGES-deep smem ring (128B swizzle)
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
 //   warps 2..5  epilogue: tcgen05.ld (TMEM -> regs), bias / GELU / residual,
-//               bf16 pack, 16-byte global stores
+//               bf16 pack -> 128B-swizzled smem staging -> TMA bulk store
 //
+// Two tile shapes share one kernel template:
+//   PAIR = 1  one CTA, 128 x BN tile, tcgen05.mma.cta_group::1
+//   PAIR = 2  an SM pair (cluster of 2), 256 x BN tile, cta_group::2: each CTA
+//             loads its 128 rows of A and HALF of B's BN rows, the leader's
+//             MMA thread drives both tensor cores, each TMEM gets its rows.
 // The accumulator is double-buffered in TMEM (2 x BN fp32 columns) so the
-// epilogue of tile i overlaps the mainloop of tile i+1.  Tiles are 128 x BN
-// (BN in {64, 128, 256}) with BK = 64 (one 128-byte swizzle atom of bf16).
-// Epilogue kinds mirror the reference EpilogueHook (tensor.py:74-106):
+// epilogue of tile i overlaps the mainloop of tile i+1.  BK = 64 (one 128B
+// swizzle atom of bf16).  Tiles are visited N-fastest so an A row block is
+// reused from L2 by every N tile before the next row block is touched.
+//
+// Why these shapes: with all operands of an encoder layer resident in the
+// 126 MB L2, the GEMMs are limited by how fast TMA can move A/B into shared
+// memory, so the tile shape that moves the fewest bytes per FLOP while still
+// filling the 148 SMs wins (see choose_tile); the 2-CTA pair halves B traffic
+// per SM.  Epilogue kinds mirror the reference EpilogueHook (tensor.py:74-106):
 // none / add_bias / add_bias_gelu (fusion.py:30-35) / bias+residual.
 
 #include "common.cuh"
@@ -26,38 +37,77 @@ struct GemmParams {
   const float* bias;
   const __nv_bfloat16* residual;
   int num_m_blocks, num_n_blocks, num_tiles;
+  int dbg;  // 0 normal; 1 = skip the MMAs (pure TMA feed); 2 = skip the TMA loads (pure MMA + epilogue)
 };
 
-constexpr int GEMM_BM = 128;
+// Optional per-CTA event trace (debug / profiling hook, off unless a buffer
+// is installed with bt_debug_gemm_trace): 64 u64 globaltimer stamps per CTA.
+//   [0] setup done, [1] producer start, then per tile it (< 10):
+//   [2+6it] mma begin, [3+6it] mma last commit, [4+6it] epi begin,
+//   [5+6it] epi end, [6+6it] tile id
+__device__ unsigned long long* g_gemm_trace = nullptr;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define BT_TRACE(slot, val)                                                          \
+  do {                                                                               \
+    if (g_gemm_trace && (slot) < 64) g_gemm_trace[blockIdx.x * 64 + (slot)] = (val); \
+  } while (0)
+
 constexpr int GEMM_BK = 64;
 constexpr int GEMM_THREADS = 192;
+constexpr size_t GEMM_SMEM_LIMIT = 232448;  // 227 KB opt-in per CTA
 
-template <int BN>
+constexpr uint32_t pow2_cols(uint32_t c) { return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512; }
+
+template <int PAIR, int BN>
 struct GemmCfg {
-  static constexpr uint32_t A_BYTES = GEMM_BM * GEMM_BK * 2;
-  static constexpr uint32_t B_BYTES = BN * GEMM_BK * 2;
+  static constexpr int BM = 128 * PAIR;  // rows per tile (per pair)
+  static constexpr int BN_CTA = BN / PAIR;  // B rows each CTA loads
+  static constexpr uint32_t A_BYTES = 128 * GEMM_BK * 2;
+  static constexpr uint32_t B_BYTES = BN_CTA * GEMM_BK * 2;
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (BN == 64) ? 8 : (BN == 128 ? 6 : 4);
-  static constexpr uint32_t TMEM_COLS = 2 * BN;  // 128 / 256 / 512: powers of two >= 32
-  static constexpr size_t SMEM = 1024 + static_cast<size_t>(STAGES) * STAGE_BYTES + 256;
+  static constexpr uint32_t STAGING_BYTES = 4 * 2 * 32 * 128;  // 4 epilogue warps x 2 buffers x 32 rows x 128 B
+  static constexpr int STAGES_FIT = static_cast<int>((GEMM_SMEM_LIMIT - 1024 - 256 - STAGING_BYTES) / STAGE_BYTES);
+  static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
+  static constexpr uint32_t TMEM_COLS = pow2_cols(2 * BN);
+  static constexpr size_t SMEM = 1024 + static_cast<size_t>(STAGES) * STAGE_BYTES + STAGING_BYTES + 256;
+  static_assert(SMEM <= GEMM_SMEM_LIMIT, "shared memory budget");
 };
 
+// Tie a second register array to a preceding tcgen05.wait::ld (so no use of
+// it is scheduled above the wait).
+__device__ __forceinline__ void reg_fence(uint32_t (&r)[32]) {
+  asm volatile(""
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                 "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]),
+                 "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]),
+                 "+r"(r[29]), "+r"(r[30]), "+r"(r[31]));
+}
+
+// Epilogue math on 32 consecutive columns of one row, packed to 16 bf16x2.
 template <int EPI>
-__device__ __forceinline__ void epilogue_store(const uint32_t (&acc)[32], const GemmParams& p, int row, int col) {
+__device__ __forceinline__ void epi_math32(const uint32_t (&acc)[32], const GemmParams& p, int row, int col, bool row_ok,
+                                           uint32_t* out16) {
   float v[32];
 #pragma unroll
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(acc[i]);
   if constexpr (EPI == BT_EPI_BIAS_RESIDUAL) {
-    const uint4* r = reinterpret_cast<const uint4*>(p.residual + static_cast<size_t>(row) * p.N + col);
+    if (row_ok) {
+      const uint4* r = reinterpret_cast<const uint4*>(p.residual + static_cast<size_t>(row) * p.N + col);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const uint4 rv = __ldg(r + q);
-      const __nv_bfloat162* rh = reinterpret_cast<const __nv_bfloat162*>(&rv);
+      for (int q = 0; q < 4; ++q) {
+        const uint4 rv = __ldg(r + q);
+        const __nv_bfloat162* rh = reinterpret_cast<const __nv_bfloat162*>(&rv);
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float2 f = __bfloat1622float2(rh[e]);
-        v[q * 8 + 2 * e] += f.x;
-        v[q * 8 + 2 * e + 1] += f.y;
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = __bfloat1622float2(rh[e]);
+          v[q * 8 + 2 * e] += f.x;
+          v[q * 8 + 2 * e + 1] += f.y;
+        }
       }
     }
   }
@@ -76,29 +126,57 @@ __device__ __forceinline__ void epilogue_store(const uint32_t (&acc)[32], const 
 #pragma unroll
     for (int i = 0; i < 32; ++i) v[i] = ptx::gelu_tanh(v[i]);
   }
-  uint4* dst = reinterpret_cast<uint4*>(p.C + static_cast<size_t>(row) * p.N + col);
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    uint4 o;
-    o.x = ptx::pack_bf16x2(v[8 * q + 0], v[8 * q + 1]);
-    o.y = ptx::pack_bf16x2(v[8 * q + 2], v[8 * q + 3]);
-    o.z = ptx::pack_bf16x2(v[8 * q + 4], v[8 * q + 5]);
-    o.w = ptx::pack_bf16x2(v[8 * q + 6], v[8 * q + 7]);
-    dst[q] = o;
+  for (int i = 0; i < 16; ++i) out16[i] = ptx::pack_bf16x2(v[2 * i], v[2 * i + 1]);
+}
+
+// One epilogue warp drains its 32 TMEM lanes (rows) x BN columns of a tile:
+// 64 columns at a time -> swizzled 32 x 128 B smem buffer -> TMA store.
+template <int BN, int EPI>
+__device__ __forceinline__ void epilogue_rows(const GemmParams& p, const CUtensorMap* tmC, uint32_t taddr, int row0,
+                                              int col0, uint8_t* stage_buf, uint32_t& buf_ctr, int lane) {
+  const int row = row0 + lane;
+  const bool row_ok = row < p.M;
+#pragma unroll 1
+  for (int c = 0; c < BN; c += 64) {
+    uint32_t r0[32], r1[32];
+    ptx::tmem_ld32(taddr + c, r0);
+    ptx::tmem_ld32(taddr + c + 32, r1);
+    ptx::tmem_wait_ld(r0);
+    reg_fence(r1);
+    uint32_t pk[32];
+    epi_math32<EPI>(r0, p, row, col0 + c, row_ok, pk);
+    epi_math32<EPI>(r1, p, row, col0 + c + 32, row_ok, pk + 16);
+    uint8_t* buf = stage_buf + (buf_ctr & 1) * 4096;
+    if (lane == 0) ptx::bulk_wait_group_read<1>();  // the store issued from this buffer 2 chunks ago has read it
+    __syncwarp();
+    uint8_t* myrow = buf + lane * 128;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      *reinterpret_cast<uint4*>(myrow + ((j ^ (lane & 7)) << 4)) =
+          make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+    ptx::fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0 && row0 < p.M) {
+      ptx::tma_store_2d(tmC, buf, col0 + c, row0);
+      ptx::bulk_commit_group();
+    }
+    ++buf_ctr;
   }
 }
 
-template <int BN, int EPI>
+template <int PAIR, int BN, int EPI>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_bf16_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                             const GemmParams p) {
-  using Cfg = GemmCfg<BN>;
+                             const __grid_constant__ CUtensorMap tmC, const GemmParams p) {
+  using Cfg = GemmCfg<PAIR, BN>;
   constexpr int STAGES = Cfg::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * Cfg::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
+  uint8_t* sC = smem + STAGES * Cfg::STAGE_BYTES;  // epilogue staging, 1024-aligned
+  uint64_t* full = reinterpret_cast<uint64_t*>(sC + Cfg::STAGING_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -106,165 +184,275 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const uint32_t rank = (PAIR == 2) ? ptx::cluster_ctarank() : 0;
+  const bool leader = rank == 0;
   const int num_k = p.K / GEMM_BK;
+  const int unit = (PAIR == 2) ? (blockIdx.x >> 1) : blockIdx.x;  // pair / CTA index
+  const int num_units = (PAIR == 2) ? (gridDim.x >> 1) : gridDim.x;
 
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tmA);
     ptx::prefetch_tmap(&tmB);
+    ptx::prefetch_tmap(&tmC);
     for (int s = 0; s < STAGES; ++s) {
-      ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&empty[s], 1);
+      ptx::mbar_init(&full[s], 1);   // (leader's) one arrive.expect_tx + the TMA bytes of every CTA
+      ptx::mbar_init(&empty[s], 1);  // one (multicast) tcgen05.commit
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
-      ptx::mbar_init(&tempty[a], 128);
+      ptx::mbar_init(&tempty[a], PAIR * 128);  // (leader's) every epilogue thread of the pair
     }
     ptx::fence_mbar_init();
   }
   if (warp == 1) {
-    ptx::tmem_alloc(tmem_holder, Cfg::TMEM_COLS);
-    ptx::tmem_relinquish();
+    if constexpr (PAIR == 2) {
+      ptx::tmem_alloc_cg2(tmem_holder, Cfg::TMEM_COLS);
+      ptx::tmem_relinquish_cg2();
+    } else {
+      ptx::tmem_alloc(tmem_holder, Cfg::TMEM_COLS);
+      ptx::tmem_relinquish();
+    }
   }
   ptx::tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR == 2) {
+    ptx::cluster_sync();
+  } else {
+    __syncthreads();
+  }
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  if (threadIdx.x == 0) BT_TRACE(0, gtimer());
+  ptx::griddep_launch_dependents();  // the next kernel may start its prologue
 
   if (warp == 0) {
-    if (lane == 0) {
-      // ---------------- TMA producer
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
-        const int mb = tile % p.num_m_blocks;
-        const int nb = tile / p.num_m_blocks;
-        for (int kb = 0; kb < num_k; ++kb) {
-          ptx::mbar_wait(&empty[stage], phase ^ 1u);
-          ptx::mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
-          ptx::tma_load_2d(sA + stage * Cfg::A_BYTES, &tmA, &full[stage], kb * GEMM_BK, mb * GEMM_BM);
-          ptx::tma_load_2d(sB + stage * Cfg::B_BYTES, &tmB, &full[stage], kb * GEMM_BK, nb * BN);
-          if (++stage == STAGES) {
-            stage = 0;
-            phase ^= 1u;
+    // ---------------- TMA producer: the whole warp walks the loop (warp-uniform
+    // control flow keeps addresses in uniform registers), one elected lane issues
+    if (lane == 0) BT_TRACE(1, gtimer());
+    const uint32_t full_leader = (PAIR == 2) ? ptx::mapa_shared(ptx::smem_u32(full), 0) : 0;
+    // Weights (B) never depend on the previous kernel: issue the first
+    // stages' B loads before griddepcontrol.wait so their DRAM latency
+    // overlaps the previous kernel's tail; A follows after the wait.
+    const int pre = (unit < p.num_tiles && p.dbg != 2) ? (num_k < STAGES ? num_k : STAGES) : 0;
+    if (pre > 0) {
+      const int brow0 = (unit % p.num_n_blocks) * BN + static_cast<int>(rank) * Cfg::BN_CTA;
+      for (int kb = 0; kb < pre; ++kb) {
+        if (ptx::elect_one()) {
+          if constexpr (PAIR == 2) {
+            if (leader) ptx::mbar_arrive_expect_tx(&full[kb], PAIR * Cfg::STAGE_BYTES);
+            ptx::tma_load_2d_cg2(sB + kb * Cfg::B_BYTES, &tmB, full_leader + kb * 8, kb * GEMM_BK, brow0);
+          } else {
+            ptx::mbar_arrive_expect_tx(&full[kb], Cfg::STAGE_BYTES);
+            ptx::tma_load_2d(sB + kb * Cfg::B_BYTES, &tmB, &full[kb], kb * GEMM_BK, brow0);
           }
+        }
+        __syncwarp();
+      }
+    }
+    ptx::griddep_wait();  // A (activations) is produced by the previous kernel
+    int stage = 0;
+    uint32_t phase = 0;
+    bool first = true;
+    for (int tile = unit; tile < p.num_tiles; tile += num_units, first = false) {
+      const int mb = tile / p.num_n_blocks;
+      const int nb = tile % p.num_n_blocks;
+      const int arow = mb * Cfg::BM + static_cast<int>(rank) * 128;
+      const int brow = nb * BN + static_cast<int>(rank) * Cfg::BN_CTA;
+      for (int kb = 0; kb < num_k; ++kb) {
+        ptx::mbar_wait(&empty[stage], phase ^ 1u);
+        if (ptx::elect_one()) {
+          const bool b_done = first && kb < pre;  // B (and expect_tx) already issued above
+          if (p.dbg == 2) {
+            if (leader) ptx::mbar_arrive(&full[stage]);
+          } else if constexpr (PAIR == 2) {
+            const uint32_t fb = full_leader + stage * 8;
+            if (!b_done) {
+              if (leader) ptx::mbar_arrive_expect_tx(&full[stage], PAIR * Cfg::STAGE_BYTES);
+              ptx::tma_load_2d_cg2(sB + stage * Cfg::B_BYTES, &tmB, fb, kb * GEMM_BK, brow);
+            }
+            ptx::tma_load_2d_cg2(sA + stage * Cfg::A_BYTES, &tmA, fb, kb * GEMM_BK, arow);
+          } else {
+            if (!b_done) {
+              ptx::mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
+              ptx::tma_load_2d(sB + stage * Cfg::B_BYTES, &tmB, &full[stage], kb * GEMM_BK, brow);
+            }
+            ptx::tma_load_2d(sA + stage * Cfg::A_BYTES, &tmA, &full[stage], kb * GEMM_BK, arow);
+          }
+        }
+        __syncwarp();
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1u;
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------- MMA issuer (one thread)
-      constexpr uint32_t idesc = ptx::idesc_bf16(GEMM_BM, BN, false, false);
+    if (leader) {
+      // ---------------- MMA issuer: the leader CTA's warp 1 walks the loop,
+      // one elected lane issues tcgen05.mma for the whole tile (both SMs for PAIR 2)
+      constexpr uint32_t idesc = ptx::idesc_bf16(Cfg::BM, BN, false, false);
+      const uint32_t a_base = ptx::smem_u32(sA);
+      const uint32_t b_base = ptx::smem_u32(sB);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++it) {
+      for (int tile = unit; tile < p.num_tiles; tile += num_units, ++it) {
         const int acc = it & 1;
         const uint32_t aphase = (it >> 1) & 1;
         ptx::mbar_wait(&tempty[acc], aphase ^ 1u);
         ptx::tc_fence_after();
+        if (lane == 0) BT_TRACE(2 + 6 * it, gtimer());
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kb = 0; kb < num_k; ++kb) {
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
-          const uint32_t a0 = ptx::smem_u32(sA + stage * Cfg::A_BYTES);
-          const uint32_t b0 = ptx::smem_u32(sB + stage * Cfg::B_BYTES);
+          const uint64_t ad0 = ptx::sdesc_sw128(a_base + stage * Cfg::A_BYTES, 1024, 16);
+          const uint64_t bd0 = ptx::sdesc_sw128(b_base + stage * Cfg::B_BYTES, 1024, 16);
+          if (ptx::elect_one()) {
+            if (p.dbg != 1) {
 #pragma unroll
-          for (int k = 0; k < GEMM_BK / 16; ++k) {
-            const uint64_t ad = ptx::sdesc_sw128(a0 + k * 32, 1024, 16);
-            const uint64_t bd = ptx::sdesc_sw128(b0 + k * 32, 1024, 16);
-            ptx::mma_bf16_ss(d_tmem, ad, bd, idesc, (kb | k) != 0);
+              for (int k = 0; k < GEMM_BK / 16; ++k) {
+                // advancing K by 16 bf16 = 32 B inside the 128B swizzle atom: +2 in the start-address field
+                if constexpr (PAIR == 2)
+                  ptx::mma_bf16_ss_cg2(d_tmem, ad0 + 2 * k, bd0 + 2 * k, idesc, (kb | k) != 0);
+                else
+                  ptx::mma_bf16_ss(d_tmem, ad0 + 2 * k, bd0 + 2 * k, idesc, (kb | k) != 0);
+              }
+            }
+            if constexpr (PAIR == 2)
+              ptx::mma_commit_cg2_mc(&empty[stage], 0x3);  // frees this stage in both CTAs
+            else
+              ptx::mma_commit(&empty[stage]);
           }
-          ptx::mma_commit(&empty[stage]);  // frees the smem slot when these MMAs retire
+          __syncwarp();
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1u;
           }
         }
-        ptx::mma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+        if (ptx::elect_one()) {
+          if constexpr (PAIR == 2)
+            ptx::mma_commit_cg2_mc(&tfull[acc], 0x3);
+          else
+            ptx::mma_commit(&tfull[acc]);
+        }
+        __syncwarp();
+        if (lane == 0) {
+          BT_TRACE(3 + 6 * it, gtimer());
+          BT_TRACE(6 + 6 * it, tile);
+        }
       }
     }
   } else {
     // ---------------- epilogue warps 2..5; warp w owns TMEM lanes 32*(w%4)
     const int quarter = warp & 3;
-    const int row_in_tile = quarter * 32 + lane;
+    uint8_t* stage_buf = sC + (warp - 2) * 8192;
+    const uint32_t tempty_leader = (PAIR == 2) ? ptx::mapa_shared(ptx::smem_u32(tempty), 0) : 0;
+    uint32_t buf_ctr = 0;
     int it = 0;
-    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++it) {
+    ptx::griddep_wait();  // C / residual may be read or written by the previous kernel
+    for (int tile = unit; tile < p.num_tiles; tile += num_units, ++it) {
       const int acc = it & 1;
       const uint32_t aphase = (it >> 1) & 1;
-      const int mb = tile % p.num_m_blocks;
-      const int nb = tile / p.num_m_blocks;
+      const int mb = tile / p.num_n_blocks;
+      const int nb = tile % p.num_n_blocks;
       ptx::mbar_wait(&tfull[acc], aphase);
       ptx::tc_fence_after();
-      const int row = mb * GEMM_BM + row_in_tile;
+      if (threadIdx.x == 64) BT_TRACE(4 + 6 * it, gtimer());
+      const int row0 = mb * Cfg::BM + static_cast<int>(rank) * 128 + quarter * 32;
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN;
-#pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
-        uint32_t r[32];
-        ptx::tmem_ld32(taddr + c, r);
-        ptx::tmem_wait_ld(r);
-        if (row < p.M) epilogue_store<EPI>(r, p, row, nb * BN + c);
-      }
+      epilogue_rows<BN, EPI>(p, &tmC, taddr, row0, nb * BN, stage_buf, buf_ctr, lane);
       ptx::tc_fence_before();
-      ptx::mbar_arrive(&tempty[acc]);
+      if constexpr (PAIR == 2)
+        ptx::mbar_arrive_cluster(tempty_leader + acc * 8);
+      else
+        ptx::mbar_arrive(&tempty[acc]);
+      if (threadIdx.x == 64) BT_TRACE(5 + 6 * it, gtimer());
     }
+    if (lane == 0) ptx::bulk_wait_group<0>();  // all of this warp's output stores complete
   }
 
   ptx::tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR == 2) {
+    ptx::cluster_sync();
+  } else {
+    __syncthreads();
+  }
   if (warp == 1) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+    if constexpr (PAIR == 2)
+      ptx::tmem_dealloc_cg2(tmem_base, Cfg::TMEM_COLS);
+    else
+      ptx::tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
   }
 }
 
-template <int BN, int EPI>
-static int launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int grid,
-                         cudaStream_t s) {
-  using Cfg = GemmCfg<BN>;
-  auto kern = gemm_bf16_tcgen05_kernel<BN, EPI>;
+template <int PAIR, int BN, int EPI>
+static int launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const GemmParams& p,
+                         int units, cudaStream_t s) {
+  using Cfg = GemmCfg<PAIR, BN>;
+  auto kern = gemm_bf16_tcgen05_kernel<PAIR, BN, EPI>;
   static bool attr_set = false;  // one flag per instantiation
   if (!attr_set) {
     BT_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Cfg::SMEM)));
     attr_set = true;
   }
-  kern<<<grid, GEMM_THREADS, Cfg::SMEM, s>>>(ta, tb, p);
-  BT_LAUNCH_CHECK();
+  BT_LAUNCH(kern, dim3(units * PAIR), dim3(GEMM_THREADS), Cfg::SMEM, s, PAIR, ta, tb, tc, p);
   return BT_OK;
 }
 
-template <int BN>
-static int dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int grid,
-                        cudaStream_t s) {
+template <int PAIR, int BN>
+static int dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
+                        const GemmParams& p, int units, cudaStream_t s) {
   switch (epi) {
-    case BT_EPI_NONE: return launch_gemm_t<BN, BT_EPI_NONE>(ta, tb, p, grid, s);
-    case BT_EPI_BIAS: return launch_gemm_t<BN, BT_EPI_BIAS>(ta, tb, p, grid, s);
-    case BT_EPI_BIAS_GELU: return launch_gemm_t<BN, BT_EPI_BIAS_GELU>(ta, tb, p, grid, s);
-    default: return launch_gemm_t<BN, BT_EPI_BIAS_RESIDUAL>(ta, tb, p, grid, s);
+    case BT_EPI_NONE: return launch_gemm_t<PAIR, BN, BT_EPI_NONE>(ta, tb, tc, p, units, s);
+    case BT_EPI_BIAS: return launch_gemm_t<PAIR, BN, BT_EPI_BIAS>(ta, tb, tc, p, units, s);
+    case BT_EPI_BIAS_GELU: return launch_gemm_t<PAIR, BN, BT_EPI_BIAS_GELU>(ta, tb, tc, p, units, s);
+    default: return launch_gemm_t<PAIR, BN, BT_EPI_BIAS_RESIDUAL>(ta, tb, tc, p, units, s);
   }
 }
 
-// Pick BN to minimise (waves x per-tile mainloop cycles): small-M problems
-// (T = 1-5k packed rows) otherwise leave most of the 148 SMs idle.
-static int choose_bn(int M, int N, int K, int sms) {
-  const int cands[3] = {256, 128, 64};
-  int best = 64;
-  double best_cost = 1e30;
-  const int mblocks = (M + GEMM_BM - 1) / GEMM_BM;
-  for (int bn : cands) {
-    if (N % bn) continue;
-    const long long tiles = static_cast<long long>(mblocks) * (N / bn);
-    const long long waves = (tiles + sms - 1) / sms;
-    const double cost = static_cast<double>(waves) * (bn * (K / 32.0) + 700.0);
-    if (cost < best_cost - 1e-9) {
+struct GemmChoice {
+  int pair;  // 1 = one CTA 128 x bn tile, 2 = SM pair 256 x bn tile
+  int bn;
+};
+
+// Cost model (cycles): tiles run in waves of `slots` concurrent tiles.  A
+// wave lasts the longer of (a) one tile's MMA time and (b) its TMA feed time,
+// bytes per CTA per k-block at the measured per-SM rate (~32 KB per 620
+// cycles with the whole chip loading from L2), plus a fixed fill/epilogue
+// cost.
+static GemmChoice choose_tile(int M, int N, int K, int sms) {
+  struct Cand { int pair, bn; };
+  const Cand cands[] = {{2, 256}, {2, 192}, {2, 128}, {1, 256}, {1, 192}, {1, 128}, {1, 64}};
+  GemmChoice best{1, 64};
+  double best_cost = 1e300;
+  const int nk = K / GEMM_BK;
+  for (const Cand& c : cands) {
+    if (N % c.bn) continue;
+    const int bm = 128 * c.pair;
+    long long remaining = static_cast<long long>((M + bm - 1) / bm) * (N / c.bn);
+    const long long slots = sms / c.pair;
+    const double mma = nk * 4.0 * (128.0 * c.bn / 256.0);                       // MMA cycles per tile
+    const double feed = nk * (128.0 + c.bn / c.pair) * GEMM_BK * 2.0 / 52.0;   // TMA feed cycles per tile
+    const double per_tile = (mma > feed ? mma : feed);
+    double cost = 0.0;
+    while (remaining > 0) {
+      const long long active = remaining < slots ? remaining : slots;
+      cost += per_tile + 2500.0;
+      remaining -= active;
+    }
+    if (cost < best_cost * 0.999) {
       best_cost = cost;
-      best = bn;
+      best = {c.pair, c.bn};
     }
   }
   return best;
 }
 
+static int g_gemm_dbg = 0;
+
 int gemm_launch(const void* A, const void* Bt, const float* bias, const void* residual, void* C, int M, int N,
-                int K, int epi, int force_bn, cudaStream_t s) {
+                int K, int epi, int force, cudaStream_t s) {
   BT_REQUIRE(M >= 0 && N > 0 && K > 0, BT_ESHAPE, "gemm: bad shape M=%d N=%d K=%d", M, N, K);
   BT_REQUIRE(K % GEMM_BK == 0, BT_ESHAPE, "gemm: K=%d must be a multiple of 64", K);
   BT_REQUIRE(N % 64 == 0, BT_ESHAPE, "gemm: N=%d must be a multiple of 64", N);
@@ -273,11 +461,15 @@ int gemm_launch(const void* A, const void* Bt, const float* bias, const void* re
   BT_REQUIRE(epi != BT_EPI_BIAS_RESIDUAL || residual != nullptr, BT_ESHAPE, "gemm: residual epilogue needs residual");
   if (M == 0) return BT_OK;
   const int sms = num_sms() > 0 ? num_sms() : 148;
-  const int bn = force_bn ? force_bn : choose_bn(M, N, K, sms);
-  BT_REQUIRE(N % bn == 0, BT_ESHAPE, "gemm: N=%d not a multiple of BN=%d", N, bn);
-  CUtensorMap ta, tb;
-  BT_TRY(make_tmap_bf16_2d(&ta, A, M, K, K, GEMM_BM, GEMM_BK));
-  BT_TRY(make_tmap_bf16_2d(&tb, Bt, N, K, K, bn, GEMM_BK));
+  GemmChoice ch = choose_tile(M, N, K, sms);
+  if (force > 0) ch = {1, force};  // test hooks: +bn = one CTA, -bn = SM pair
+  if (force < 0) ch = {2, -force};
+  BT_REQUIRE(N % ch.bn == 0, BT_ESHAPE, "gemm: N=%d not a multiple of BN=%d", N, ch.bn);
+  const int bm = 128 * ch.pair;
+  CUtensorMap ta, tb, tc;
+  BT_TRY(make_tmap_bf16_2d(&ta, A, M, K, K, 128, GEMM_BK));
+  BT_TRY(make_tmap_bf16_2d(&tb, Bt, N, K, K, ch.bn / ch.pair, GEMM_BK));
+  BT_TRY(make_tmap_bf16_2d(&tc, C, M, N, N, 32, 64));
   GemmParams p;
   p.M = M;
   p.N = N;
@@ -285,15 +477,28 @@ int gemm_launch(const void* A, const void* Bt, const float* bias, const void* re
   p.C = static_cast<__nv_bfloat16*>(C);
   p.bias = bias;
   p.residual = static_cast<const __nv_bfloat16*>(residual);
-  p.num_m_blocks = (M + GEMM_BM - 1) / GEMM_BM;
-  p.num_n_blocks = N / bn;
+  p.num_m_blocks = (M + bm - 1) / bm;
+  p.num_n_blocks = N / ch.bn;
   p.num_tiles = p.num_m_blocks * p.num_n_blocks;
-  const int grid = p.num_tiles < sms ? p.num_tiles : sms;
-  switch (bn) {
-    case 64: return dispatch_epi<64>(epi, ta, tb, p, grid, s);
-    case 128: return dispatch_epi<128>(epi, ta, tb, p, grid, s);
-    default: return dispatch_epi<256>(epi, ta, tb, p, grid, s);
+  p.dbg = g_gemm_dbg;
+  const int slots = sms / ch.pair;
+  const int units = p.num_tiles < slots ? p.num_tiles : slots;
+  if (ch.pair == 2) {
+    switch (ch.bn) {
+      case 128: return dispatch_epi<2, 128>(epi, ta, tb, tc, p, units, s);
+      case 192: return dispatch_epi<2, 192>(epi, ta, tb, tc, p, units, s);
+      case 256: return dispatch_epi<2, 256>(epi, ta, tb, tc, p, units, s);
+      default: BT_REQUIRE(false, BT_ECONFIG, "gemm: SM-pair tile width %d unsupported", ch.bn);
+    }
   }
+  switch (ch.bn) {
+    case 64: return dispatch_epi<1, 64>(epi, ta, tb, tc, p, units, s);
+    case 128: return dispatch_epi<1, 128>(epi, ta, tb, tc, p, units, s);
+    case 192: return dispatch_epi<1, 192>(epi, ta, tb, tc, p, units, s);
+    case 256: return dispatch_epi<1, 256>(epi, ta, tb, tc, p, units, s);
+    default: BT_REQUIRE(false, BT_ECONFIG, "gemm: tile width %d unsupported", ch.bn);
+  }
+  return BT_OK;
 }
 
 }  // namespace bt
@@ -303,9 +508,26 @@ extern "C" int bt_gemm(const void* A, const void* Bt, const float* bias, const v
   return bt::gemm_launch(A, Bt, bias, residual, C, M, N, K, epilogue, 0, bt::as_stream(stream));
 }
 
-// Test hook: force a tile width (64/128/256) so every instantiation is covered.
+// Debug hook: install (or clear, with NULL) the per-CTA GEMM event trace buffer
+// (>= 64 u64 per CTA of the next launches).
+extern "C" int bt_debug_gemm_trace(unsigned long long* buf) {
+  BT_CUDA_CHECK(cudaMemcpyToSymbol(bt::g_gemm_trace, &buf, sizeof(buf)));
+  return BT_OK;
+}
+
+// Debug hook: 0 normal; 1 = GEMMs skip their MMAs (measure the TMA feed alone);
+// 2 = GEMMs skip their TMA loads (measure MMA + epilogue alone).  Results are
+// garbage in modes 1 and 2.
+extern "C" int bt_debug_gemm_mode(int mode) {
+  BT_REQUIRE(mode >= 0 && mode <= 2, BT_ECONFIG, "bt_debug_gemm_mode: mode must be 0..2");
+  bt::g_gemm_dbg = mode;
+  return BT_OK;
+}
+
+// Test hook: force a tile (+bn: one CTA 128 x bn; -bn: SM pair 256 x bn) so every instantiation is covered.
 extern "C" int bt_gemm_bn(const void* A, const void* Bt, const float* bias, const void* residual, void* C, int M,
                           int N, int K, int epilogue, int bn, bt_stream_t stream) {
-  BT_REQUIRE(bn == 64 || bn == 128 || bn == 256, BT_ECONFIG, "bt_gemm_bn: bn must be 64/128/256, got %d", bn);
+  BT_REQUIRE(bn == 64 || bn == 128 || bn == 192 || bn == 256 || bn == -128 || bn == -192 || bn == -256, BT_ECONFIG,
+             "bt_gemm_bn: bn must be 64/128/192/256 (one CTA) or -128/-192/-256 (SM pair), got %d", bn);
   return bt::gemm_launch(A, Bt, bias, residual, C, M, N, K, epilogue, bn, bt::as_stream(stream));
 }

@@ -18,6 +18,8 @@ __global__ void __launch_bounds__(256) ln_bias_residual_kernel(const __nv_bfloat
                                                                const float* __restrict__ gamma,
                                                                const float* __restrict__ beta, float eps,
                                                                __nv_bfloat16* __restrict__ out, int T, int k) {
+  ptx::griddep_launch_dependents();
+  ptx::griddep_wait();
   const int lane = threadIdx.x & 31;
   const int wpb = blockDim.x >> 5;
   const int nchunk = k >> 3;
@@ -100,14 +102,16 @@ __global__ void __launch_bounds__(256) ln_bias_residual_kernel(const __nv_bfloat
 }
 
 template <int NCH>
-static void launch_ln(const __nv_bfloat16* x, const __nv_bfloat16* r, const float* b, const float* g, const float* be,
+static int launch_ln(const __nv_bfloat16* x, const __nv_bfloat16* r, const float* b, const float* g, const float* be,
                       float eps, __nv_bfloat16* out, int T, int k, cudaStream_t s) {
   const int threads = 256, wpb = threads / 32;
   const int sms = num_sms() > 0 ? num_sms() : 148;
   long long grid = (T + wpb - 1) / wpb;
   if (grid > sms * 8LL) grid = sms * 8LL;
   if (grid < 1) grid = 1;
-  ln_bias_residual_kernel<NCH><<<static_cast<int>(grid), threads, 0, s>>>(x, r, b, g, be, eps, out, T, k);
+  BT_LAUNCH(ln_bias_residual_kernel<NCH>, dim3(static_cast<int>(grid)), dim3(threads), 0, s, 1, x, r, b, g, be, eps,
+            out, T, k);
+  return BT_OK;
 }
 
 }  // namespace bt
@@ -125,14 +129,12 @@ extern "C" int bt_ln_bias_residual(const void* x, const void* residual, const fl
   cudaStream_t s = bt::as_stream(stream);
   const int nch = (k / 8 + 31) / 32;
   switch (nch) {
-    case 1: bt::launch_ln<1>(xb, rb, bias, gamma, beta, eps, ob, T, k, s); break;
-    case 2: bt::launch_ln<2>(xb, rb, bias, gamma, beta, eps, ob, T, k, s); break;
-    case 3: bt::launch_ln<3>(xb, rb, bias, gamma, beta, eps, ob, T, k, s); break;
-    case 4: bt::launch_ln<4>(xb, rb, bias, gamma, beta, eps, ob, T, k, s); break;
-    case 5: case 6: bt::launch_ln<6>(xb, rb, bias, gamma, beta, eps, ob, T, k, s); break;
-    case 7: case 8: bt::launch_ln<8>(xb, rb, bias, gamma, beta, eps, ob, T, k, s); break;
-    default: bt::launch_ln<16>(xb, rb, bias, gamma, beta, eps, ob, T, k, s); break;
+    case 1: return bt::launch_ln<1>(xb, rb, bias, gamma, beta, eps, ob, T, k, s);
+    case 2: return bt::launch_ln<2>(xb, rb, bias, gamma, beta, eps, ob, T, k, s);
+    case 3: return bt::launch_ln<3>(xb, rb, bias, gamma, beta, eps, ob, T, k, s);
+    case 4: return bt::launch_ln<4>(xb, rb, bias, gamma, beta, eps, ob, T, k, s);
+    case 5: case 6: return bt::launch_ln<6>(xb, rb, bias, gamma, beta, eps, ob, T, k, s);
+    case 7: case 8: return bt::launch_ln<8>(xb, rb, bias, gamma, beta, eps, ob, T, k, s);
+    default: return bt::launch_ln<16>(xb, rb, bias, gamma, beta, eps, ob, T, k, s);
   }
-  BT_LAUNCH_CHECK();
-  return BT_OK;
 }

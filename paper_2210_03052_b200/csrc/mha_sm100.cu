@@ -115,6 +115,8 @@ __global__ void __launch_bounds__(128, 1) mha_short_kernel(const __grid_constant
   ptx::tc_fence_after();
   const uint32_t tmem = *holder;
   constexpr uint32_t O_COL = MHA_SHORT_MAX_KEYS;
+  ptx::griddep_launch_dependents();
+  ptx::griddep_wait();  // qkv is produced by the previous kernel
 
   if (threadIdx.x == 0) {
     // stage Q tile and the whole K/V head slab of this sequence
@@ -260,6 +262,8 @@ __global__ void __launch_bounds__(128, 1) mha_long_kernel(const __grid_constant_
   ptx::tc_fence_after();
   const uint32_t tmem = *holder;
   constexpr uint32_t S_COL = 0, O_COL = 128;
+  ptx::griddep_launch_dependents();
+  ptx::griddep_wait();  // qkv is produced by the previous kernel
   constexpr uint32_t idesc_s = ptx::idesc_bf16(128, 128, false, false);
   constexpr uint32_t idesc_o = ptx::idesc_bf16(128, MHA_D, false, true);
 
@@ -416,20 +420,19 @@ int mha_launch(const void* qkv, const int32_t* seq_starts, int bs, int mx, int H
     static bool set1 = false, set2 = false, set3 = false;
     if (nkb == 1) {
       if (!set1) { BT_TRY(set_smem(mha_short_kernel<1>, ShortCfg<1>::SMEM)); set1 = true; }
-      mha_short_kernel<1><<<grid, 128, ShortCfg<1>::SMEM, s>>>(tm, p);
+      BT_LAUNCH(mha_short_kernel<1>, grid, dim3(128), ShortCfg<1>::SMEM, s, 1, tm, p);
     } else if (nkb == 2) {
       if (!set2) { BT_TRY(set_smem(mha_short_kernel<2>, ShortCfg<2>::SMEM)); set2 = true; }
-      mha_short_kernel<2><<<grid, 128, ShortCfg<2>::SMEM, s>>>(tm, p);
+      BT_LAUNCH(mha_short_kernel<2>, grid, dim3(128), ShortCfg<2>::SMEM, s, 1, tm, p);
     } else {
       if (!set3) { BT_TRY(set_smem(mha_short_kernel<3>, ShortCfg<3>::SMEM)); set3 = true; }
-      mha_short_kernel<3><<<grid, 128, ShortCfg<3>::SMEM, s>>>(tm, p);
+      BT_LAUNCH(mha_short_kernel<3>, grid, dim3(128), ShortCfg<3>::SMEM, s, 1, tm, p);
     }
   } else {
     static bool setl = false;
     if (!setl) { BT_TRY(set_smem(mha_long_kernel, LongCfg::SMEM)); setl = true; }
-    mha_long_kernel<<<grid, 128, LongCfg::SMEM, s>>>(tm, p);
+    BT_LAUNCH(mha_long_kernel, grid, dim3(128), LongCfg::SMEM, s, 1, tm, p);
   }
-  BT_LAUNCH_CHECK();
   return BT_OK;
 }
 

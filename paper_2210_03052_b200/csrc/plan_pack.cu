@@ -6,6 +6,7 @@
 // sized in multiples of the SM count.
 
 #include <cstdarg>
+#include <cstdlib>
 #include <cstring>
 
 #include <type_traits>
@@ -27,6 +28,15 @@ void set_error(const char* fmt, ...) {
 }
 const char* last_error() { return t_err; }
 
+bool pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("BT_PDL");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on != 0;
+}
+
 int num_sms() {
   static int cached = -1;
   if (cached < 0) {
@@ -46,6 +56,8 @@ int num_sms() {
 // 102-109 rejects anything else).
 __global__ void plan_rows_kernel(const uint8_t* __restrict__ mask, int bs, int mx, int32_t* __restrict__ lengths,
                                  int32_t* __restrict__ status) {
+  ptx::griddep_launch_dependents();
+  ptx::griddep_wait();
   const int warps_per_block = blockDim.x / 32;
   const int lane = threadIdx.x & 31;
   for (int row = blockIdx.x * warps_per_block + threadIdx.x / 32; row < bs; row += gridDim.x * warps_per_block) {
@@ -80,6 +92,8 @@ __global__ void __launch_bounds__(1024) plan_scan_kernel(const int32_t* __restri
                                                           int32_t* __restrict__ valid_cnt) {
   __shared__ int32_t warp_sums[32];
   __shared__ int32_t carry_s;
+  ptx::griddep_launch_dependents();
+  ptx::griddep_wait();
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   if (tid == 0) carry_s = 0;
   __syncthreads();
@@ -120,6 +134,8 @@ __global__ void __launch_bounds__(1024) plan_scan_kernel(const int32_t* __restri
 // One CTA-slice per sequence, grid-strided.
 __global__ void plan_offsets_kernel(const int32_t* __restrict__ seq_starts, int bs, int mx,
                                     int32_t* __restrict__ offsets) {
+  ptx::griddep_launch_dependents();
+  ptx::griddep_wait();
   for (int b = blockIdx.x; b < bs; b += gridDim.x) {
     const int s0 = seq_starts[b];
     const int len = seq_starts[b + 1] - s0;
@@ -194,6 +210,8 @@ __device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float v) { return
 template <typename Tin, typename Tout>
 __global__ void pack_scalar_kernel(const Tin* __restrict__ padded, const int32_t* __restrict__ offsets, int T, int k,
                                    Tout* __restrict__ packed) {
+  ptx::griddep_launch_dependents();
+  ptx::griddep_wait();
   const long long total = static_cast<long long>(T) * k;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -205,6 +223,8 @@ __global__ void pack_scalar_kernel(const Tin* __restrict__ padded, const int32_t
 template <typename Tin, typename Tout>
 __global__ void unpack_scalar_kernel(const Tin* __restrict__ packed, const int32_t* __restrict__ seq_starts, int bs,
                                      int mx, int k, Tout* __restrict__ padded) {
+  ptx::griddep_launch_dependents();
+  ptx::griddep_wait();
   const long long total = static_cast<long long>(bs) * mx * k;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -221,6 +241,8 @@ __global__ void unpack_scalar_kernel(const Tin* __restrict__ packed, const int32
 template <typename Tin, typename Tout>
 __global__ void pack_kernel(const Tin* __restrict__ padded, const int32_t* __restrict__ offsets, int T, int k,
                             Tout* __restrict__ packed) {
+  ptx::griddep_launch_dependents();
+  ptx::griddep_wait();
   const int chunks = k / 8;
   const long long total = static_cast<long long>(T) * chunks;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
@@ -237,6 +259,8 @@ __global__ void pack_kernel(const Tin* __restrict__ padded, const int32_t* __res
 template <typename Tin, typename Tout>
 __global__ void unpack_kernel(const Tin* __restrict__ packed, const int32_t* __restrict__ seq_starts, int bs,
                               int mx, int k, Tout* __restrict__ padded) {
+  ptx::griddep_launch_dependents();
+  ptx::griddep_wait();
   const int chunks = k / 8;
   const long long total = static_cast<long long>(bs) * mx * chunks;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
@@ -266,26 +290,28 @@ static int grid_for(long long work_items, int threads) {
 }
 
 template <typename Tin, typename Tout>
-static void launch_pack(const void* in, const int32_t* offsets, int T, int k, void* out, cudaStream_t s) {
+static int launch_pack(const void* in, const int32_t* offsets, int T, int k, void* out, cudaStream_t s) {
   const int threads = 256;
   if (k % 8 == 0) {
-    pack_kernel<<<grid_for(static_cast<long long>(T) * (k / 8), threads), threads, 0, s>>>(
-        static_cast<const Tin*>(in), offsets, T, k, static_cast<Tout*>(out));
+    BT_LAUNCH((pack_kernel<Tin, Tout>), dim3(grid_for(static_cast<long long>(T) * (k / 8), threads)), dim3(threads), 0,
+              s, 1, static_cast<const Tin*>(in), offsets, T, k, static_cast<Tout*>(out));
   } else {
-    pack_scalar_kernel<<<grid_for(static_cast<long long>(T) * k, threads), threads, 0, s>>>(
-        static_cast<const Tin*>(in), offsets, T, k, static_cast<Tout*>(out));
+    BT_LAUNCH((pack_scalar_kernel<Tin, Tout>), dim3(grid_for(static_cast<long long>(T) * k, threads)), dim3(threads), 0,
+              s, 1, static_cast<const Tin*>(in), offsets, T, k, static_cast<Tout*>(out));
   }
+  return BT_OK;
 }
 template <typename Tin, typename Tout>
-static void launch_unpack(const void* in, const int32_t* starts, int bs, int mx, int k, void* out, cudaStream_t s) {
+static int launch_unpack(const void* in, const int32_t* starts, int bs, int mx, int k, void* out, cudaStream_t s) {
   const int threads = 256;
   if (k % 8 == 0) {
-    unpack_kernel<<<grid_for(static_cast<long long>(bs) * mx * (k / 8), threads), threads, 0, s>>>(
-        static_cast<const Tin*>(in), starts, bs, mx, k, static_cast<Tout*>(out));
+    BT_LAUNCH((unpack_kernel<Tin, Tout>), dim3(grid_for(static_cast<long long>(bs) * mx * (k / 8), threads)),
+              dim3(threads), 0, s, 1, static_cast<const Tin*>(in), starts, bs, mx, k, static_cast<Tout*>(out));
   } else {
-    unpack_scalar_kernel<<<grid_for(static_cast<long long>(bs) * mx * k, threads), threads, 0, s>>>(
-        static_cast<const Tin*>(in), starts, bs, mx, k, static_cast<Tout*>(out));
+    BT_LAUNCH((unpack_scalar_kernel<Tin, Tout>), dim3(grid_for(static_cast<long long>(bs) * mx * k, threads)),
+              dim3(threads), 0, s, 1, static_cast<const Tin*>(in), starts, bs, mx, k, static_cast<Tout*>(out));
   }
+  return BT_OK;
 }
 
 }  // namespace bt
@@ -310,12 +336,10 @@ int bt_plan_mask(const uint8_t* mask, int bs, int mx, int32_t* lengths, int32_t*
   const int sms = num_sms() > 0 ? num_sms() : 148;
   int grid = (bs + warps - 1) / warps;
   if (grid > sms * 8) grid = sms * 8;
-  plan_rows_kernel<<<grid, warps * 32, 0, s>>>(mask, bs, mx, lengths, status_dev);
-  BT_LAUNCH_CHECK();
-  plan_scan_kernel<<<1, 1024, 0, s>>>(lengths, bs, seq_starts, valid_cnt_dev);
-  BT_LAUNCH_CHECK();
-  plan_offsets_kernel<<<bs < sms * 4 ? bs : sms * 4, 256, 0, s>>>(seq_starts, bs, mx, offsets);
-  BT_LAUNCH_CHECK();
+  BT_LAUNCH(plan_rows_kernel, dim3(grid), dim3(warps * 32), 0, s, 1, mask, bs, mx, lengths, status_dev);
+  BT_LAUNCH(plan_scan_kernel, dim3(1), dim3(1024), 0, s, 1, (const int32_t*)lengths, bs, seq_starts, valid_cnt_dev);
+  BT_LAUNCH(plan_offsets_kernel, dim3(bs < sms * 4 ? bs : sms * 4), dim3(256), 0, s, 1, (const int32_t*)seq_starts,
+            bs, mx, offsets);
   return BT_OK;
 }
 
@@ -325,11 +349,10 @@ int bt_plan_lengths(const int32_t* lengths, int bs, int mx, int32_t* seq_starts,
   BT_REQUIRE(lengths && seq_starts, BT_ESHAPE, "null pointer");
   cudaStream_t s = as_stream(stream);
   const int sms = num_sms() > 0 ? num_sms() : 148;
-  plan_scan_kernel<<<1, 1024, 0, s>>>(lengths, bs, seq_starts, nullptr);
-  BT_LAUNCH_CHECK();
+  BT_LAUNCH(plan_scan_kernel, dim3(1), dim3(1024), 0, s, 1, lengths, bs, seq_starts, (int32_t*)nullptr);
   if (offsets) {
-    plan_offsets_kernel<<<bs < sms * 4 ? bs : sms * 4, 256, 0, s>>>(seq_starts, bs, mx, offsets);
-    BT_LAUNCH_CHECK();
+    BT_LAUNCH(plan_offsets_kernel, dim3(bs < sms * 4 ? bs : sms * 4), dim3(256), 0, s, 1, (const int32_t*)seq_starts,
+              bs, mx, offsets);
   }
   return BT_OK;
 }
@@ -341,12 +364,10 @@ int bt_pack(const void* padded, int in_dtype, const int32_t* offsets, int T, int
              "pack: unsupported dtypes %d -> %d", in_dtype, out_dtype);
   if (T == 0) return BT_OK;
   cudaStream_t s = as_stream(stream);
-  if (in_dtype == BT_F32 && out_dtype == BT_BF16) launch_pack<float, __nv_bfloat16>(padded, offsets, T, k, packed, s);
-  else if (in_dtype == BT_F32) launch_pack<float, float>(padded, offsets, T, k, packed, s);
-  else if (out_dtype == BT_BF16) launch_pack<__nv_bfloat16, __nv_bfloat16>(padded, offsets, T, k, packed, s);
-  else launch_pack<__nv_bfloat16, float>(padded, offsets, T, k, packed, s);
-  BT_LAUNCH_CHECK();
-  return BT_OK;
+  if (in_dtype == BT_F32 && out_dtype == BT_BF16) return launch_pack<float, __nv_bfloat16>(padded, offsets, T, k, packed, s);
+  if (in_dtype == BT_F32) return launch_pack<float, float>(padded, offsets, T, k, packed, s);
+  if (out_dtype == BT_BF16) return launch_pack<__nv_bfloat16, __nv_bfloat16>(padded, offsets, T, k, packed, s);
+  return launch_pack<__nv_bfloat16, float>(padded, offsets, T, k, packed, s);
 }
 
 int bt_unpack(const void* packed, int in_dtype, const int32_t* seq_starts, int bs, int mx, int k, void* padded,
@@ -355,12 +376,10 @@ int bt_unpack(const void* packed, int in_dtype, const int32_t* seq_starts, int b
   BT_REQUIRE((in_dtype == BT_F32 || in_dtype == BT_BF16) && (out_dtype == BT_F32 || out_dtype == BT_BF16), BT_ECONFIG,
              "unpack: unsupported dtypes %d -> %d", in_dtype, out_dtype);
   cudaStream_t s = as_stream(stream);
-  if (in_dtype == BT_BF16 && out_dtype == BT_F32) launch_unpack<__nv_bfloat16, float>(packed, seq_starts, bs, mx, k, padded, s);
-  else if (in_dtype == BT_F32 && out_dtype == BT_F32) launch_unpack<float, float>(packed, seq_starts, bs, mx, k, padded, s);
-  else if (in_dtype == BT_BF16) launch_unpack<__nv_bfloat16, __nv_bfloat16>(packed, seq_starts, bs, mx, k, padded, s);
-  else launch_unpack<float, __nv_bfloat16>(packed, seq_starts, bs, mx, k, padded, s);
-  BT_LAUNCH_CHECK();
-  return BT_OK;
+  if (in_dtype == BT_BF16 && out_dtype == BT_F32) return launch_unpack<__nv_bfloat16, float>(packed, seq_starts, bs, mx, k, padded, s);
+  if (in_dtype == BT_F32 && out_dtype == BT_F32) return launch_unpack<float, float>(packed, seq_starts, bs, mx, k, padded, s);
+  if (in_dtype == BT_BF16) return launch_unpack<__nv_bfloat16, __nv_bfloat16>(packed, seq_starts, bs, mx, k, padded, s);
+  return launch_unpack<float, __nv_bfloat16>(packed, seq_starts, bs, mx, k, padded, s);
 }
 
 }  // extern "C"

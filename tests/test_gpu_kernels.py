@@ -35,14 +35,15 @@ def torch_tanh(t):
     return torch.tanh(t)
 
 
-@pytest.mark.parametrize("bn", [64, 128, 256])
+@pytest.mark.parametrize("bn", [64, 128, 192, 256, -128, -192, -256])
 @pytest.mark.parametrize("epi", [0, 1, 2, 3])
-@pytest.mark.parametrize("M,N,K", [(1, 256, 64), (200, 768, 768), (2458, 2304, 768), (129, 1024, 4096)])
+@pytest.mark.parametrize("M,N,K", [(1, 768, 64), (200, 768, 768), (2458, 2304, 768), (129, 1024, 4096),
+                                   (300, 3072, 128)])
 def test_gemm(env, bn, epi, M, N, K):
     bt, torch = env
     from paper_2210_03052_b200.tensor import gemm_device
 
-    if N % bn:
+    if N % abs(bn):
         pytest.skip("N not a multiple of BN")
     a = (torch.randn(M, K, device="cuda") * 0.5).to(torch.bfloat16)
     w = (torch.randn(N, K, device="cuda") / math.sqrt(K)).to(torch.bfloat16)
