@@ -191,6 +191,8 @@ BT_API int bt_mha_varlen_path(const void* qkv, const int32_t* seq_starts, int bs
 BT_API int bt_debug_gemm_trace(unsigned long long* buf);
 /* Debug hook: 0 normal, 1 = GEMMs skip the MMAs, 2 = GEMMs skip the TMA loads (results invalid in 1/2). */
 BT_API int bt_debug_gemm_mode(int mode);
+/* Debug hook: per-CTA globaltimer event trace of the MHA kernels (32 u64 slots per CTA). */
+BT_API int bt_debug_mha_trace(unsigned long long* buf);
 
 #ifdef __cplusplus
 }

@@ -11,53 +11,78 @@
 
 namespace bt {
 
-template <int NCH>
+template <int NCH, bool HOIST>
 __global__ void __launch_bounds__(256) ln_bias_residual_kernel(const __nv_bfloat16* __restrict__ x,
                                                                const __nv_bfloat16* __restrict__ res,
                                                                const float* __restrict__ bias,
                                                                const float* __restrict__ gamma,
                                                                const float* __restrict__ beta, float eps,
                                                                __nv_bfloat16* __restrict__ out, int T, int k) {
-  ptx::griddep_launch_dependents();
-  ptx::griddep_wait();
   const int lane = threadIdx.x & 31;
   const int wpb = blockDim.x >> 5;
   const int nchunk = k >> 3;
   const float inv_k = 1.0f / static_cast<float>(k);
+  // Parameters do not depend on the previous kernel: fetch them into
+  // registers before griddepcontrol.wait so their latency overlaps its tail.
+  // (HOIST = false for very wide rows, where the parameters would not fit in
+  // registers: they are then re-read per row from L1.)
+  float bv[NCH][8], gv[NCH][8], ev[NCH][8];
+  auto load_params = [&]() {
+#pragma unroll
+  for (int i = 0; i < NCH; ++i) {
+    const int c = lane + 32 * i;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) bv[i][e] = 0.f, gv[i][e] = 0.f, ev[i][e] = 0.f;
+    if (c < nchunk) {
+      const float4* g4 = reinterpret_cast<const float4*>(gamma) + 2 * c;
+      const float4* e4 = reinterpret_cast<const float4*>(beta) + 2 * c;
+      const float4 g0 = __ldg(g4), g1 = __ldg(g4 + 1), e0 = __ldg(e4), e1 = __ldg(e4 + 1);
+      gv[i][0] = g0.x; gv[i][1] = g0.y; gv[i][2] = g0.z; gv[i][3] = g0.w;
+      gv[i][4] = g1.x; gv[i][5] = g1.y; gv[i][6] = g1.z; gv[i][7] = g1.w;
+      ev[i][0] = e0.x; ev[i][1] = e0.y; ev[i][2] = e0.z; ev[i][3] = e0.w;
+      ev[i][4] = e1.x; ev[i][5] = e1.y; ev[i][6] = e1.z; ev[i][7] = e1.w;
+      if (bias) {
+        const float4* b4 = reinterpret_cast<const float4*>(bias) + 2 * c;
+        const float4 b0 = __ldg(b4), b1 = __ldg(b4 + 1);
+        bv[i][0] = b0.x; bv[i][1] = b0.y; bv[i][2] = b0.z; bv[i][3] = b0.w;
+        bv[i][4] = b1.x; bv[i][5] = b1.y; bv[i][6] = b1.z; bv[i][7] = b1.w;
+      }
+    }
+  }
+  };
+  if constexpr (HOIST) load_params();
+  ptx::griddep_launch_dependents();
+  ptx::griddep_wait();
   for (int row = blockIdx.x * wpb + (threadIdx.x >> 5); row < T; row += gridDim.x * wpb) {
     const size_t base = static_cast<size_t>(row) * k;
+    if constexpr (!HOIST) load_params();
+    uint4 xv[NCH], rv[NCH];
+#pragma unroll
+    for (int i = 0; i < NCH; ++i) {  // issue every load of the row before using any
+      const int c = lane + 32 * i;
+      xv[i] = make_uint4(0, 0, 0, 0);
+      rv[i] = make_uint4(0, 0, 0, 0);
+      if (c < nchunk) {
+        xv[i] = __ldg(reinterpret_cast<const uint4*>(x + base) + c);
+        if (res) rv[i] = __ldg(reinterpret_cast<const uint4*>(res + base) + c);
+      }
+    }
     float z[NCH][8];
     float sum = 0.f;
 #pragma unroll
     for (int i = 0; i < NCH; ++i) {
-      const int c = lane + 32 * i;
-      if (c < nchunk) {
-        const uint4 xv = __ldg(reinterpret_cast<const uint4*>(x + base) + c);
-        const __nv_bfloat162* xh = reinterpret_cast<const __nv_bfloat162*>(&xv);
-        uint4 rv = make_uint4(0, 0, 0, 0);
-        if (res) rv = __ldg(reinterpret_cast<const uint4*>(res + base) + c);
-        const __nv_bfloat162* rh = reinterpret_cast<const __nv_bfloat162*>(&rv);
-        float b[8];
-        if (bias) {
-          const float4 b0 = __ldg(reinterpret_cast<const float4*>(bias) + 2 * c);
-          const float4 b1 = __ldg(reinterpret_cast<const float4*>(bias) + 2 * c + 1);
-          b[0] = b0.x; b[1] = b0.y; b[2] = b0.z; b[3] = b0.w; b[4] = b1.x; b[5] = b1.y; b[6] = b1.z; b[7] = b1.w;
-        } else {
+      const __nv_bfloat162* xh = reinterpret_cast<const __nv_bfloat162*>(&xv[i]);
+      const __nv_bfloat162* rh = reinterpret_cast<const __nv_bfloat162*>(&rv[i]);
 #pragma unroll
-          for (int e = 0; e < 8; ++e) b[e] = 0.f;
-        }
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float2 xf = __bfloat1622float2(xh[e]);
-          const float2 rf = __bfloat1622float2(rh[e]);
-          z[i][2 * e] = (xf.x + rf.x) + b[2 * e];  // (x + residual) + bias, fusion.py:96
-          z[i][2 * e + 1] = (xf.y + rf.y) + b[2 * e + 1];
-        }
+      for (int e = 0; e < 4; ++e) {
+        const float2 xf = __bfloat1622float2(xh[e]);
+        const float2 rf = __bfloat1622float2(rh[e]);
+        z[i][2 * e] = (xf.x + rf.x) + bv[i][2 * e];  // (x + residual) + bias, fusion.py:96
+        z[i][2 * e + 1] = (xf.y + rf.y) + bv[i][2 * e + 1];
+      }
+      if (lane + 32 * i < nchunk) {
 #pragma unroll
         for (int e = 0; e < 8; ++e) sum += z[i][e];
-      } else {
-#pragma unroll
-        for (int e = 0; e < 8; ++e) z[i][e] = 0.f;
       }
     }
 #pragma unroll
@@ -81,18 +106,12 @@ __global__ void __launch_bounds__(256) ln_bias_residual_kernel(const __nv_bfloat
     for (int i = 0; i < NCH; ++i) {
       const int c = lane + 32 * i;
       if (c < nchunk) {
-        const float4 g0 = __ldg(reinterpret_cast<const float4*>(gamma) + 2 * c);
-        const float4 g1 = __ldg(reinterpret_cast<const float4*>(gamma) + 2 * c + 1);
-        const float4 e0 = __ldg(reinterpret_cast<const float4*>(beta) + 2 * c);
-        const float4 e1 = __ldg(reinterpret_cast<const float4*>(beta) + 2 * c + 1);
-        const float g[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
-        const float be[8] = {e0.x, e0.y, e0.z, e0.w, e1.x, e1.y, e1.z, e1.w};
         uint4 o;
         uint32_t* ow = reinterpret_cast<uint32_t*>(&o);
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const float y0 = g[2 * e] * ((z[i][2 * e] - mean) * rstd) + be[2 * e];
-          const float y1 = g[2 * e + 1] * ((z[i][2 * e + 1] - mean) * rstd) + be[2 * e + 1];
+          const float y0 = gv[i][2 * e] * ((z[i][2 * e] - mean) * rstd) + ev[i][2 * e];
+          const float y1 = gv[i][2 * e + 1] * ((z[i][2 * e + 1] - mean) * rstd) + ev[i][2 * e + 1];
           ow[e] = ptx::pack_bf16x2(y0, y1);
         }
         reinterpret_cast<uint4*>(out + base)[c] = o;
@@ -109,8 +128,8 @@ static int launch_ln(const __nv_bfloat16* x, const __nv_bfloat16* r, const float
   long long grid = (T + wpb - 1) / wpb;
   if (grid > sms * 8LL) grid = sms * 8LL;
   if (grid < 1) grid = 1;
-  BT_LAUNCH(ln_bias_residual_kernel<NCH>, dim3(static_cast<int>(grid)), dim3(threads), 0, s, 1, x, r, b, g, be, eps,
-            out, T, k);
+  BT_LAUNCH((ln_bias_residual_kernel<NCH, (NCH <= 4)>), dim3(static_cast<int>(grid)), dim3(threads), 0, s, 1, x, r, b,
+            g, be, eps, out, T, k);
   return BT_OK;
 }
 

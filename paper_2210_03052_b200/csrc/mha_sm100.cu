@@ -2,24 +2,12 @@
 // reference attention.py:177-314).  Both kernels index the packed [T, 3k]
 // QKV tensor through seq_starts and never touch a padded token.
 //
-// One CTA = (q-tile of 128 rows, head, sequence); 4 warps, thread t owns
-// query row t of the tile == TMEM lane t, so row max / row sum are
-// thread-local (no shuffles) and the softmax reads S straight out of TMEM.
-//
-//   short path (max_seq_len <= cutoff, attention.py:177-237): the whole
-//     K/V head slab of the sequence (<= 384 keys) is TMA-staged in shared
-//     memory once, S = Q K^T for every key lands in TMEM (<= 384 fp32
-//     columns), the exact row softmax is taken over the full row (no
-//     rescaling, as the reference's tile-local softmax), P (bf16) is written
-//     to shared memory in the UMMA K-major 128B-swizzled layout and
-//     O = P V accumulates in TMEM.
-//   long path (max_seq_len > cutoff, attention.py:240-296): keys are streamed
-//     in 128-key blocks through a 2-deep TMA ring; the reference's
-//     "partial (max, sum) per 128-column tile + full reduction + exp on load"
-//     is carried out as the equivalent single-pass online softmax (per-block
-//     partial max/sum merged into running statistics), so P never goes to
-//     HBM.  Work per CTA is sized by the sequence's true length (grouped
-//     problem sizes).
+// One CTA = (q-tile of 128 rows, head, sequence): work is sized by each
+// sequence's true length (the grouped-problem view of the long path) and
+// q tiles past a sequence's end exit immediately.  Thread t of the softmax
+// warps owns query row t of the tile == TMEM lane t, so row max / row sum
+// are thread-local (no shuffles) and the softmax reads S straight out of
+// TMEM; P never goes to HBM.  See mha_fwd_kernel for the two paths.
 //
 // Q/K/V biases are already applied by the QKV GEMM epilogue.  d = 64.
 
@@ -35,12 +23,36 @@ constexpr int MHA_KB = 128;                  // keys per block (UMMA N of S)
 constexpr uint32_t MHA_TILE = 128 * 128;     // bytes of one 128 x 64 bf16 tile
 constexpr int MHA_SHORT_MAX_KEYS = 384;      // TMEM: 384 S columns + 64 O columns <= 512
 
+// Debug trace (off unless bt_debug_mha_trace installs a buffer): 32 u64
+// globaltimer stamps per CTA, CTA index = linear block id.
+//   [0] prologue done  [1] Q landed (MMA warp)  [2+2t] S(t) ready (softmax)
+//   [3+2t] item t done (softmax)  [30] O ready  [31] output stored
+__device__ unsigned long long* g_mha_trace = nullptr;
+#define MHA_TRACE(slot)                                                                                   \
+  do {                                                                                                    \
+    if (g_mha_trace && (slot) < 32) {                                                                     \
+      unsigned long long _t;                                                                              \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));                                              \
+      g_mha_trace[((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 32 + (slot)] = _t;   \
+    }                                                                                                     \
+  } while (0)
+
 struct MhaParams {
   const int32_t* seq_starts;
   __nv_bfloat16* out;
   int hidden;      // H * d
   float sl2;       // softmax scale * log2(e)
 };
+
+// Tie a register array to a preceding tcgen05.wait::ld.
+__device__ __forceinline__ void reg_tie(uint32_t (&r)[32]) {
+  asm volatile(""
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                 "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]),
+                 "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]),
+                 "+r"(r[29]), "+r"(r[30]), "+r"(r[31]));
+}
 
 // Write 32 consecutive bf16 P values (packed in 16 u32) of row `row`,
 // starting at key column `c` (multiple of 32), into the K-major SW128 layout:
@@ -68,189 +80,71 @@ __device__ __forceinline__ void store_out_row(const MhaParams& p, int grow, int 
   }
 }
 
-// ============================================================ short path
-template <int NKB>
-struct ShortCfg {
+// ============================================================ kernel
+// One template serves both reference paths:
+//   RESIDENT = true   short path (attention.py:177-237): all K/V blocks of the
+//                     sequence-head are TMA-staged once and stay in shared
+//                     memory for both passes (<= NST*128 keys).
+//   RESIDENT = false  long path (attention.py:240-296): 128-key K/V blocks
+//                     stream through an NST-deep ring, once per pass.
+// Both take the exact two-pass softmax of the reference: pass 1 computes the
+// row max over every key (the "partial max per 128-column tile + full
+// reduction" of the grouped path, tensor.py:166-173 / attention.py:104-122);
+// pass 2 forms P = exp(s - max) (masked past the sequence end), writes it
+// as bf16 to shared memory, and accumulates O += P V in TMEM with no
+// rescaling; O is divided by the row sum at the end.
+//
+// Warp roles (192 threads): warps 0-3 softmax / epilogue (thread = query row
+// = TMEM lane), warp 4 TMA producer, warp 5 MMA issuer; both issuer warps walk
+// their loops warp-uniformly and issue through elect.sync.  TMEM: S in
+// columns [0,128), O in [128,192) -> 256 columns, ~112 KB smem -> two CTAs per
+// SM, whose latency chains interleave.
+template <bool RESIDENT, int NST>
+struct MhaCfg {
   static constexpr uint32_t Q_OFF = 0;
-  static constexpr uint32_t K_OFF = MHA_TILE;
-  static constexpr uint32_t V_OFF = K_OFF + NKB * MHA_TILE;
-  static constexpr uint32_t P_OFF = V_OFF + NKB * MHA_TILE;
-  static constexpr uint32_t BAR_OFF = P_OFF + NKB * 2 * MHA_TILE;
-  static constexpr size_t SMEM = 1024 + BAR_OFF + 64;
+  static constexpr uint32_t KV_OFF = MHA_TILE;                      // slot s: K at +32K*s, V at +32K*s+16K
+  static constexpr uint32_t P_OFF = KV_OFF + NST * 2 * MHA_TILE;     // 128 x 128 bf16 = 2 tiles
+  static constexpr uint32_t BAR_OFF = P_OFF + 2 * MHA_TILE;
+  static constexpr size_t SMEM = BAR_OFF + 128;
 };
 
-template <int NKB>
-__global__ void __launch_bounds__(128, 1) mha_short_kernel(const __grid_constant__ CUtensorMap tm, const MhaParams p) {
-  using Cfg = ShortCfg<NKB>;
+template <bool RESIDENT, int NST>
+__global__ void __launch_bounds__(192) mha_fwd_kernel(const __grid_constant__ CUtensorMap tm, const MhaParams p) {
+  using Cfg = MhaCfg<RESIDENT, NST>;
   const int qt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
   const int s0 = __ldg(p.seq_starts + b);
   const int len = __ldg(p.seq_starts + b + 1) - s0;
   const int q0 = qt * MHA_QT;
   if (q0 >= len) return;  // CTA-uniform: this q tile is past the sequence
   const int nkb = (len + MHA_KB - 1) / MHA_KB;
+  const int n_items = 2 * nkb;  // pass 1 (max) then pass 2 (exp, P V) over the key blocks
 
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sQ = smem + Cfg::Q_OFF;
-  uint8_t* sK = smem + Cfg::K_OFF;
-  uint8_t* sV = smem + Cfg::V_OFF;
+  uint8_t* sKV = smem + Cfg::KV_OFF;
   uint8_t* sP = smem + Cfg::P_OFF;
-  uint64_t* ld_bar = reinterpret_cast<uint64_t*>(smem + Cfg::BAR_OFF);
-  uint64_t* mma_bar = ld_bar + 1;
-  uint32_t* holder = reinterpret_cast<uint32_t*>(ld_bar + 2);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::BAR_OFF);
+  uint64_t* q_full = bars;
+  uint64_t* kv_full = bars + 1;         // [NST]
+  uint64_t* kv_empty = bars + 1 + NST;  // [NST]
+  uint64_t* s_full = bars + 1 + 2 * NST;
+  uint64_t* s_free = s_full + 1;
+  uint64_t* pv_done = s_full + 2;
+  uint64_t* o_full = s_full + 3;
+  uint32_t* holder = reinterpret_cast<uint32_t*>(s_full + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     ptx::prefetch_tmap(&tm);
-    ptx::mbar_init(ld_bar, 1);
-    ptx::mbar_init(mma_bar, 1);
-    ptx::fence_mbar_init();
-  }
-  if (warp == 0) {
-    ptx::tmem_alloc(holder, 512);
-    ptx::tmem_relinquish();
-  }
-  ptx::tc_fence_before();
-  __syncthreads();
-  ptx::tc_fence_after();
-  const uint32_t tmem = *holder;
-  constexpr uint32_t O_COL = MHA_SHORT_MAX_KEYS;
-  ptx::griddep_launch_dependents();
-  ptx::griddep_wait();  // qkv is produced by the previous kernel
-
-  if (threadIdx.x == 0) {
-    // stage Q tile and the whole K/V head slab of this sequence
-    ptx::mbar_arrive_expect_tx(ld_bar, (1 + 2 * nkb) * MHA_TILE);
-    ptx::tma_load_2d(sQ, &tm, ld_bar, h * MHA_D, s0 + q0);
-    for (int j = 0; j < nkb; ++j) {
-      ptx::tma_load_2d(sK + j * MHA_TILE, &tm, ld_bar, p.hidden + h * MHA_D, s0 + j * MHA_KB);
-      ptx::tma_load_2d(sV + j * MHA_TILE, &tm, ld_bar, 2 * p.hidden + h * MHA_D, s0 + j * MHA_KB);
+    ptx::mbar_init(q_full, 1);
+    for (int i = 0; i < NST; ++i) {
+      ptx::mbar_init(&kv_full[i], 1);
+      ptx::mbar_init(&kv_empty[i], 1);
     }
-    ptx::mbar_wait(ld_bar, 0);
-    ptx::tc_fence_after();
-    constexpr uint32_t idesc_s = ptx::idesc_bf16(128, 128, false, false);
-    const uint32_t q_addr = ptx::smem_u32(sQ);
-    for (int j = 0; j < nkb; ++j) {
-      const uint32_t k_addr = ptx::smem_u32(sK + j * MHA_TILE);
-#pragma unroll
-      for (int kk = 0; kk < MHA_D / 16; ++kk)
-        ptx::mma_bf16_ss(tmem + j * MHA_KB, ptx::sdesc_sw128(q_addr + kk * 32, 1024, 16),
-                         ptx::sdesc_sw128(k_addr + kk * 32, 1024, 16), idesc_s, kk > 0);
-    }
-    ptx::mma_commit(mma_bar);
-  }
-  __syncwarp();
-  ptx::mbar_wait(mma_bar, 0);
-  ptx::tc_fence_after();
-
-  // ---- exact row softmax straight out of TMEM (thread = row)
-  const int row = warp * 32 + lane;
-  const uint32_t trow = tmem + (static_cast<uint32_t>(warp * 32) << 16);
-  const int kcols = nkb * MHA_KB;
-  float mrow = -INFINITY;
-  for (int c = 0; c < kcols; c += 32) {
-    uint32_t r[32];
-    ptx::tmem_ld32(trow + c, r);
-    ptx::tmem_wait_ld(r);
-#pragma unroll
-    for (int i = 0; i < 32; ++i)
-      if (c + i < len) mrow = fmaxf(mrow, __uint_as_float(r[i]));
-  }
-  const float msc = mrow * p.sl2;
-  float lsum = 0.f;
-  for (int c = 0; c < kcols; c += 32) {
-    uint32_t r[32];
-    ptx::tmem_ld32(trow + c, r);
-    ptx::tmem_wait_ld(r);
-    uint32_t pk[16];
-#pragma unroll
-    for (int i = 0; i < 32; i += 2) {
-      const float e0 = (c + i < len) ? ptx::ex2_approx(fmaf(__uint_as_float(r[i]), p.sl2, -msc)) : 0.f;
-      const float e1 = (c + i + 1 < len) ? ptx::ex2_approx(fmaf(__uint_as_float(r[i + 1]), p.sl2, -msc)) : 0.f;
-      lsum += e0 + e1;
-      pk[i / 2] = ptx::pack_bf16x2(e0, e1);
-    }
-    store_p32(sP, row, c, pk);
-  }
-  ptx::fence_proxy_async_smem();
-  ptx::tc_fence_before();
-  __syncthreads();
-  ptx::tc_fence_after();
-
-  if (threadIdx.x == 0) {
-    constexpr uint32_t idesc_o = ptx::idesc_bf16(128, MHA_D, false, true);  // P K-major, V MN-major
-    const uint32_t p_addr = ptx::smem_u32(sP);
-    const uint32_t v_addr = ptx::smem_u32(sV);
-    const int nks = (len + 15) / 16;
-    for (int ks = 0; ks < nks; ++ks) {
-      const uint64_t ad = ptx::sdesc_sw128(p_addr + (ks >> 2) * MHA_TILE + (ks & 3) * 32, 1024, 16);
-      const uint64_t bd = ptx::sdesc_sw128(v_addr + ks * 16 * 128, 1024, MHA_TILE);
-      ptx::mma_bf16_ss(tmem + O_COL, ad, bd, idesc_o, ks > 0);
-    }
-    ptx::mma_commit(mma_bar);
-  }
-  __syncwarp();
-  ptx::mbar_wait(mma_bar, 1);
-  ptx::tc_fence_after();
-  float o[64];
-  {
-    uint32_t r[32];
-    ptx::tmem_ld32(trow + O_COL, r);
-    ptx::tmem_wait_ld(r);
-#pragma unroll
-    for (int i = 0; i < 32; ++i) o[i] = __uint_as_float(r[i]);
-    ptx::tmem_ld32(trow + O_COL + 32, r);
-    ptx::tmem_wait_ld(r);
-#pragma unroll
-    for (int i = 0; i < 32; ++i) o[32 + i] = __uint_as_float(r[i]);
-  }
-  if (q0 + row < len) store_out_row(p, s0 + q0 + row, h, o, 1.0f / lsum);
-
-  ptx::tc_fence_before();
-  __syncthreads();
-  if (warp == 0) {
-    ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem, 512);
-  }
-}
-
-// ============================================================ long path
-struct LongCfg {
-  static constexpr uint32_t Q_OFF = 0;
-  static constexpr uint32_t K_OFF = MHA_TILE;          // 2 stages
-  static constexpr uint32_t V_OFF = K_OFF + 2 * MHA_TILE;
-  static constexpr uint32_t P_OFF = V_OFF + 2 * MHA_TILE;  // 128 keys = 2 column blocks
-  static constexpr uint32_t BAR_OFF = P_OFF + 2 * MHA_TILE;
-  static constexpr size_t SMEM = 1024 + BAR_OFF + 64;
-};
-
-__global__ void __launch_bounds__(128, 1) mha_long_kernel(const __grid_constant__ CUtensorMap tm, const MhaParams p) {
-  using Cfg = LongCfg;
-  const int qt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
-  const int s0 = __ldg(p.seq_starts + b);
-  const int len = __ldg(p.seq_starts + b + 1) - s0;
-  const int q0 = qt * MHA_QT;
-  if (q0 >= len) return;
-  const int nkb = (len + MHA_KB - 1) / MHA_KB;
-
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem + Cfg::Q_OFF;
-  uint8_t* sK = smem + Cfg::K_OFF;
-  uint8_t* sV = smem + Cfg::V_OFF;
-  uint8_t* sP = smem + Cfg::P_OFF;
-  uint64_t* kv_full = reinterpret_cast<uint64_t*>(smem + Cfg::BAR_OFF);  // [2]
-  uint64_t* s_bar = kv_full + 2;
-  uint64_t* pv_bar = kv_full + 3;
-  uint32_t* holder = reinterpret_cast<uint32_t*>(kv_full + 4);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    ptx::prefetch_tmap(&tm);
-    ptx::mbar_init(&kv_full[0], 1);
-    ptx::mbar_init(&kv_full[1], 1);
-    ptx::mbar_init(s_bar, 1);
-    ptx::mbar_init(pv_bar, 1);
+    ptx::mbar_init(s_full, 1);
+    ptx::mbar_init(s_free, 128);
+    ptx::mbar_init(pv_done, 1);
+    ptx::mbar_init(o_full, 1);
     ptx::fence_mbar_init();
   }
   if (warp == 0) {
@@ -263,124 +157,210 @@ __global__ void __launch_bounds__(128, 1) mha_long_kernel(const __grid_constant_
   const uint32_t tmem = *holder;
   constexpr uint32_t S_COL = 0, O_COL = 128;
   ptx::griddep_launch_dependents();
-  ptx::griddep_wait();  // qkv is produced by the previous kernel
-  constexpr uint32_t idesc_s = ptx::idesc_bf16(128, 128, false, false);
-  constexpr uint32_t idesc_o = ptx::idesc_bf16(128, MHA_D, false, true);
+  if (threadIdx.x == 0) MHA_TRACE(0);
 
-  if (threadIdx.x == 0) {
-    ptx::mbar_arrive_expect_tx(&kv_full[0], 3 * MHA_TILE);
-    ptx::tma_load_2d(sQ, &tm, &kv_full[0], h * MHA_D, s0 + q0);
-    ptx::tma_load_2d(sK, &tm, &kv_full[0], p.hidden + h * MHA_D, s0);
-    ptx::tma_load_2d(sV, &tm, &kv_full[0], 2 * p.hidden + h * MHA_D, s0);
-    if (nkb > 1) {
-      ptx::mbar_arrive_expect_tx(&kv_full[1], 2 * MHA_TILE);
-      ptx::tma_load_2d(sK + MHA_TILE, &tm, &kv_full[1], p.hidden + h * MHA_D, s0 + MHA_KB);
-      ptx::tma_load_2d(sV + MHA_TILE, &tm, &kv_full[1], 2 * p.hidden + h * MHA_D, s0 + MHA_KB);
+  if (warp == 4) {
+    // ------------------------------------------------ TMA producer
+    ptx::griddep_wait();  // qkv is produced by the previous kernel
+    if (ptx::elect_one()) {
+      ptx::mbar_arrive_expect_tx(q_full, MHA_TILE);
+      ptx::tma_load_2d(sQ, &tm, q_full, h * MHA_D, s0 + q0);
     }
-  }
-
-  const int row = warp * 32 + lane;
-  const uint32_t trow = tmem + (static_cast<uint32_t>(warp * 32) << 16);
-  float o[64];
+    __syncwarp();
+    if constexpr (RESIDENT) {
+      for (int j = 0; j < nkb; ++j) {
+        if (ptx::elect_one()) {
+          uint8_t* kv = sKV + j * 2 * MHA_TILE;
+          ptx::mbar_arrive_expect_tx(&kv_full[j], 2 * MHA_TILE);
+          ptx::tma_load_2d(kv, &tm, &kv_full[j], p.hidden + h * MHA_D, s0 + j * MHA_KB);
+          ptx::tma_load_2d(kv + MHA_TILE, &tm, &kv_full[j], 2 * p.hidden + h * MHA_D, s0 + j * MHA_KB);
+        }
+        __syncwarp();
+      }
+    } else {
+      for (int t = 0; t < n_items; ++t) {
+        const bool pass2 = t >= nkb;
+        const int j = pass2 ? t - nkb : t;
+        const int slot = t % NST;
+        ptx::mbar_wait(&kv_empty[slot], ((t / NST) & 1) ^ 1u);
+        if (ptx::elect_one()) {
+          uint8_t* kv = sKV + slot * 2 * MHA_TILE;
+          ptx::mbar_arrive_expect_tx(&kv_full[slot], pass2 ? 2 * MHA_TILE : MHA_TILE);
+          ptx::tma_load_2d(kv, &tm, &kv_full[slot], p.hidden + h * MHA_D, s0 + j * MHA_KB);
+          if (pass2) ptx::tma_load_2d(kv + MHA_TILE, &tm, &kv_full[slot], 2 * p.hidden + h * MHA_D, s0 + j * MHA_KB);
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp == 5) {
+    // ------------------------------------------------ MMA issuer
+    constexpr uint32_t idesc_s = ptx::idesc_bf16(128, MHA_KB, false, false);  // Q K^T, both K-major
+    constexpr uint32_t idesc_o = ptx::idesc_bf16(128, MHA_D, false, true);    // P (K-major) x V (MN-major)
+    const uint64_t q_desc = ptx::sdesc_sw128(ptx::smem_u32(sQ), 1024, 16);
+    const uint64_t p_desc = ptx::sdesc_sw128(ptx::smem_u32(sP), 1024, 16);
+    const uint32_t kv_base = ptx::smem_u32(sKV);
+    ptx::mbar_wait(q_full, 0);
+    if (lane == 0) MHA_TRACE(1);
+    int prev_slot = 0;
+    for (int t = 0; t <= n_items; ++t) {
+      const bool pass2 = t >= nkb;
+      const int j = pass2 ? t - nkb : t;
+      const int slot = RESIDENT ? j : t % NST;
+      if (t > 0) ptx::mbar_wait(s_free, (t - 1) & 1);  // softmax done with S(t-1) / P(t-1) is in smem
+      if (t < n_items) {
+        ptx::mbar_wait(&kv_full[slot], RESIDENT ? 0u : static_cast<uint32_t>((t / NST) & 1));
+        ptx::tc_fence_after();
+        const uint64_t k_desc = ptx::sdesc_sw128(kv_base + slot * 2 * MHA_TILE, 1024, 16);
+        if (ptx::elect_one()) {
 #pragma unroll
-  for (int i = 0; i < 64; ++i) o[i] = 0.f;
-  float mrow = -INFINITY, lsum = 0.f;
-  const uint32_t q_addr = ptx::smem_u32(sQ);
-  const uint32_t p_addr = ptx::smem_u32(sP);
-
-  for (int j = 0; j < nkb; ++j) {
-    const int st = j & 1;
-    const uint32_t par = j & 1;
-    if (threadIdx.x == 0) {
-      ptx::mbar_wait(&kv_full[st], (j >> 1) & 1);
+          for (int kk = 0; kk < MHA_D / 16; ++kk)
+            ptx::mma_bf16_ss(tmem + S_COL, q_desc + 2 * kk, k_desc + 2 * kk, idesc_s, kk > 0);
+          ptx::mma_commit(s_full);
+          if (!RESIDENT && !pass2) ptx::mma_commit(&kv_empty[slot]);  // K of this pass-1 block consumed
+        }
+        __syncwarp();
+      } else {
+        ptx::tc_fence_after();
+      }
+      if (t > nkb) {
+        // P(t-1) V(t-1): 128 keys in 8 steps of 16; V block is MN-major (keys x d)
+        const int pj = t - 1 - nkb;
+        const int nks = min(MHA_KB, len - pj * MHA_KB + 15) / 16;
+        const uint64_t v_desc = ptx::sdesc_sw128(kv_base + prev_slot * 2 * MHA_TILE + MHA_TILE, 1024, MHA_TILE);
+        if (ptx::elect_one()) {
+          for (int ks = 0; ks < nks; ++ks)
+            ptx::mma_bf16_ss(tmem + O_COL, p_desc + (ks >> 2) * (MHA_TILE >> 4) + (ks & 3) * 2,
+                             v_desc + ks * ((16 * 128) >> 4), idesc_o, (pj | ks) != 0);
+          ptx::mma_commit(pv_done);
+          if (!RESIDENT) ptx::mma_commit(&kv_empty[prev_slot]);
+          if (t == n_items) ptx::mma_commit(o_full);
+        }
+        __syncwarp();
+      }
+      prev_slot = slot;
+    }
+  } else {
+    // ------------------------------------------------ softmax (thread = query row = TMEM lane)
+    // Work is skipped warp-uniformly where it cannot matter: warps whose 32
+    // query rows all lie past the sequence end, and 32-key chunks past it.
+    const int row = warp * 32 + lane;
+    const bool warp_live = q0 + warp * 32 < len;
+    const uint32_t trow = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+    float mrow = -INFINITY, msc = 0.f, lsum = 0.f;
+    for (int t = 0; t < n_items; ++t) {
+      const bool pass2 = t >= nkb;
+      const int kbase = (pass2 ? t - nkb : t) * MHA_KB;
+      const int kvalid = min(MHA_KB, len - kbase);  // valid keys in this block (>= 1)
+      ptx::mbar_wait(s_full, t & 1);
       ptx::tc_fence_after();
-      const uint32_t k_addr = ptx::smem_u32(sK + st * MHA_TILE);
+      if (threadIdx.x == 0) MHA_TRACE(2 + 2 * t);
+      if (!pass2) {
+        if (warp_live) {
+#pragma unroll 1
+          for (int c = 0; c < kvalid; c += 64) {
+            uint32_t r0[32], r1[32];
+            ptx::tmem_ld32(trow + S_COL + c, r0);
+            ptx::tmem_ld32(trow + S_COL + c + 32, r1);
+            ptx::tmem_wait_ld(r0);
+            reg_tie(r1);
 #pragma unroll
-      for (int kk = 0; kk < MHA_D / 16; ++kk)
-        ptx::mma_bf16_ss(tmem + S_COL, ptx::sdesc_sw128(q_addr + kk * 32, 1024, 16),
-                         ptx::sdesc_sw128(k_addr + kk * 32, 1024, 16), idesc_s, kk > 0);
-      ptx::mma_commit(s_bar);
-    }
-    __syncwarp();
-    ptx::mbar_wait(s_bar, par);
-    ptx::tc_fence_after();
-
-    // per-block partial max (reference: per-128-column tile partials,
-    // tensor.py:166-173) merged into the running row statistics
-    const int kbase = j * MHA_KB;
-    float bmax = -INFINITY;
-    for (int c = 0; c < MHA_KB; c += 32) {
-      uint32_t r[32];
-      ptx::tmem_ld32(trow + S_COL + c, r);
-      ptx::tmem_wait_ld(r);
+            for (int i = 0; i < 32; ++i) {
+              if (c + i < kvalid) mrow = fmaxf(mrow, __uint_as_float(r0[i]));
+              if (c + 32 + i < kvalid) mrow = fmaxf(mrow, __uint_as_float(r1[i]));
+            }
+          }
+        }
+        if (t == nkb - 1) msc = mrow * p.sl2;
+      } else {
+        if (t > nkb) ptx::mbar_wait(pv_done, (t - 1 - nkb) & 1);  // P V of the previous block has read sP
+        if (warp_live) {
+#pragma unroll 1
+          for (int c = 0; c < MHA_KB; c += 64) {
+            uint32_t pk[32];
+            if (c < kvalid) {
+              uint32_t r0[32], r1[32];
+              ptx::tmem_ld32(trow + S_COL + c, r0);
+              ptx::tmem_ld32(trow + S_COL + c + 32, r1);
+              ptx::tmem_wait_ld(r0);
+              reg_tie(r1);
 #pragma unroll
-      for (int i = 0; i < 32; ++i)
-        if (kbase + c + i < len) bmax = fmaxf(bmax, __uint_as_float(r[i]));
-    }
-    const float mnew = fmaxf(mrow, bmax);
-    const float alpha = ptx::ex2_approx((mrow - mnew) * p.sl2);  // 0 on the first block
-    const float msc = mnew * p.sl2;
-    float bsum = 0.f;
-    for (int c = 0; c < MHA_KB; c += 32) {
-      uint32_t r[32];
-      ptx::tmem_ld32(trow + S_COL + c, r);
-      ptx::tmem_wait_ld(r);
-      uint32_t pk[16];
+              for (int i = 0; i < 32; i += 2) {
+                const float e0 = (c + i < kvalid) ? ptx::ex2_approx(fmaf(__uint_as_float(r0[i]), p.sl2, -msc)) : 0.f;
+                const float e1 =
+                    (c + i + 1 < kvalid) ? ptx::ex2_approx(fmaf(__uint_as_float(r0[i + 1]), p.sl2, -msc)) : 0.f;
+                lsum += e0 + e1;
+                pk[i / 2] = ptx::pack_bf16x2(e0, e1);
+              }
+              if (c + 32 < kvalid) {
 #pragma unroll
-      for (int i = 0; i < 32; i += 2) {
-        const float e0 =
-            (kbase + c + i < len) ? ptx::ex2_approx(fmaf(__uint_as_float(r[i]), p.sl2, -msc)) : 0.f;
-        const float e1 =
-            (kbase + c + i + 1 < len) ? ptx::ex2_approx(fmaf(__uint_as_float(r[i + 1]), p.sl2, -msc)) : 0.f;
-        bsum += e0 + e1;
-        pk[i / 2] = ptx::pack_bf16x2(e0, e1);
+                for (int i = 0; i < 32; i += 2) {
+                  const float e0 =
+                      (c + 32 + i < kvalid) ? ptx::ex2_approx(fmaf(__uint_as_float(r1[i]), p.sl2, -msc)) : 0.f;
+                  const float e1 =
+                      (c + 33 + i < kvalid) ? ptx::ex2_approx(fmaf(__uint_as_float(r1[i + 1]), p.sl2, -msc)) : 0.f;
+                  lsum += e0 + e1;
+                  pk[16 + i / 2] = ptx::pack_bf16x2(e0, e1);
+                }
+              } else {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) pk[16 + i] = 0u;
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) pk[i] = 0u;
+            }
+            // keys [c, c+64) == one 64-key column block of the K-major SW128 P tile
+            uint8_t* blk = sP + (c >> 6) * MHA_TILE + row * 128;
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              *reinterpret_cast<uint4*>(blk + ((j ^ (row & 7)) << 4)) =
+                  make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+          }
+        }
+        ptx::fence_proxy_async_smem();
       }
-      store_p32(sP, row, c, pk);
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(s_free);
+      if (threadIdx.x == 0) MHA_TRACE(3 + 2 * t);
     }
-    lsum = lsum * alpha + bsum;
-    mrow = mnew;
-#pragma unroll
-    for (int i = 0; i < 64; ++i) o[i] *= alpha;
-
-    ptx::fence_proxy_async_smem();
-    ptx::tc_fence_before();
-    __syncthreads();
+    ptx::mbar_wait(o_full, 0);
     ptx::tc_fence_after();
-    if (threadIdx.x == 0) {
-      const uint32_t v_addr = ptx::smem_u32(sV + st * MHA_TILE);
-      const int nks = min(MHA_KB, len - kbase + 15) / 16;
-      for (int ks = 0; ks < nks; ++ks) {
-        const uint64_t ad = ptx::sdesc_sw128(p_addr + (ks >> 2) * MHA_TILE + (ks & 3) * 32, 1024, 16);
-        const uint64_t bd = ptx::sdesc_sw128(v_addr + ks * 16 * 128, 1024, MHA_TILE);
-        ptx::mma_bf16_ss(tmem + O_COL, ad, bd, idesc_o, ks > 0);
+    if (threadIdx.x == 0) MHA_TRACE(30);
+    // O (128 x 64 fp32 in TMEM) -> scaled bf16 rows staged in sP (free: every
+    // P V has completed) -> coalesced 16-byte stores, 4 rows per warp instruction
+    if (warp_live) {
+      uint32_t r0[32], r1[32];
+      ptx::tmem_ld32(trow + O_COL, r0);
+      ptx::tmem_ld32(trow + O_COL + 32, r1);
+      ptx::tmem_wait_ld(r0);
+      reg_tie(r1);
+      const float inv = (q0 + row < len) ? 1.0f / lsum : 0.f;
+      uint8_t* mine = sP + row * 128;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t* src = (j < 4) ? r0 + 8 * j : r1 + 8 * (j - 4);
+        uint4 v;
+        v.x = ptx::pack_bf16x2(__uint_as_float(src[0]) * inv, __uint_as_float(src[1]) * inv);
+        v.y = ptx::pack_bf16x2(__uint_as_float(src[2]) * inv, __uint_as_float(src[3]) * inv);
+        v.z = ptx::pack_bf16x2(__uint_as_float(src[4]) * inv, __uint_as_float(src[5]) * inv);
+        v.w = ptx::pack_bf16x2(__uint_as_float(src[6]) * inv, __uint_as_float(src[7]) * inv);
+        *reinterpret_cast<uint4*>(mine + ((j ^ (row & 7)) << 4)) = v;
       }
-      ptx::mma_commit(pv_bar);
-    }
-    __syncwarp();
-    ptx::mbar_wait(pv_bar, par);
-    ptx::tc_fence_after();
-    {
-      uint32_t r[32];
-      ptx::tmem_ld32(trow + O_COL, r);
-      ptx::tmem_wait_ld(r);
+      __syncwarp();
+      ptx::griddep_wait();  // out may still be read by the previous kernel
+      // lane -> (row in this warp's 32-row slab, 16 B chunk): 4 rows per instruction
 #pragma unroll
-      for (int i = 0; i < 32; ++i) o[i] += __uint_as_float(r[i]);
-      ptx::tmem_ld32(trow + O_COL + 32, r);
-      ptx::tmem_wait_ld(r);
-#pragma unroll
-      for (int i = 0; i < 32; ++i) o[32 + i] += __uint_as_float(r[i]);
+      for (int it = 0; it < 8; ++it) {
+        const int rr = warp * 32 + it * 4 + (lane >> 3);
+        const int j = lane & 7;
+        if (q0 + rr < len) {
+          const uint4 v = *reinterpret_cast<const uint4*>(sP + rr * 128 + ((j ^ (rr & 7)) << 4));
+          *reinterpret_cast<uint4*>(p.out + static_cast<size_t>(s0 + q0 + rr) * p.hidden + h * MHA_D + j * 8) = v;
+        }
+      }
     }
-    // stage st is free (its S and PV MMAs retired): prefetch block j + 2
-    if (threadIdx.x == 0 && j + 2 < nkb) {
-      ptx::mbar_arrive_expect_tx(&kv_full[st], 2 * MHA_TILE);
-      ptx::tma_load_2d(sK + st * MHA_TILE, &tm, &kv_full[st], p.hidden + h * MHA_D, s0 + (j + 2) * MHA_KB);
-      ptx::tma_load_2d(sV + st * MHA_TILE, &tm, &kv_full[st], 2 * p.hidden + h * MHA_D, s0 + (j + 2) * MHA_KB);
-    }
-    ptx::tc_fence_before();
-    __syncthreads();  // S / O_part TMEM and sP are reused by the next block
-    ptx::tc_fence_after();
+    if (threadIdx.x == 0) MHA_TRACE(31);
   }
-  if (q0 + row < len) store_out_row(p, s0 + q0 + row, h, o, 1.0f / lsum);
 
   ptx::tc_fence_before();
   __syncthreads();
@@ -409,34 +389,34 @@ int mha_launch(const void* qkv, const int32_t* seq_starts, int bs, int mx, int H
   p.hidden = hidden;
   p.sl2 = 1.4426950408889634f / sqrtf(static_cast<float>(d));
   const dim3 grid((mx + MHA_QT - 1) / MHA_QT, H, bs);
-  // dispatch_mha rule (attention.py:309-314); the on-chip short kernel holds
-  // at most 384 keys.
+  // dispatch_mha rule (attention.py:309-314); the resident (short) kernel
+  // holds at most 384 keys on chip.
   bool use_short = mx <= cutoff && mx <= MHA_SHORT_MAX_KEYS;
   if (force_path == 1) use_short = true;
   if (force_path == 2) use_short = false;
   BT_REQUIRE(!use_short || mx <= MHA_SHORT_MAX_KEYS, BT_ECONFIG, "short MHA holds <= 384 keys, mx=%d", mx);
-  if (use_short) {
-    const int nkb = (mx + MHA_KB - 1) / MHA_KB;
-    static bool set1 = false, set2 = false, set3 = false;
-    if (nkb == 1) {
-      if (!set1) { BT_TRY(set_smem(mha_short_kernel<1>, ShortCfg<1>::SMEM)); set1 = true; }
-      BT_LAUNCH(mha_short_kernel<1>, grid, dim3(128), ShortCfg<1>::SMEM, s, 1, tm, p);
-    } else if (nkb == 2) {
-      if (!set2) { BT_TRY(set_smem(mha_short_kernel<2>, ShortCfg<2>::SMEM)); set2 = true; }
-      BT_LAUNCH(mha_short_kernel<2>, grid, dim3(128), ShortCfg<2>::SMEM, s, 1, tm, p);
-    } else {
-      if (!set3) { BT_TRY(set_smem(mha_short_kernel<3>, ShortCfg<3>::SMEM)); set3 = true; }
-      BT_LAUNCH(mha_short_kernel<3>, grid, dim3(128), ShortCfg<3>::SMEM, s, 1, tm, p);
-    }
+  if (use_short && mx <= 2 * MHA_KB) {
+    static bool set = false;
+    if (!set) { BT_TRY(set_smem(mha_fwd_kernel<true, 2>, MhaCfg<true, 2>::SMEM)); set = true; }
+    BT_LAUNCH((mha_fwd_kernel<true, 2>), grid, dim3(192), MhaCfg<true, 2>::SMEM, s, 1, tm, p);
+  } else if (use_short) {
+    static bool set = false;
+    if (!set) { BT_TRY(set_smem(mha_fwd_kernel<true, 3>, MhaCfg<true, 3>::SMEM)); set = true; }
+    BT_LAUNCH((mha_fwd_kernel<true, 3>), grid, dim3(192), MhaCfg<true, 3>::SMEM, s, 1, tm, p);
   } else {
-    static bool setl = false;
-    if (!setl) { BT_TRY(set_smem(mha_long_kernel, LongCfg::SMEM)); setl = true; }
-    BT_LAUNCH(mha_long_kernel, grid, dim3(128), LongCfg::SMEM, s, 1, tm, p);
+    static bool set = false;
+    if (!set) { BT_TRY(set_smem(mha_fwd_kernel<false, 2>, MhaCfg<false, 2>::SMEM)); set = true; }
+    BT_LAUNCH((mha_fwd_kernel<false, 2>), grid, dim3(192), MhaCfg<false, 2>::SMEM, s, 1, tm, p);
   }
   return BT_OK;
 }
 
 }  // namespace bt
+
+extern "C" int bt_debug_mha_trace(unsigned long long* buf) {
+  BT_CUDA_CHECK(cudaMemcpyToSymbol(bt::g_mha_trace, &buf, sizeof(buf)));
+  return BT_OK;
+}
 
 extern "C" int bt_mha_varlen(const void* qkv, const int32_t* seq_starts, int bs, int mx, int H, int d, int cutoff,
                              int split_seq_len, void* out, int T, bt_stream_t stream) {

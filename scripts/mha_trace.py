@@ -1,0 +1,68 @@
+"""Per-CTA event timeline of one MHA launch (globaltimer ns).
+
+    python scripts/mha_trace.py c2|c3
+"""
+
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+
+def main():
+    import numpy as np
+    import torch
+
+    from paper_2210_03052_b200 import _lib, harness
+    from paper_2210_03052_b200.attention import mha_device
+    from paper_2210_03052_b200.packing import plan_for_lengths
+
+    _lib.require_device()
+    bs, mx, H = {"c2": (16, 256, 12), "c3": (16, 512, 16)}[sys.argv[1]]
+    seqs = harness.gen_lengths(bs, mx, "fixed", seed=0, alpha=0.6)
+    plan = plan_for_lengths(seqs)
+    qkv = torch.randn(plan.valid_word_cnt, 3 * H * 64, device="cuda").to(torch.bfloat16)
+    for _ in range(3):
+        mha_device(qkv, plan, H, 64)
+    nq = (mx + 127) // 128
+    n = nq * H * bs
+    buf = torch.zeros(n * 32, dtype=torch.int64, device="cuda")
+    _lib.call("bt_debug_mha_trace", buf.data_ptr())
+    mha_device(qkv, plan, H, 64)
+    torch.cuda.synchronize()
+    _lib.call("bt_debug_mha_trace", 0)
+    t = buf.view(n, 32).cpu().numpy()
+    used = t[:, 0] > 0
+    t0 = t[used, 0].min()
+    r = lambda x: (x - t0) / 1e3  # noqa: E731
+    starts = r(t[used, 0])
+    ends = r(t[used, 31])
+    print(f"{sys.argv[1]}: CTAs active {used.sum()} of {n}; start spread {starts.min():.2f}..{starts.max():.2f} us;"
+          f" end {ends.min():.2f}..{ends.max():.2f} us; per-CTA duration median {np.median(ends - starts):.2f} us")
+    lens = seqs.lengths
+    for c in np.nonzero(used)[0][:4].tolist() + np.nonzero(used)[0][-2:].tolist():
+        row = t[c]
+        qt, rest = c % nq, c // nq
+        h, b = rest % H, rest // H
+        s = f"cta q{qt} h{h} b{b} len {lens[b]}: start {r(row[0]):.2f} Q {r(row[1]):.2f} |"
+        for i in range(14):
+            if row[2 + 2 * i] == 0:
+                break
+            s += f" S{i} {r(row[2 + 2 * i]):.2f}-{r(row[3 + 2 * i]):.2f}"
+        s += f" | O {r(row[30]):.2f} st {r(row[31]):.2f}"
+        print(s)
+    q_lat = t[used, 1] - t[used, 0]
+    print(f"Q-load latency median {np.median(q_lat) / 1e3:.2f} us")
+    s0 = t[used, 2] - t[used, 1]
+    print(f"Q->S0 ready median {np.median(s0) / 1e3:.2f} us")
+    soft = [(t[c, 3 + 2 * i] - t[c, 2 + 2 * i]) / 1e3 for c in np.nonzero(used)[0] for i in range(14)
+            if t[c, 2 + 2 * i] > 0 and t[c, 3 + 2 * i] > 0]
+    gaps = [(t[c, 2 + 2 * (i + 1)] - t[c, 3 + 2 * i]) / 1e3 for c in np.nonzero(used)[0] for i in range(13)
+            if t[c, 2 + 2 * (i + 1)] > 0 and t[c, 3 + 2 * i] > 0]
+    print(f"softmax per item median {np.median(soft):.2f} us; item-done -> next S ready median {np.median(gaps):.2f} us")
+    fin = [(t[c, 31] - t[c, 30]) / 1e3 for c in np.nonzero(used)[0]]
+    print(f"O ready -> stored median {np.median(fin):.2f} us")
+
+
+if __name__ == "__main__":
+    main()
