@@ -109,6 +109,14 @@ BT_API int bt_gemm(const void* A, const void* Bt, const float* bias, const void*
 BT_API int bt_mha_varlen(const void* qkv, const int32_t* seq_starts, int bs, int mx, int H, int d, int cutoff,
                   int split_seq_len, void* out, int T, bt_stream_t stream);
 
+/* mha_baseline (attention.py:135-174): the same attention over the PADDED
+ * layout, qkv bf16 [bs*mx, 3*H*d] (biases applied), out bf16 [bs*mx, H*d].
+ * The whole mx x mx rectangle is computed (the unfused baseline's cost),
+ * keys >= len[b] are masked out of the softmax and query rows >= len[b] are
+ * written as zeros.  seq_starts supplies the lengths. */
+BT_API int bt_mha_padded(const void* qkv, const int32_t* seq_starts, int bs, int mx, int H, int d, void* out,
+                         bt_stream_t stream);
+
 /* ---- add-bias + residual + LayerNorm (fusion.py:79-98) ----------------- */
 
 /* out = LN((x + residual) + bias) * gamma + beta, row-wise over k columns,

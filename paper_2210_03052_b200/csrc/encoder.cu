@@ -18,7 +18,7 @@ namespace bt {
 int gemm_launch(const void* A, const void* Bt, const float* bias, const void* residual, void* C, int M, int N, int K,
                 int epi, int force_bn, cudaStream_t s);
 int mha_launch(const void* qkv, const int32_t* seq_starts, int bs, int mx, int H, int d, int cutoff, int T, void* out,
-               int force_path, cudaStream_t s);
+               int force_path, cudaStream_t s, int padded);
 
 static inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
@@ -85,7 +85,7 @@ extern "C" int bt_encoder_layer(const bt_layer_weights* w, const bt_layer_cfg* c
 
   BT_TRY(bt::gemm_launch(x, w->qkv_w, w->qkv_b, nullptr, L.qkv, T, 3 * k, k, BT_EPI_BIAS, 0, s));
   BT_TRY(bt::mha_launch(L.qkv, seq_starts, bs, cfg->max_seq_len, cfg->head_num, cfg->head_size, cfg->cutoff, T, L.ctx,
-                        0, s));
+                        0, s, 0));
   BT_TRY(bt::gemm_launch(L.ctx, w->ao_w, nullptr, nullptr, L.proj, T, k, k, BT_EPI_NONE, 0, s));
   BT_TRY(bt_ln_bias_residual(L.proj, x, w->ao_b, w->ln0_g, w->ln0_b, w->ln0_eps, L.y0, T, k, stream));
   BT_TRY(bt::gemm_launch(L.y0, w->w1, w->b1, nullptr, L.h1, T, f, k, BT_EPI_BIAS_GELU, 0, s));

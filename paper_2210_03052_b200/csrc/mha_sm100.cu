@@ -42,6 +42,8 @@ struct MhaParams {
   __nv_bfloat16* out;
   int hidden;      // H * d
   float sl2;       // softmax scale * log2(e)
+  int padded;      // 1: padded layout (reference mha_baseline, attention.py:135-174)
+  int mx;          // max_seq_len (row stride of a sequence in the padded layout)
 };
 
 // Tie a register array to a preceding tcgen05.wait::ld.
@@ -112,11 +114,18 @@ template <bool RESIDENT, int NST>
 __global__ void __launch_bounds__(192) mha_fwd_kernel(const __grid_constant__ CUtensorMap tm, const MhaParams p) {
   using Cfg = MhaCfg<RESIDENT, NST>;
   const int qt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
-  const int s0 = __ldg(p.seq_starts + b);
-  const int len = __ldg(p.seq_starts + b + 1) - s0;
+  const int sb = __ldg(p.seq_starts + b);
+  const int len = __ldg(p.seq_starts + b + 1) - sb;
+  // Packed layout: the sequence's rows start at seq_starts[b] and only its
+  // len rows / keys are touched.  Padded layout (the reference's unfused
+  // baseline): rows start at b*mx and the whole mx x mx rectangle is
+  // computed, keys >= len masked out of the softmax (exp -> 0, the -1e9 mask
+  // of attention.py:162-163) and query rows >= len written as zeros.
+  const int s0 = p.padded ? b * p.mx : sb;
+  const int work = p.padded ? p.mx : len;
   const int q0 = qt * MHA_QT;
-  if (q0 >= len) return;  // CTA-uniform: this q tile is past the sequence
-  const int nkb = (len + MHA_KB - 1) / MHA_KB;
+  if (q0 >= work) return;  // CTA-uniform: this q tile is past the sequence
+  const int nkb = (work + MHA_KB - 1) / MHA_KB;
   const int n_items = 2 * nkb;  // pass 1 (max) then pass 2 (exp, P V) over the key blocks
 
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -225,7 +234,7 @@ __global__ void __launch_bounds__(192) mha_fwd_kernel(const __grid_constant__ CU
       if (t > nkb) {
         // P(t-1) V(t-1): 128 keys in 8 steps of 16; V block is MN-major (keys x d)
         const int pj = t - 1 - nkb;
-        const int nks = min(MHA_KB, len - pj * MHA_KB + 15) / 16;
+        const int nks = min(MHA_KB, work - pj * MHA_KB + 15) / 16;
         const uint64_t v_desc = ptx::sdesc_sw128(kv_base + prev_slot * 2 * MHA_TILE + MHA_TILE, 1024, MHA_TILE);
         if (ptx::elect_one()) {
           for (int ks = 0; ks < nks; ++ks)
@@ -244,13 +253,13 @@ __global__ void __launch_bounds__(192) mha_fwd_kernel(const __grid_constant__ CU
     // Work is skipped warp-uniformly where it cannot matter: warps whose 32
     // query rows all lie past the sequence end, and 32-key chunks past it.
     const int row = warp * 32 + lane;
-    const bool warp_live = q0 + warp * 32 < len;
+    const bool warp_live = q0 + warp * 32 < work;
     const uint32_t trow = tmem + (static_cast<uint32_t>(warp * 32) << 16);
     float mrow = -INFINITY, msc = 0.f, lsum = 0.f;
     for (int t = 0; t < n_items; ++t) {
       const bool pass2 = t >= nkb;
       const int kbase = (pass2 ? t - nkb : t) * MHA_KB;
-      const int kvalid = min(MHA_KB, len - kbase);  // valid keys in this block (>= 1)
+      const int kvalid = min(MHA_KB, len - kbase);  // valid keys in this block (<= 0: all masked)
       ptx::mbar_wait(s_full, t & 1);
       ptx::tc_fence_after();
       if (threadIdx.x == 0) MHA_TRACE(2 + 2 * t);
@@ -353,7 +362,7 @@ __global__ void __launch_bounds__(192) mha_fwd_kernel(const __grid_constant__ CU
       for (int it = 0; it < 8; ++it) {
         const int rr = warp * 32 + it * 4 + (lane >> 3);
         const int j = lane & 7;
-        if (q0 + rr < len) {
+        if (q0 + rr < work) {
           const uint4 v = *reinterpret_cast<const uint4*>(sP + rr * 128 + ((j ^ (rr & 7)) << 4));
           *reinterpret_cast<uint4*>(p.out + static_cast<size_t>(s0 + q0 + rr) * p.hidden + h * MHA_D + j * 8) = v;
         }
@@ -377,7 +386,7 @@ static int set_smem(K kern, size_t bytes) {
 }
 
 int mha_launch(const void* qkv, const int32_t* seq_starts, int bs, int mx, int H, int d, int cutoff, int T,
-               void* out, int force_path, cudaStream_t s) {
+               void* out, int force_path, cudaStream_t s, int padded) {
   BT_REQUIRE(d == MHA_D, BT_ECONFIG, "fused MHA supports head_size 64, got %d", d);
   BT_REQUIRE(bs >= 1 && mx >= 1 && H >= 1 && T >= 1, BT_ESHAPE, "mha: bad shape bs=%d mx=%d H=%d T=%d", bs, mx, H, T);
   const int hidden = H * d;
@@ -388,6 +397,9 @@ int mha_launch(const void* qkv, const int32_t* seq_starts, int bs, int mx, int H
   p.out = static_cast<__nv_bfloat16*>(out);
   p.hidden = hidden;
   p.sl2 = 1.4426950408889634f / sqrtf(static_cast<float>(d));
+  p.padded = padded;
+  p.mx = mx;
+  BT_REQUIRE(!padded || T == bs * mx, BT_ESHAPE, "padded mha: qkv must have bs*mx = %d rows, got %d", bs * mx, T);
   const dim3 grid((mx + MHA_QT - 1) / MHA_QT, H, bs);
   // dispatch_mha rule (attention.py:309-314); the resident (short) kernel
   // holds at most 384 keys on chip.
@@ -421,11 +433,16 @@ extern "C" int bt_debug_mha_trace(unsigned long long* buf) {
 extern "C" int bt_mha_varlen(const void* qkv, const int32_t* seq_starts, int bs, int mx, int H, int d, int cutoff,
                              int split_seq_len, void* out, int T, bt_stream_t stream) {
   BT_REQUIRE(split_seq_len >= 1, BT_ESHAPE, "split_seq_len must be >= 1, got %d", split_seq_len);
-  return bt::mha_launch(qkv, seq_starts, bs, mx, H, d, cutoff, T, out, 0, bt::as_stream(stream));
+  return bt::mha_launch(qkv, seq_starts, bs, mx, H, d, cutoff, T, out, 0, bt::as_stream(stream), 0);
+}
+
+extern "C" int bt_mha_padded(const void* qkv, const int32_t* seq_starts, int bs, int mx, int H, int d, void* out,
+                             bt_stream_t stream) {
+  return bt::mha_launch(qkv, seq_starts, bs, mx, H, d, 384, bs * mx, out, 0, bt::as_stream(stream), 1);
 }
 
 // Test hook: force the short (1) or long (2) kernel regardless of cutoff.
 extern "C" int bt_mha_varlen_path(const void* qkv, const int32_t* seq_starts, int bs, int mx, int H, int d,
                                   void* out, int T, int path, bt_stream_t stream) {
-  return bt::mha_launch(qkv, seq_starts, bs, mx, H, d, 384, T, out, path, bt::as_stream(stream));
+  return bt::mha_launch(qkv, seq_starts, bs, mx, H, d, 384, T, out, path, bt::as_stream(stream), 0);
 }
