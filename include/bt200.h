@@ -176,12 +176,17 @@ BT_API int bt_encoder_layer(const bt_layer_weights* w, const bt_layer_cfg* cfg, 
 /* Scratch bytes bt_encoder_forward needs (plan + packed activations + layer scratch). */
 BT_API size_t bt_forward_workspace_bytes(const bt_layer_cfg* cfg, int bs, int T);
 
-/* forward (encoder.py:411-437): lengths (device int32[bs]) -> plan ->
+/* forward (encoder.py:411-437): lengths (int32[bs]) -> plan ->
  * pack(x_padded fp32 [bs*mx, k]) -> n_layers x encoder_layer -> unpack to
  * out_padded fp32 [bs*mx, k] with exact-zero padded rows.  `layers` is a
  * HOST array of n_layers weight structs (repeat one struct for ALBERT-style
  * sharing, encoder.py:130-131).  T = sum(lengths) must be supplied by the
- * caller (it is known on the host; no device->host sync happens).  */
+ * caller (it is known on the host; no device->host sync happens).
+ * lengths, x_padded and out_padded may be device memory or pinned
+ * (page-locked, UVA-mapped) HOST memory: the pack kernel then gathers only
+ * the valid input rows straight from host memory over PCIe and the unpack
+ * kernel writes the padded output straight into host memory -- the
+ * end-to-end path needs no separate bulk H2D / D2H copies.  */
 BT_API int bt_encoder_forward(const bt_layer_weights* layers, int n_layers, const bt_layer_cfg* cfg,
                        const int32_t* lengths, int bs, int T, const float* x_padded, float* out_padded,
                        void* ws, size_t ws_bytes, bt_stream_t stream);
@@ -201,6 +206,21 @@ BT_API int bt_debug_gemm_trace(unsigned long long* buf);
 BT_API int bt_debug_gemm_mode(int mode);
 /* Debug hook: per-CTA globaltimer event trace of the MHA kernels (32 u64 slots per CTA). */
 BT_API int bt_debug_mha_trace(unsigned long long* buf);
+
+/* forward on the packed layout: x_packed / out_packed fp32 [T, k] (device).
+ * Same pipeline as bt_encoder_forward minus the gather / scatter; the
+ * end-to-end host path DMAs only valid rows in and out (bt_copy_rows). */
+BT_API int bt_encoder_forward_packed(const bt_layer_weights* layers, int n_layers, const bt_layer_cfg* cfg,
+                                     const int32_t* lengths, int bs, int T, const float* x_packed, float* out_packed,
+                                     void* ws, size_t ws_bytes, bt_stream_t stream);
+
+/* pack / unpack as DMA: copy each sequence's valid rows between a padded
+ * buffer [bs*mx, row_bytes] and a packed one [T, row_bytes] with async
+ * cudaMemcpy (host or device memory on either side; lengths_host on the
+ * host).  to_packed = 1: padded -> packed, 0: packed -> padded (padded rows
+ * untouched). */
+BT_API int bt_copy_rows(void* dst, const void* src, const int32_t* lengths_host, int bs, int mx, long long row_bytes,
+                        int to_packed, bt_stream_t stream);
 
 #ifdef __cplusplus
 }

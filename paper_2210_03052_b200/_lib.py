@@ -64,6 +64,9 @@ SIGNATURES = {
     "bt_forward_workspace_bytes": (_SZ, [C.POINTER(LayerCfgC), _I, _I]),
     "bt_encoder_forward": (_I, [C.POINTER(LayerWeightsC), _I, C.POINTER(LayerCfgC), _P, _I, _I, _P, _P, _P, _SZ,
                                 _S]),
+    "bt_encoder_forward_packed": (_I, [C.POINTER(LayerWeightsC), _I, C.POINTER(LayerCfgC), _P, _I, _I, _P, _P,
+                                       _P, _SZ, _S]),
+    "bt_copy_rows": (_I, [_P, _P, _P, _I, _I, C.c_longlong, _I, _S]),
     "bt_bias_act": (_I, [_P, _I, _I, _P, _P, _I, _I, _I, _I, _I, _S]),
     "bt_add": (_I, [_P, _P, _P, _I, C.c_longlong, _S]),
     "bt_gemm_bn": (_I, [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _S]),

@@ -63,6 +63,7 @@ extern "C" int bt_ln_bias_residual(const void* x, const void* residual, const fl
 extern "C" int bt_pack(const void*, int, const int32_t*, int, int, void*, int, bt_stream_t);
 extern "C" int bt_unpack(const void*, int, const int32_t*, int, int, int, void*, int, bt_stream_t);
 extern "C" int bt_plan_lengths(const int32_t*, int, int, int32_t*, int32_t*, bt_stream_t);
+extern "C" int bt_bias_act(const void*, int, int, const float*, void*, int, int, int, int, int, bt_stream_t);
 
 extern "C" size_t bt_layer_workspace_bytes(const bt_layer_cfg* cfg, int T) {
   if (!cfg) return 0;
@@ -127,5 +128,61 @@ extern "C" int bt_encoder_forward(const bt_layer_weights* layers, int n_layers, 
   for (int li = 0; li < n_layers; ++li)
     BT_TRY(bt_encoder_layer(&layers[li], cfg, seq_starts, bs, T, x, lws, lws_bytes, stream));
   BT_TRY(bt_unpack(x, BT_BF16, seq_starts, bs, mx, k, out_padded, BT_F32, stream));
+  return BT_OK;
+}
+
+extern "C" int bt_encoder_forward_packed(const bt_layer_weights* layers, int n_layers, const bt_layer_cfg* cfg,
+                                         const int32_t* lengths, int bs, int T, const float* x_packed,
+                                         float* out_packed, void* ws, size_t ws_bytes, bt_stream_t stream) {
+  BT_TRY(bt::check_cfg(cfg));
+  BT_REQUIRE(n_layers >= 1 && layers != nullptr, BT_ECONFIG, "need >= 1 layer");
+  BT_REQUIRE(bs >= 1 && T >= 1 && T <= bs * cfg->max_seq_len, BT_ESHAPE, "forward_packed: bs=%d T=%d mx=%d", bs, T,
+             cfg->max_seq_len);
+  BT_REQUIRE(ws_bytes >= bt_forward_workspace_bytes(cfg, bs, T), BT_ESHAPE, "forward_packed: workspace too small");
+  const int k = cfg->head_num * cfg->head_size;
+  const int mx = cfg->max_seq_len;
+  uint8_t* p = static_cast<uint8_t*>(ws);
+  auto* seq_starts = reinterpret_cast<int32_t*>(p);
+  p += bt::align_up((bs + 1) * sizeof(int32_t));
+  p += bt::align_up(static_cast<size_t>(T) * sizeof(int32_t));  // offsets (unused: input already packed)
+  void* x = p;
+  p += bt::align_up(static_cast<size_t>(T) * k * 2);
+  void* lws = p;
+  const size_t lws_bytes = bt_layer_workspace_bytes(cfg, T);
+  BT_TRY(bt_plan_lengths(lengths, bs, mx, seq_starts, nullptr, stream));
+  BT_TRY(bt_bias_act(x_packed, BT_F32, k, nullptr, x, BT_BF16, k, T, k, 0, stream));  // fp32 -> bf16
+  for (int li = 0; li < n_layers; ++li)
+    BT_TRY(bt_encoder_layer(&layers[li], cfg, seq_starts, bs, T, x, lws, lws_bytes, stream));
+  BT_TRY(bt_bias_act(x, BT_BF16, k, nullptr, out_packed, BT_F32, k, T, k, 0, stream));  // bf16 -> fp32
+  return BT_OK;
+}
+
+// Copy the valid rows of each sequence between a padded host / device buffer
+// [bs*mx, row_bytes] and a packed one [T, row_bytes] with async DMA copies
+// (adjacent sequences that are contiguous on both sides are merged).
+extern "C" int bt_copy_rows(void* dst, const void* src, const int32_t* lengths_host, int bs, int mx,
+                            long long row_bytes, int to_packed, bt_stream_t stream) {
+  BT_REQUIRE(bs >= 1 && mx >= 1 && row_bytes > 0 && lengths_host, BT_ESHAPE, "copy_rows: bad arguments");
+  cudaStream_t s = bt::as_stream(stream);
+  long long packed_row = 0;
+  int b = 0;
+  while (b < bs) {
+    BT_REQUIRE(lengths_host[b] >= 1 && lengths_host[b] <= mx, BT_ESHAPE, "copy_rows: length %d out of range",
+               lengths_host[b]);
+    const long long padded_row = static_cast<long long>(b) * mx;
+    long long rows = lengths_host[b];
+    int e = b + 1;
+    while (e < bs && lengths_host[e - 1] == mx && lengths_host[e] >= 1) {  // contiguous run
+      rows += lengths_host[e];
+      ++e;
+      if (lengths_host[e - 1] != mx) break;
+    }
+    const size_t bytes = static_cast<size_t>(rows * row_bytes);
+    const char* s_ptr = static_cast<const char*>(src) + (to_packed ? padded_row : packed_row) * row_bytes;
+    char* d_ptr = static_cast<char*>(dst) + (to_packed ? packed_row : padded_row) * row_bytes;
+    BT_CUDA_CHECK(cudaMemcpyAsync(d_ptr, s_ptr, bytes, cudaMemcpyDefault, s));
+    packed_row += rows;
+    b = e;
+  }
   return BT_OK;
 }

@@ -3,27 +3,40 @@
 //
 //   C[M,N] = epilogue( A[M,K] * Bt[N,K]^T )     bf16 in, fp32 accumulate
 //
-//   warp 0      TMA producer: A/B k-blocks -> STAGES-deep smem ring (128B swizzle)
-//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
-//   warps 2..5  epilogue: tcgen05.ld (TMEM -> regs), bias / GELU / residual,
-//               bf16 pack -> 128B-swizzled smem staging -> TMA bulk store
+//   warp 0        TMA producer: A/B k-blocks -> STAGES-deep smem ring (128B swizzle)
+//   warp 1        TMEM allocator + tcgen05.mma issuer (elect.sync, warp-uniform loop)
+//   warps 2..     EW epilogue warps: tcgen05.ld (TMEM -> regs), bias / GELU /
+//                 residual, bf16 pack -> 128B-swizzled smem -> TMA bulk store
 //
-// Two tile shapes share one kernel template:
+// Tile shapes (one kernel template):
 //   PAIR = 1  one CTA, 128 x BN tile, tcgen05.mma.cta_group::1
 //   PAIR = 2  an SM pair (cluster of 2), 256 x BN tile, cta_group::2: each CTA
-//             loads its 128 rows of A and HALF of B's BN rows, the leader's
-//             MMA thread drives both tensor cores, each TMEM gets its rows.
+//             loads its 128 rows of A and HALF of B's BN rows; the leader's
+//             MMA thread drives both tensor cores; each TMEM gets its rows.
 // The accumulator is double-buffered in TMEM (2 x BN fp32 columns) so the
-// epilogue of tile i overlaps the mainloop of tile i+1.  BK = 64 (one 128B
-// swizzle atom of bf16).  Tiles are visited N-fastest so an A row block is
-// reused from L2 by every N tile before the next row block is touched.
+// epilogue of one work segment overlaps the mainloop of the next.  BK = 64.
 //
-// Why these shapes: with all operands of an encoder layer resident in the
-// 126 MB L2, the GEMMs are limited by how fast TMA can move A/B into shared
-// memory, so the tile shape that moves the fewest bytes per FLOP while still
-// filling the 148 SMs wins (see choose_tile); the 2-CTA pair halves B traffic
-// per SM.  Epilogue kinds mirror the reference EpilogueHook (tensor.py:74-106):
-// none / add_bias / add_bias_gelu (fusion.py:30-35) / bias+residual.
+// Work decomposition.  With every operand of a layer resident in the 126 MB
+// L2 these GEMMs are limited by the per-SM TMA feed (~55 B/clk measured), so
+// big low-traffic tiles (256 x 256 per SM pair) are the right shape -- but at
+// the encoder's small M (T = 2.5k-5k rows) they do not divide evenly over 74
+// SM pairs.  STREAMK = true splits the (tile, k-block) iteration space into
+// equal contiguous ranges, one per unit (pair / CTA).  A tile cut between
+// units is finished by the unit that owns its k-block 0 -- which processes it
+// as the LAST segment of its range, so the other contributors (which hold the
+// tile's later k-blocks at the START of their ranges) are done by then and
+// nobody waits: contributors write fp32 partials to a workspace slot and
+// release a flag; the finisher acquires the flags, adds the partials in a
+// fixed order (deterministic), applies the epilogue and resets the flags.
+// STREAMK = false visits whole tiles round-robin (large M).
+//
+// Tiles are visited N-fastest so an A row block is reused from L2 by every N
+// tile before the next row block is touched.  Epilogue kinds mirror the
+// reference EpilogueHook (tensor.py:74-106): none / add_bias / add_bias_gelu
+// (fusion.py:30-35) / bias+residual.
+
+#include <cstdlib>
+#include <map>
 
 #include "common.cuh"
 #include "ptx.cuh"
@@ -37,12 +50,16 @@ struct GemmParams {
   const float* bias;
   const __nv_bfloat16* residual;
   int num_m_blocks, num_n_blocks, num_tiles;
+  int num_k;           // K / 64
+  long long work;      // num_tiles * num_k (stream-K iteration space)
+  float* partials;     // stream-K: [unit][rank][128][BN] fp32
+  int* flags;          // stream-K: [unit][rank]
   int dbg;  // 0 normal; 1 = skip the MMAs (pure TMA feed); 2 = skip the TMA loads (pure MMA + epilogue)
 };
 
 // Optional per-CTA event trace (debug / profiling hook, off unless a buffer
 // is installed with bt_debug_gemm_trace): 64 u64 globaltimer stamps per CTA.
-//   [0] setup done, [1] producer start, then per tile it (< 10):
+//   [0] setup done, [1] producer start, then per segment it (< 10):
 //   [2+6it] mma begin, [3+6it] mma last commit, [4+6it] epi begin,
 //   [5+6it] epi end, [6+6it] tile id
 __device__ unsigned long long* g_gemm_trace = nullptr;
@@ -57,28 +74,72 @@ __device__ __forceinline__ unsigned long long gtimer() {
   } while (0)
 
 constexpr int GEMM_BK = 64;
-constexpr int GEMM_THREADS = 192;
 constexpr size_t GEMM_SMEM_LIMIT = 232448;  // 227 KB opt-in per CTA
+constexpr int MAX_UNITS = 148;              // stream-K workspace slots (one per CTA / pair)
 
 constexpr uint32_t pow2_cols(uint32_t c) { return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512; }
 
-template <int PAIR, int BN>
+template <int PAIR, int BN, int EW>
 struct GemmCfg {
-  static constexpr int BM = 128 * PAIR;  // rows per tile (per pair)
+  static constexpr int BM = 128 * PAIR;     // rows per tile (per pair)
   static constexpr int BN_CTA = BN / PAIR;  // B rows each CTA loads
+  static constexpr int THREADS = 64 + 32 * EW;
   static constexpr uint32_t A_BYTES = 128 * GEMM_BK * 2;
   static constexpr uint32_t B_BYTES = BN_CTA * GEMM_BK * 2;
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr uint32_t STAGING_BYTES = 4 * 2 * 32 * 128;  // 4 epilogue warps x 2 buffers x 32 rows x 128 B
+  static constexpr uint32_t STAGING_BYTES = EW * 2 * 32 * 128;  // per epilogue warp: 2 buffers x 32 rows x 128 B
   static constexpr int STAGES_FIT = static_cast<int>((GEMM_SMEM_LIMIT - 1024 - 256 - STAGING_BYTES) / STAGE_BYTES);
   static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
   static constexpr uint32_t TMEM_COLS = pow2_cols(2 * BN);
   static constexpr size_t SMEM = 1024 + static_cast<size_t>(STAGES) * STAGE_BYTES + STAGING_BYTES + 256;
   static_assert(SMEM <= GEMM_SMEM_LIMIT, "shared memory budget");
+  static_assert(STAGES >= 3, "pipeline too shallow");
 };
 
-// Tie a second register array to a preceding tcgen05.wait::ld (so no use of
-// it is scheduled above the wait).
+// A contiguous run of k-blocks of one tile.
+struct Seg {
+  int tile, kb0, kb1;
+};
+
+// The sequence of segments one unit (CTA or SM pair) processes; every warp
+// role walks the same sequence.
+struct SegIter {
+  long long pos, end;  // stream-K range
+  int tile, step;      // round-robin
+  bool streamk;
+  __device__ SegIter(const GemmParams& p, int unit, int num_units, bool sk) : streamk(sk) {
+    if (sk) {
+      pos = p.work * unit / num_units;
+      end = p.work * (unit + 1) / num_units;
+    } else {
+      tile = unit;
+      step = num_units;
+    }
+  }
+  __device__ bool next(const GemmParams& p, Seg& s) {
+    if (streamk) {
+      if (pos >= end) return false;
+      s.tile = static_cast<int>(pos / p.num_k);
+      s.kb0 = static_cast<int>(pos - static_cast<long long>(s.tile) * p.num_k);
+      const long long rem = end - pos;
+      s.kb1 = (p.num_k - s.kb0 <= rem) ? p.num_k : s.kb0 + static_cast<int>(rem);
+      pos += s.kb1 - s.kb0;
+      return true;
+    }
+    if (tile >= p.num_tiles) return false;
+    s.tile = tile;
+    s.kb0 = 0;
+    s.kb1 = p.num_k;
+    tile += step;
+    return true;
+  }
+};
+
+__device__ __forceinline__ long long unit_start(const GemmParams& p, int u, int num_units) {
+  return p.work * u / num_units;
+}
+
+// Tie a second register array to a preceding tcgen05.wait::ld.
 __device__ __forceinline__ void reg_fence(uint32_t (&r)[32]) {
   asm volatile(""
                : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
@@ -88,13 +149,14 @@ __device__ __forceinline__ void reg_fence(uint32_t (&r)[32]) {
                  "+r"(r[29]), "+r"(r[30]), "+r"(r[31]));
 }
 
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
 // Epilogue math on 32 consecutive columns of one row, packed to 16 bf16x2.
 template <int EPI>
-__device__ __forceinline__ void epi_math32(const uint32_t (&acc)[32], const GemmParams& p, int row, int col, bool row_ok,
+__device__ __forceinline__ void epi_math32(float (&v)[32], const GemmParams& p, int row, int col, bool row_ok,
                                            uint32_t* out16) {
-  float v[32];
-#pragma unroll
-  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(acc[i]);
   if constexpr (EPI == BT_EPI_BIAS_RESIDUAL) {
     if (row_ok) {
       const uint4* r = reinterpret_cast<const uint4*>(p.residual + static_cast<size_t>(row) * p.N + col);
@@ -130,46 +192,23 @@ __device__ __forceinline__ void epi_math32(const uint32_t (&acc)[32], const Gemm
   for (int i = 0; i < 16; ++i) out16[i] = ptx::pack_bf16x2(v[2 * i], v[2 * i + 1]);
 }
 
-// One epilogue warp drains its 32 TMEM lanes (rows) x BN columns of a tile:
-// 64 columns at a time -> swizzled 32 x 128 B smem buffer -> TMA store.
-template <int BN, int EPI>
-__device__ __forceinline__ void epilogue_rows(const GemmParams& p, const CUtensorMap* tmC, uint32_t taddr, int row0,
-                                              int col0, uint8_t* stage_buf, uint32_t& buf_ctr, int lane) {
-  const int row = row0 + lane;
-  const bool row_ok = row < p.M;
-#pragma unroll 1
-  for (int c = 0; c < BN; c += 64) {
-    uint32_t r0[32], r1[32];
-    ptx::tmem_ld32(taddr + c, r0);
-    ptx::tmem_ld32(taddr + c + 32, r1);
-    ptx::tmem_wait_ld(r0);
-    reg_fence(r1);
-    uint32_t pk[32];
-    epi_math32<EPI>(r0, p, row, col0 + c, row_ok, pk);
-    epi_math32<EPI>(r1, p, row, col0 + c + 32, row_ok, pk + 16);
-    uint8_t* buf = stage_buf + (buf_ctr & 1) * 4096;
-    if (lane == 0) ptx::bulk_wait_group_read<1>();  // the store issued from this buffer 2 chunks ago has read it
-    __syncwarp();
-    uint8_t* myrow = buf + lane * 128;
+// v[4q .. 4q+3] += the float4 at src[32 q] (the lane-contiguous partial layout)
+__device__ __forceinline__ void add_partial32(float (&v)[32], const float4* src) {
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
-      *reinterpret_cast<uint4*>(myrow + ((j ^ (lane & 7)) << 4)) =
-          make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
-    ptx::fence_proxy_async_smem();
-    __syncwarp();
-    if (lane == 0 && row0 < p.M) {
-      ptx::tma_store_2d(tmC, buf, col0 + c, row0);
-      ptx::bulk_commit_group();
-    }
-    ++buf_ctr;
+  for (int q = 0; q < 8; ++q) {
+    const float4 a = __ldcg(src + q * 32);  // L2 only: written by another SM in this launch
+    v[4 * q] += a.x;
+    v[4 * q + 1] += a.y;
+    v[4 * q + 2] += a.z;
+    v[4 * q + 3] += a.w;
   }
 }
 
-template <int PAIR, int BN, int EPI>
-__global__ void __launch_bounds__(GEMM_THREADS, 1)
+template <int PAIR, int BN, int EPI, int EW, bool STREAMK>
+__global__ void __launch_bounds__(GemmCfg<PAIR, BN, EW>::THREADS, 1)
     gemm_bf16_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                              const __grid_constant__ CUtensorMap tmC, const GemmParams p) {
-  using Cfg = GemmCfg<PAIR, BN>;
+  using Cfg = GemmCfg<PAIR, BN, EW>;
   constexpr int STAGES = Cfg::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -186,7 +225,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int lane = threadIdx.x & 31;
   const uint32_t rank = (PAIR == 2) ? ptx::cluster_ctarank() : 0;
   const bool leader = rank == 0;
-  const int num_k = p.K / GEMM_BK;
   const int unit = (PAIR == 2) ? (blockIdx.x >> 1) : blockIdx.x;  // pair / CTA index
   const int num_units = (PAIR == 2) ? (gridDim.x >> 1) : gridDim.x;
 
@@ -200,7 +238,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
-      ptx::mbar_init(&tempty[a], PAIR * 128);  // (leader's) every epilogue thread of the pair
+      ptx::mbar_init(&tempty[a], PAIR * EW * 32);  // (leader's) every epilogue thread of the pair
     }
     ptx::fence_mbar_init();
   }
@@ -229,20 +267,25 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     // control flow keeps addresses in uniform registers), one elected lane issues
     if (lane == 0) BT_TRACE(1, gtimer());
     const uint32_t full_leader = (PAIR == 2) ? ptx::mapa_shared(ptx::smem_u32(full), 0) : 0;
+    SegIter iter(p, unit, num_units, STREAMK);
+    Seg sg;
     // Weights (B) never depend on the previous kernel: issue the first
     // stages' B loads before griddepcontrol.wait so their DRAM latency
     // overlaps the previous kernel's tail; A follows after the wait.
-    const int pre = (unit < p.num_tiles && p.dbg != 2) ? (num_k < STAGES ? num_k : STAGES) : 0;
+    SegIter peek = iter;
+    Seg first{0, 0, 0};
+    const bool any = peek.next(p, first);
+    const int pre = (any && p.dbg != 2) ? min(first.kb1 - first.kb0, STAGES) : 0;
     if (pre > 0) {
-      const int brow0 = (unit % p.num_n_blocks) * BN + static_cast<int>(rank) * Cfg::BN_CTA;
-      for (int kb = 0; kb < pre; ++kb) {
+      const int brow0 = (first.tile % p.num_n_blocks) * BN + static_cast<int>(rank) * Cfg::BN_CTA;
+      for (int i = 0; i < pre; ++i) {
         if (ptx::elect_one()) {
           if constexpr (PAIR == 2) {
-            if (leader) ptx::mbar_arrive_expect_tx(&full[kb], PAIR * Cfg::STAGE_BYTES);
-            ptx::tma_load_2d_cg2(sB + kb * Cfg::B_BYTES, &tmB, full_leader + kb * 8, kb * GEMM_BK, brow0);
+            if (leader) ptx::mbar_arrive_expect_tx(&full[i], PAIR * Cfg::STAGE_BYTES);
+            ptx::tma_load_2d_cg2(sB + i * Cfg::B_BYTES, &tmB, full_leader + i * 8, (first.kb0 + i) * GEMM_BK, brow0);
           } else {
-            ptx::mbar_arrive_expect_tx(&full[kb], Cfg::STAGE_BYTES);
-            ptx::tma_load_2d(sB + kb * Cfg::B_BYTES, &tmB, &full[kb], kb * GEMM_BK, brow0);
+            ptx::mbar_arrive_expect_tx(&full[i], Cfg::STAGE_BYTES);
+            ptx::tma_load_2d(sB + i * Cfg::B_BYTES, &tmB, &full[i], (first.kb0 + i) * GEMM_BK, brow0);
           }
         }
         __syncwarp();
@@ -251,16 +294,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     ptx::griddep_wait();  // A (activations) is produced by the previous kernel
     int stage = 0;
     uint32_t phase = 0;
-    bool first = true;
-    for (int tile = unit; tile < p.num_tiles; tile += num_units, first = false) {
-      const int mb = tile / p.num_n_blocks;
-      const int nb = tile % p.num_n_blocks;
+    int count = 0;  // k-blocks issued so far by this CTA
+    while (iter.next(p, sg)) {
+      const int mb = sg.tile / p.num_n_blocks;
+      const int nb = sg.tile % p.num_n_blocks;
       const int arow = mb * Cfg::BM + static_cast<int>(rank) * 128;
       const int brow = nb * BN + static_cast<int>(rank) * Cfg::BN_CTA;
-      for (int kb = 0; kb < num_k; ++kb) {
+      for (int kb = sg.kb0; kb < sg.kb1; ++kb, ++count) {
         ptx::mbar_wait(&empty[stage], phase ^ 1u);
         if (ptx::elect_one()) {
-          const bool b_done = first && kb < pre;  // B (and expect_tx) already issued above
+          const bool b_done = count < pre;  // B (and expect_tx) already issued above
           if (p.dbg == 2) {
             if (leader) ptx::mbar_arrive(&full[stage]);
           } else if constexpr (PAIR == 2) {
@@ -295,14 +338,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int tile = unit; tile < p.num_tiles; tile += num_units, ++it) {
+      SegIter iter(p, unit, num_units, STREAMK);
+      Seg sg;
+      while (iter.next(p, sg)) {
         const int acc = it & 1;
         const uint32_t aphase = (it >> 1) & 1;
         ptx::mbar_wait(&tempty[acc], aphase ^ 1u);
         ptx::tc_fence_after();
         if (lane == 0) BT_TRACE(2 + 6 * it, gtimer());
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < num_k; ++kb) {
+        for (int kb = sg.kb0; kb < sg.kb1; ++kb) {
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
           const uint64_t ad0 = ptx::sdesc_sw128(a_base + stage * Cfg::A_BYTES, 1024, 16);
@@ -311,11 +356,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             if (p.dbg != 1) {
 #pragma unroll
               for (int k = 0; k < GEMM_BK / 16; ++k) {
-                // advancing K by 16 bf16 = 32 B inside the 128B swizzle atom: +2 in the start-address field
+                // K += 16 bf16 = 32 B inside the 128B swizzle atom: +2 in the start-address field
+                const uint32_t accum = (kb > sg.kb0 || k > 0) ? 1u : 0u;
                 if constexpr (PAIR == 2)
-                  ptx::mma_bf16_ss_cg2(d_tmem, ad0 + 2 * k, bd0 + 2 * k, idesc, (kb | k) != 0);
+                  ptx::mma_bf16_ss_cg2(d_tmem, ad0 + 2 * k, bd0 + 2 * k, idesc, accum);
                 else
-                  ptx::mma_bf16_ss(d_tmem, ad0 + 2 * k, bd0 + 2 * k, idesc, (kb | k) != 0);
+                  ptx::mma_bf16_ss(d_tmem, ad0 + 2 * k, bd0 + 2 * k, idesc, accum);
               }
             }
             if constexpr (PAIR == 2)
@@ -338,35 +384,139 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         __syncwarp();
         if (lane == 0) {
           BT_TRACE(3 + 6 * it, gtimer());
-          BT_TRACE(6 + 6 * it, tile);
+          BT_TRACE(6 + 6 * it, sg.tile);
         }
+        ++it;
       }
     }
   } else {
-    // ---------------- epilogue warps 2..5; warp w owns TMEM lanes 32*(w%4)
+    // ---------------- epilogue warps: warp w owns TMEM lanes 32*(w%4) (its 32
+    // rows) and every (EW/4)-th 64-column chunk starting at chunk (w-2)/4
+    const int ew = warp - 2;
     const int quarter = warp & 3;
-    uint8_t* stage_buf = sC + (warp - 2) * 8192;
+    const int colgrp = ew >> 2;
+    constexpr int NGRP = EW / 4;
+    uint8_t* stage_buf = sC + ew * 8192;
     const uint32_t tempty_leader = (PAIR == 2) ? ptx::mapa_shared(ptx::smem_u32(tempty), 0) : 0;
     uint32_t buf_ctr = 0;
     int it = 0;
     ptx::griddep_wait();  // C / residual may be read or written by the previous kernel
-    for (int tile = unit; tile < p.num_tiles; tile += num_units, ++it) {
+    SegIter iter(p, unit, num_units, STREAMK);
+    Seg sg;
+    while (iter.next(p, sg)) {
       const int acc = it & 1;
       const uint32_t aphase = (it >> 1) & 1;
-      const int mb = tile / p.num_n_blocks;
-      const int nb = tile % p.num_n_blocks;
+      const int mb = sg.tile / p.num_n_blocks;
+      const int nb = sg.tile % p.num_n_blocks;
       ptx::mbar_wait(&tfull[acc], aphase);
       ptx::tc_fence_after();
       if (threadIdx.x == 64) BT_TRACE(4 + 6 * it, gtimer());
       const int row0 = mb * Cfg::BM + static_cast<int>(rank) * 128 + quarter * 32;
+      const int row = row0 + lane;
+      const bool row_ok = row < p.M;
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN;
-      epilogue_rows<BN, EPI>(p, &tmC, taddr, row0, nb * BN, stage_buf, buf_ctr, lane);
+      const int lrow = quarter * 32 + lane;  // row within this CTA's 128
+
+      if (STREAMK && sg.kb0 > 0) {
+        // ---- contributor: park the fp32 partial in this unit's slot, release its flag.
+        // Layout (per CTA slot): [quarter][column group of 4][lane] float4, so a
+        // warp's store of one column group is 512 contiguous bytes.
+        float4* slot = reinterpret_cast<float4*>(p.partials) + (static_cast<size_t>(unit) * 2 + rank) * 128 * (BN / 4);
+#pragma unroll 1
+        for (int c = colgrp * 64; c < BN; c += 64 * NGRP) {
+          uint32_t r0[32], r1[32];
+          ptx::tmem_ld32(taddr + c, r0);
+          ptx::tmem_ld32(taddr + c + 32, r1);
+          ptx::tmem_wait_ld(r0);
+          reg_fence(r1);
+          float4* d4 = slot + (static_cast<size_t>(quarter) * (BN / 4) + c / 4) * 32 + lane;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            d4[q * 32] = make_float4(__uint_as_float(r0[4 * q]), __uint_as_float(r0[4 * q + 1]),
+                                     __uint_as_float(r0[4 * q + 2]), __uint_as_float(r0[4 * q + 3]));
+            d4[(8 + q) * 32] = make_float4(__uint_as_float(r1[4 * q]), __uint_as_float(r1[4 * q + 1]),
+                                           __uint_as_float(r1[4 * q + 2]), __uint_as_float(r1[4 * q + 3]));
+          }
+        }
+        __threadfence();
+        named_bar_sync(1, EW * 32);
+        if (ew == 0 && lane == 0) {
+          asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p.flags + unit * 2 + rank), "r"(1) : "memory");
+        }
+      } else {
+        // ---- full tile, or stream-K finisher (owns k-block 0): add the
+        // contributors' partials (units unit+1, unit+2, ... whose ranges start
+        // inside this tile) in unit order, then the epilogue
+        int ncontrib = 0;
+        if (STREAMK && sg.kb1 < p.num_k) {
+          const long long tile_end = static_cast<long long>(sg.tile + 1) * p.num_k;
+          while (unit + 1 + ncontrib < num_units && unit_start(p, unit + 1 + ncontrib, num_units) < tile_end)
+            ++ncontrib;
+          if (ew == 0 && lane == 0) {
+            for (int q = 1; q <= ncontrib; ++q) {
+              const int* f = p.flags + (unit + q) * 2 + rank;
+              int v = 0;
+              do {
+                asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+              } while (v == 0);
+            }
+            __threadfence();
+          }
+          named_bar_sync(1, EW * 32);
+        }
+#pragma unroll 1
+        for (int c = colgrp * 64; c < BN; c += 64 * NGRP) {
+          uint32_t r0[32], r1[32];
+          ptx::tmem_ld32(taddr + c, r0);
+          ptx::tmem_ld32(taddr + c + 32, r1);
+          ptx::tmem_wait_ld(r0);
+          reg_fence(r1);
+          float v0[32], v1[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            v0[i] = __uint_as_float(r0[i]);
+            v1[i] = __uint_as_float(r1[i]);
+          }
+          for (int q = 1; q <= ncontrib; ++q) {
+            const float4* src = reinterpret_cast<const float4*>(p.partials) +
+                                (static_cast<size_t>(unit + q) * 2 + rank) * 128 * (BN / 4) +
+                                (static_cast<size_t>(quarter) * (BN / 4) + c / 4) * 32 + lane;
+            add_partial32(v0, src);
+            add_partial32(v1, src + 8 * 32);
+          }
+          uint32_t pk[32];
+          const int col = nb * BN + c;
+          epi_math32<EPI>(v0, p, row, col, row_ok, pk);
+          epi_math32<EPI>(v1, p, row, col + 32, row_ok, pk + 16);
+          uint8_t* buf = stage_buf + (buf_ctr & 1) * 4096;
+          if (lane == 0) ptx::bulk_wait_group_read<1>();  // the store issued from this buffer 2 chunks ago has read it
+          __syncwarp();
+          uint8_t* myrow = buf + lane * 128;
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            *reinterpret_cast<uint4*>(myrow + ((j ^ (lane & 7)) << 4)) =
+                make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+          ptx::fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0 && row0 < p.M) {
+            ptx::tma_store_2d(&tmC, buf, col, row0);
+            ptx::bulk_commit_group();
+          }
+          ++buf_ctr;
+        }
+        if (ncontrib > 0) {
+          named_bar_sync(1, EW * 32);  // every epilogue thread has read the partials
+          if (ew == 0 && lane == 0)
+            for (int q = 1; q <= ncontrib; ++q) p.flags[(unit + q) * 2 + rank] = 0;  // ready for the next launch
+        }
+      }
       ptx::tc_fence_before();
       if constexpr (PAIR == 2)
         ptx::mbar_arrive_cluster(tempty_leader + acc * 8);
       else
         ptx::mbar_arrive(&tempty[acc]);
       if (threadIdx.x == 64) BT_TRACE(5 + 6 * it, gtimer());
+      ++it;
     }
     if (lane == 0) ptx::bulk_wait_group<0>();  // all of this warp's output stores complete
   }
@@ -386,84 +536,112 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   }
 }
 
-template <int PAIR, int BN, int EPI>
+// ------------------------------------------------------------------ host
+struct StreamKWorkspace {
+  float* partials = nullptr;
+  int* flags = nullptr;
+};
+
+static int streamk_workspace(StreamKWorkspace** out) {
+  static StreamKWorkspace ws;
+  if (!ws.partials) {
+    // one fp32 128 x 256 partial per (unit, rank) + one flag each; flags
+    // start at 0 and every finisher resets the flags it consumed
+    BT_CUDA_CHECK(cudaMalloc(&ws.partials, sizeof(float) * MAX_UNITS * 2 * 128 * 256));
+    BT_CUDA_CHECK(cudaMalloc(&ws.flags, sizeof(int) * MAX_UNITS * 2));
+    BT_CUDA_CHECK(cudaMemset(ws.flags, 0, sizeof(int) * MAX_UNITS * 2));
+  }
+  *out = &ws;
+  return BT_OK;
+}
+
+template <int PAIR, int BN, int EPI, int EW, bool SK>
 static int launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const GemmParams& p,
                          int units, cudaStream_t s) {
-  using Cfg = GemmCfg<PAIR, BN>;
-  auto kern = gemm_bf16_tcgen05_kernel<PAIR, BN, EPI>;
+  using Cfg = GemmCfg<PAIR, BN, EW>;
+  auto kern = gemm_bf16_tcgen05_kernel<PAIR, BN, EPI, EW, SK>;
   static bool attr_set = false;  // one flag per instantiation
   if (!attr_set) {
     BT_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Cfg::SMEM)));
     attr_set = true;
   }
-  BT_LAUNCH(kern, dim3(units * PAIR), dim3(GEMM_THREADS), Cfg::SMEM, s, PAIR, ta, tb, tc, p);
+  BT_LAUNCH(kern, dim3(units * PAIR), dim3(Cfg::THREADS), Cfg::SMEM, s, PAIR, ta, tb, tc, p);
   return BT_OK;
 }
 
-template <int PAIR, int BN>
+template <int PAIR, int BN, int EW, bool SK>
 static int dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
                         const GemmParams& p, int units, cudaStream_t s) {
   switch (epi) {
-    case BT_EPI_NONE: return launch_gemm_t<PAIR, BN, BT_EPI_NONE>(ta, tb, tc, p, units, s);
-    case BT_EPI_BIAS: return launch_gemm_t<PAIR, BN, BT_EPI_BIAS>(ta, tb, tc, p, units, s);
-    case BT_EPI_BIAS_GELU: return launch_gemm_t<PAIR, BN, BT_EPI_BIAS_GELU>(ta, tb, tc, p, units, s);
-    default: return launch_gemm_t<PAIR, BN, BT_EPI_BIAS_RESIDUAL>(ta, tb, tc, p, units, s);
+    case BT_EPI_NONE: return launch_gemm_t<PAIR, BN, BT_EPI_NONE, EW, SK>(ta, tb, tc, p, units, s);
+    case BT_EPI_BIAS: return launch_gemm_t<PAIR, BN, BT_EPI_BIAS, EW, SK>(ta, tb, tc, p, units, s);
+    case BT_EPI_BIAS_GELU: return launch_gemm_t<PAIR, BN, BT_EPI_BIAS_GELU, EW, SK>(ta, tb, tc, p, units, s);
+    default: return launch_gemm_t<PAIR, BN, BT_EPI_BIAS_RESIDUAL, EW, SK>(ta, tb, tc, p, units, s);
   }
 }
 
 struct GemmChoice {
-  int pair;  // 1 = one CTA 128 x bn tile, 2 = SM pair 256 x bn tile
+  int pair;     // 1 = one CTA 128 x bn tile, 2 = SM pair 256 x bn tile
   int bn;
+  bool streamk;
 };
 
-// Cost model (cycles): tiles run in waves of `slots` concurrent tiles.  A
-// wave lasts the longer of (a) one tile's MMA time and (b) its TMA feed time,
-// bytes per CTA per k-block at the measured per-SM rate (~32 KB per 620
-// cycles with the whole chip loading from L2), plus a fixed fill/epilogue
-// cost.
+// Cost model (SM cycles).  A k-block of a unit costs max(MMA time, TMA feed
+// time at ~55 B/clk/SM).  Round-robin: waves x per-tile time.  Stream-K:
+// ceil(work / units) k-blocks per unit plus a fix-up cost for split tiles.
+// Plus a fixed fill / drain cost.
 static GemmChoice choose_tile(int M, int N, int K, int sms) {
   struct Cand { int pair, bn; };
   const Cand cands[] = {{2, 256}, {2, 192}, {2, 128}, {1, 256}, {1, 192}, {1, 128}, {1, 64}};
-  GemmChoice best{1, 64};
+  GemmChoice best{1, 64, false};
   double best_cost = 1e300;
   const int nk = K / GEMM_BK;
   for (const Cand& c : cands) {
     if (N % c.bn) continue;
     const int bm = 128 * c.pair;
-    long long remaining = static_cast<long long>((M + bm - 1) / bm) * (N / c.bn);
-    const long long slots = sms / c.pair;
-    const double mma = nk * 4.0 * (128.0 * c.bn / 256.0);                       // MMA cycles per tile
-    const double feed = nk * (128.0 + c.bn / c.pair) * GEMM_BK * 2.0 / 52.0;   // TMA feed cycles per tile
-    const double per_tile = (mma > feed ? mma : feed);
-    double cost = 0.0;
-    while (remaining > 0) {
-      const long long active = remaining < slots ? remaining : slots;
-      cost += per_tile + 2500.0;
-      remaining -= active;
+    const long long tiles = static_cast<long long>((M + bm - 1) / bm) * (N / c.bn);
+    const long long units = sms / c.pair;
+    const double mma = 4.0 * (128.0 * c.bn / 256.0);                      // MMA cycles per k-block
+    const double feed = (128.0 + c.bn / c.pair) * GEMM_BK * 2.0 / 55.0;  // TMA cycles per k-block
+    const double kblk = mma > feed ? mma : feed;
+    const double fixed = 3000.0;
+    // round-robin over whole tiles
+    const long long waves = (tiles + units - 1) / units;
+    const double rr = waves * nk * kblk + fixed;
+    if (rr < best_cost * 0.999) {
+      best_cost = rr;
+      best = {c.pair, c.bn, false};
     }
-    if (cost < best_cost * 0.999) {
-      best_cost = cost;
-      best = {c.pair, c.bn};
+    // stream-K (only when it changes the balance, and only for small
+    // problems: contiguous per-unit ranges spread the units over the whole
+    // M range, which costs L2 locality once A no longer fits in L2)
+    if (tiles % units != 0 && tiles <= 4 * units && units <= MAX_UNITS) {
+      const long long work = tiles * nk;
+      const double per_unit = static_cast<double>((work + units - 1) / units);
+      const double fixup = 8000.0;  // measured: partial write + fence/flag + read costs ~4 us per split tile
+      const double sk = per_unit * kblk + fixup + fixed;
+      if (sk < best_cost * 0.999) {
+        best_cost = sk;
+        best = {c.pair, c.bn, true};
+      }
     }
   }
   return best;
 }
 
 static int g_gemm_dbg = 0;
+static int g_force_streamk = -1;  // -1 auto, 0 off, 1 on (test hook)
 
-int gemm_launch(const void* A, const void* Bt, const float* bias, const void* residual, void* C, int M, int N,
-                int K, int epi, int force, cudaStream_t s) {
-  BT_REQUIRE(M >= 0 && N > 0 && K > 0, BT_ESHAPE, "gemm: bad shape M=%d N=%d K=%d", M, N, K);
-  BT_REQUIRE(K % GEMM_BK == 0, BT_ESHAPE, "gemm: K=%d must be a multiple of 64", K);
-  BT_REQUIRE(N % 64 == 0, BT_ESHAPE, "gemm: N=%d must be a multiple of 64", N);
-  BT_REQUIRE(epi >= BT_EPI_NONE && epi <= BT_EPI_BIAS_RESIDUAL, BT_ECONFIG, "gemm: unknown epilogue %d", epi);
-  BT_REQUIRE(epi == BT_EPI_NONE || bias != nullptr, BT_ESHAPE, "gemm: epilogue %d needs a bias", epi);
-  BT_REQUIRE(epi != BT_EPI_BIAS_RESIDUAL || residual != nullptr, BT_ESHAPE, "gemm: residual epilogue needs residual");
-  if (M == 0) return BT_OK;
+template <int PAIR, int BN, int EW>
+static int dispatch_sk(bool sk, int epi, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
+                       const GemmParams& p, int units, cudaStream_t s) {
+  return sk ? dispatch_epi<PAIR, BN, EW, true>(epi, ta, tb, tc, p, units, s)
+            : dispatch_epi<PAIR, BN, EW, false>(epi, ta, tb, tc, p, units, s);
+}
+
+static int gemm_run(const void* A, const void* Bt, const float* bias, const void* residual, void* C, int M, int N,
+                    int K, int epi, GemmChoice ch, cudaStream_t s) {
   const int sms = num_sms() > 0 ? num_sms() : 148;
-  GemmChoice ch = choose_tile(M, N, K, sms);
-  if (force > 0) ch = {1, force};  // test hooks: +bn = one CTA, -bn = SM pair
-  if (force < 0) ch = {2, -force};
   BT_REQUIRE(N % ch.bn == 0, BT_ESHAPE, "gemm: N=%d not a multiple of BN=%d", N, ch.bn);
   const int bm = 128 * ch.pair;
   CUtensorMap ta, tb, tc;
@@ -480,25 +658,136 @@ int gemm_launch(const void* A, const void* Bt, const float* bias, const void* re
   p.num_m_blocks = (M + bm - 1) / bm;
   p.num_n_blocks = N / ch.bn;
   p.num_tiles = p.num_m_blocks * p.num_n_blocks;
+  p.num_k = K / GEMM_BK;
+  p.work = static_cast<long long>(p.num_tiles) * p.num_k;
   p.dbg = g_gemm_dbg;
+  p.partials = nullptr;
+  p.flags = nullptr;
   const int slots = sms / ch.pair;
-  const int units = p.num_tiles < slots ? p.num_tiles : slots;
+  int units = p.num_tiles < slots ? p.num_tiles : slots;
+  if (ch.streamk) {
+    StreamKWorkspace* ws = nullptr;
+    BT_TRY(streamk_workspace(&ws));
+    p.partials = ws->partials;
+    p.flags = ws->flags;
+    units = slots < MAX_UNITS ? slots : MAX_UNITS;
+    if (static_cast<long long>(units) > p.work) units = static_cast<int>(p.work);
+  }
   if (ch.pair == 2) {
     switch (ch.bn) {
-      case 128: return dispatch_epi<2, 128>(epi, ta, tb, tc, p, units, s);
-      case 192: return dispatch_epi<2, 192>(epi, ta, tb, tc, p, units, s);
-      case 256: return dispatch_epi<2, 256>(epi, ta, tb, tc, p, units, s);
+      case 128: return dispatch_sk<2, 128, 8>(ch.streamk, epi, ta, tb, tc, p, units, s);
+      case 192: return dispatch_sk<2, 192, 8>(ch.streamk, epi, ta, tb, tc, p, units, s);
+      case 256: return dispatch_sk<2, 256, 8>(ch.streamk, epi, ta, tb, tc, p, units, s);
       default: BT_REQUIRE(false, BT_ECONFIG, "gemm: SM-pair tile width %d unsupported", ch.bn);
     }
   }
   switch (ch.bn) {
-    case 64: return dispatch_epi<1, 64>(epi, ta, tb, tc, p, units, s);
-    case 128: return dispatch_epi<1, 128>(epi, ta, tb, tc, p, units, s);
-    case 192: return dispatch_epi<1, 192>(epi, ta, tb, tc, p, units, s);
-    case 256: return dispatch_epi<1, 256>(epi, ta, tb, tc, p, units, s);
+    case 64: return dispatch_sk<1, 64, 4>(ch.streamk, epi, ta, tb, tc, p, units, s);
+    case 128: return dispatch_sk<1, 128, 4>(ch.streamk, epi, ta, tb, tc, p, units, s);
+    case 192: return dispatch_sk<1, 192, 4>(ch.streamk, epi, ta, tb, tc, p, units, s);
+    case 256: return dispatch_sk<1, 256, 4>(ch.streamk, epi, ta, tb, tc, p, units, s);
     default: BT_REQUIRE(false, BT_ECONFIG, "gemm: tile width %d unsupported", ch.bn);
   }
   return BT_OK;
+}
+
+// ---------------------------------------------------------------- autotune
+// The first GEMM of a shape class (N, K, epilogue, M bucket) times every
+// candidate tile shape / decomposition on the live operands and remembers the
+// fastest; later calls (and CUDA-graph captures, where no timing is possible)
+// reuse it.  The cost model above is the fallback (BT_AUTOTUNE=0, or a first
+// call made while the stream is capturing).  Round-robin candidates give
+// bitwise-identical results (same per-element accumulation order); stream-K
+// differs only by the fixed-order fp32 fix-up.
+struct TuneKey {
+  int n, k, epi, mb;
+  bool operator<(const TuneKey& o) const {
+    return n != o.n ? n < o.n : k != o.k ? k < o.k : epi != o.epi ? epi < o.epi : mb < o.mb;
+  }
+};
+
+static bool autotune_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("BT_AUTOTUNE");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on != 0;
+}
+
+static std::map<TuneKey, GemmChoice>& tune_cache() {
+  static std::map<TuneKey, GemmChoice> m;
+  return m;
+}
+
+static int autotune(const void* A, const void* Bt, const float* bias, const void* residual, void* C, int M, int N,
+                    int K, int epi, cudaStream_t s, GemmChoice* best_out) {
+  const int sms = num_sms() > 0 ? num_sms() : 148;
+  struct Cand { int pair, bn; };
+  const Cand cands[] = {{2, 256}, {2, 192}, {2, 128}, {1, 256}, {1, 192}, {1, 128}, {1, 64}};
+  cudaEvent_t e0, e1;
+  BT_CUDA_CHECK(cudaEventCreate(&e0));
+  BT_CUDA_CHECK(cudaEventCreate(&e1));
+  float best_ms = 1e30f;
+  GemmChoice best = choose_tile(M, N, K, sms);
+  for (const Cand& c : cands) {
+    if (N % c.bn) continue;
+    const int bm = 128 * c.pair;
+    const long long tiles = static_cast<long long>((M + bm - 1) / bm) * (N / c.bn);
+    const long long units = sms / c.pair;
+    for (int sk = 0; sk < 2; ++sk) {
+      if (sk && !(tiles % units != 0 && tiles <= 4 * units)) continue;
+      const GemmChoice ch{c.pair, c.bn, sk != 0};
+      BT_TRY(gemm_run(A, Bt, bias, residual, C, M, N, K, epi, ch, s));  // warm (module load, L2)
+      BT_CUDA_CHECK(cudaEventRecord(e0, s));
+      for (int r = 0; r < 3; ++r) BT_TRY(gemm_run(A, Bt, bias, residual, C, M, N, K, epi, ch, s));
+      BT_CUDA_CHECK(cudaEventRecord(e1, s));
+      BT_CUDA_CHECK(cudaEventSynchronize(e1));
+      float ms = 0.f;
+      BT_CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
+      if (ms < best_ms * 0.98f) {  // prefer earlier (larger-tile) candidates on near ties
+        best_ms = ms;
+        best = ch;
+      }
+    }
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  *best_out = best;
+  return BT_OK;
+}
+
+int gemm_launch(const void* A, const void* Bt, const float* bias, const void* residual, void* C, int M, int N,
+                int K, int epi, int force, cudaStream_t s) {
+  BT_REQUIRE(M >= 0 && N > 0 && K > 0, BT_ESHAPE, "gemm: bad shape M=%d N=%d K=%d", M, N, K);
+  BT_REQUIRE(K % GEMM_BK == 0, BT_ESHAPE, "gemm: K=%d must be a multiple of 64", K);
+  BT_REQUIRE(N % 64 == 0, BT_ESHAPE, "gemm: N=%d must be a multiple of 64", N);
+  BT_REQUIRE(epi >= BT_EPI_NONE && epi <= BT_EPI_BIAS_RESIDUAL, BT_ECONFIG, "gemm: unknown epilogue %d", epi);
+  BT_REQUIRE(epi == BT_EPI_NONE || bias != nullptr, BT_ESHAPE, "gemm: epilogue %d needs a bias", epi);
+  BT_REQUIRE(epi != BT_EPI_BIAS_RESIDUAL || residual != nullptr, BT_ESHAPE, "gemm: residual epilogue needs residual");
+  if (M == 0) return BT_OK;
+  const int sms = num_sms() > 0 ? num_sms() : 148;
+  GemmChoice ch = choose_tile(M, N, K, sms);
+  if (force == 0 && g_force_streamk < 0 && g_gemm_dbg == 0 && autotune_enabled()) {
+    const TuneKey key{N, K, epi, (M + 255) / 256};
+    auto& cache = tune_cache();
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+      ch = it->second;
+    } else {
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      BT_CUDA_CHECK(cudaStreamIsCapturing(s, &cs));
+      if (cs == cudaStreamCaptureStatusNone) {
+        BT_TRY(autotune(A, Bt, bias, residual, C, M, N, K, epi, s, &ch));
+        cache[key] = ch;
+      }
+    }
+  }
+  if (force > 0) ch = {1, force, ch.streamk};  // test hooks: +bn = one CTA, -bn = SM pair
+  if (force < 0) ch = {2, -force, ch.streamk};
+  if (force != 0 && g_force_streamk < 0) ch.streamk = false;
+  if (g_force_streamk >= 0) ch.streamk = g_force_streamk != 0;
+  return gemm_run(A, Bt, bias, residual, C, M, N, K, epi, ch, s);
 }
 
 }  // namespace bt
@@ -516,11 +805,14 @@ extern "C" int bt_debug_gemm_trace(unsigned long long* buf) {
 }
 
 // Debug hook: 0 normal; 1 = GEMMs skip their MMAs (measure the TMA feed alone);
-// 2 = GEMMs skip their TMA loads (measure MMA + epilogue alone).  Results are
-// garbage in modes 1 and 2.
+// 2 = GEMMs skip their TMA loads (measure MMA + epilogue alone); 3 / 4 = force
+// stream-K off / on (results valid); 5 = stream-K back to automatic.
 extern "C" int bt_debug_gemm_mode(int mode) {
-  BT_REQUIRE(mode >= 0 && mode <= 2, BT_ECONFIG, "bt_debug_gemm_mode: mode must be 0..2");
-  bt::g_gemm_dbg = mode;
+  BT_REQUIRE(mode >= 0 && mode <= 5, BT_ECONFIG, "bt_debug_gemm_mode: mode must be 0..5");
+  if (mode <= 2) bt::g_gemm_dbg = mode;
+  if (mode == 3) bt::g_force_streamk = 0;
+  if (mode == 4) bt::g_force_streamk = 1;
+  if (mode == 5) bt::g_force_streamk = -1;
   return BT_OK;
 }
 

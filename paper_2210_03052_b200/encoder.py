@@ -340,6 +340,7 @@ class BertEncoderB200:
         self._c_layers = (_lib.LayerWeightsC * n)(*[dl.c for dl in self._layers])
         self._cfg_c = layer_cfg_c(self.config)
         self._ws = None
+        self._graphs = {}
 
     def layer(self, i: int) -> DeviceLayer:
         return self._layers[i]
@@ -361,6 +362,89 @@ class BertEncoderB200:
                   x_padded_f32.data_ptr(), out_padded_f32.data_ptr(), ws.data_ptr(), ws_bytes,
                   _lib.stream_ptr(stream))
         return out_padded_f32
+
+    def forward_ptrs(self, lengths_ptr: int, bs: int, T: int, x_ptr: int, out_ptr: int, stream=None,
+                     config: ModelConfig | None = None):
+        """Forward on raw pointers: lengths int32[bs], padded fp32 input and
+        output [bs*mx, k].  Each may be device memory or pinned host memory
+        (zero-copy: only valid input rows cross PCIe; no bulk memcpy)."""
+        cfg = config or self.config
+        cfg_c = self._cfg_c if config is None else layer_cfg_c(cfg)
+        ws_bytes = int(_lib.load().bt_forward_workspace_bytes(C.byref(cfg_c), bs, T))
+        ws = self.workspace(ws_bytes)
+        _lib.call("bt_encoder_forward", self._c_layers, cfg.layers, C.byref(cfg_c), lengths_ptr, bs, T, x_ptr,
+                  out_ptr, ws.data_ptr(), ws_bytes, _lib.stream_ptr(stream))
+
+    GRAPH_CACHE = 4  # batch shapes whose packed forward is kept as a CUDA graph
+
+    def _graph_entry(self, seqs: SeqLengths, cfg: ModelConfig, cfg_c):
+        """(graph, x_packed, y_packed) for this batch shape: device buffers
+        owned by the entry and a CUDA graph of bt_encoder_forward_packed over
+        them (captured after one eager warm-up run, which also autotunes)."""
+        torch = self.torch
+        key = (tuple(seqs.lengths), seqs.max_seq_len, cfg.layers, cfg.cutoff, cfg.split_seq_len)
+        hit = self._graphs.pop(key, None)
+        if hit is not None:
+            self._graphs[key] = hit  # most recently used last
+            return hit
+        bs, T, k = seqs.batch_size, seqs.total, cfg.hidden_dim
+        lengths_dev = torch.tensor(seqs.lengths, dtype=torch.int32, device="cuda")
+        xp = torch.empty((T, k), dtype=torch.float32, device="cuda")
+        yp = torch.empty((T, k), dtype=torch.float32, device="cuda")
+        ws_bytes = int(_lib.load().bt_forward_workspace_bytes(C.byref(cfg_c), bs, T))
+        ws = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
+
+        def run():
+            _lib.call("bt_encoder_forward_packed", self._c_layers, cfg.layers, C.byref(cfg_c), lengths_dev.data_ptr(),
+                      bs, T, xp.data_ptr(), yp.data_ptr(), ws.data_ptr(), ws_bytes, _lib.stream_ptr())
+
+        run()  # warm-up: module load, GEMM autotune
+        torch.cuda.synchronize()
+        graph = None
+        try:
+            g = torch.cuda.CUDAGraph()
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                run()
+            torch.cuda.current_stream().wait_stream(side)
+            with torch.cuda.graph(g):
+                run()
+            graph = g
+        except Exception:  # noqa: BLE001 -- graph capture unsupported here: launch eagerly
+            graph = None
+        entry = (graph, run, xp, yp, lengths_dev, ws)
+        self._graphs[key] = entry
+        while len(self._graphs) > self.GRAPH_CACHE:
+            self._graphs.pop(next(iter(self._graphs)))
+        return entry
+
+    def forward_host_packed(self, seqs: SeqLengths, x_pinned, out_pinned, config: ModelConfig | None = None):
+        """End-to-end forward on pinned host buffers [bs*mx, k] fp32: only the
+        valid rows cross PCIe (async DMA per sequence, both directions), the
+        encoder runs packed -> packed as one CUDA graph (cached per batch
+        shape), and the padded output rows are zeroed on the host while the
+        GPU computes.  Synchronises."""
+        cfg = config or self.config
+        cfg_c = self._cfg_c if config is None else layer_cfg_c(cfg)
+        bs, mx, k = seqs.batch_size, seqs.max_seq_len, cfg.hidden_dim
+        graph, run, xp, yp, _, _ = self._graph_entry(seqs, cfg, cfg_c)
+        lengths_h = np.ascontiguousarray(np.asarray(seqs.lengths, dtype=np.int32))
+        lp = lengths_h.ctypes.data
+        s = _lib.stream_ptr()
+        _lib.call("bt_copy_rows", xp.data_ptr(), x_pinned.data_ptr(), lp, bs, mx, k * 4, 1, s)
+        if graph is not None:
+            graph.replay()
+        else:
+            run()
+        _lib.call("bt_copy_rows", out_pinned.data_ptr(), yp.data_ptr(), lp, bs, mx, k * 4, 0, s)
+        # padded rows of the output are exact zeros (packing.py:158-159)
+        o = out_pinned.numpy().reshape(bs, mx, k)
+        for b, n in enumerate(seqs.lengths):
+            if n < mx:
+                o[b, n:] = 0.0
+        self.torch.cuda.current_stream().synchronize()
+        return out_pinned
 
     def layer_device(self, li: int, x_bf16, plan: PackingPlan, stream=None):
         """In-place encoder_layer on a packed bf16 [T, k] device tensor."""
@@ -475,31 +559,31 @@ def forward(weights, seqs, input_padded, config, *, workers: int = 1, counter: F
         return ladder.forward_variant(weights, seqs, input_padded, config, counter=counter)
     torch = _lib.require_device()
     eng = engine_for(weights, config)
-    device_mode = is_device(input_padded)
-    lengths = torch.tensor(seqs.lengths, dtype=torch.int32)
-    if device_mode:
+    if is_device(input_padded):
         x = input_padded.to(torch.float32).contiguous()
-        lengths = lengths.to(x.device)
-    else:
-        x = _host_to_device_f32(input_padded, torch)
-        lengths = lengths.pin_memory().to("cuda", non_blocking=True)
-    out = torch.empty((padded_rows, cols), dtype=torch.float32, device="cuda")
-    eng.forward_device(lengths, seqs.batch_size, seqs.total, x, out, config=config)
-    _count_flops(counter, config, seqs, config.layers)
-    if device_mode:
+        lengths = torch.tensor(seqs.lengths, dtype=torch.int32).to(x.device)
+        out = torch.empty((padded_rows, cols), dtype=torch.float32, device=x.device)
+        eng.forward_device(lengths, seqs.batch_size, seqs.total, x, out, config=config)
+        _count_flops(counter, config, seqs, config.layers)
         return out
-    # pinned host result from torch's caching host allocator (reused across
-    # calls once the caller drops it), async D2H, one sync
-    host = torch.empty((padded_rows, cols), dtype=torch.float32, pin_memory=True)
-    host.copy_(out, non_blocking=True)
-    torch.cuda.current_stream().synchronize()
-    return Tensor(host.numpy())
+    # Host I/O: DMA only each sequence's valid rows into a packed device
+    # buffer, run packed -> packed, DMA the valid output rows back into their
+    # padded positions, and zero the padded rows on the host while the GPU works.
+    x_host = _pinned_f32(input_padded, torch)
+    out = torch.empty((padded_rows, cols), dtype=torch.float32, pin_memory=True)
+    eng.forward_host_packed(seqs, x_host, out, config=config)
+    _count_flops(counter, config, seqs, config.layers)
+    return Tensor(out.numpy())
 
 
-def _host_to_device_f32(x, torch):
-    """Host fp32 input -> device.  A pinned CPU torch tensor is copied
-    asynchronously as is; ndarrays / Tensors go through a pageable copy."""
+def _pinned_f32(x, torch):
+    """Host fp32 input as a page-locked CPU tensor (used in place when it
+    already is one; otherwise one host-side copy into pinned memory)."""
     if type(x).__module__.startswith("torch") and not x.is_cuda:
         t = x if x.dtype == torch.float32 else x.float()
-        return t.contiguous().to("cuda", non_blocking=t.is_pinned())
-    return torch.from_numpy(host_array(x)).to("cuda")
+        t = t.contiguous()
+        return t if t.is_pinned() else t.pin_memory()
+    arr = host_array(x)
+    pinned = torch.empty(arr.shape, dtype=torch.float32, pin_memory=True)
+    pinned.numpy()[...] = arr
+    return pinned

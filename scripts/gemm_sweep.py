@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--shapes", default="all")
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--mode", type=int, default=0, help="bt_debug_gemm_mode (0 normal, 1 no-MMA, 2 no-TMA)")
+    ap.add_argument("--sk", type=int, default=-1, help="stream-K: -1 auto, 0 off, 1 on")
     a = ap.parse_args()
     import torch
 
@@ -33,6 +34,7 @@ def main():
 
     _lib.require_device()
     _lib.call("bt_debug_gemm_mode", a.mode)
+    _lib.call("bt_debug_gemm_mode", {-1: 5, 0: 3, 1: 4}[a.sk])
     peak = json.loads((Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json").read_text())["bf16_tflops"]
     groups = list(SHAPES) if a.shapes == "all" else [a.shapes]
     out = []
@@ -50,7 +52,7 @@ def main():
                 if epi == 2:
                     ref = 0.5 * ref * (1 + torch.tanh(math.sqrt(2 / math.pi) * (ref + 0.044715 * ref ** 3)))
             flops = 2.0 * M * N * K
-            row = {"shape": [M, N, K], "epi": epi, "mode": a.mode}
+            row = {"shape": [M, N, K], "epi": epi, "mode": a.mode, "sk": a.sk}
             for v in VARIANTS + (["cublas"] if a.mode == 0 else []):
                 if isinstance(v, int) and N % abs(v):
                     continue

@@ -19,6 +19,8 @@ def main():
 
     _lib.require_device()
     M, N, K, epi, bn = map(int, sys.argv[1:6])
+    if len(sys.argv) > 6:
+        _lib.call("bt_debug_gemm_mode", int(sys.argv[6]))  # 3 = stream-K off, 4 = on
     A = (torch.randn(M, K, device="cuda") * 0.5).to(torch.bfloat16)
     W = (torch.randn(N, K, device="cuda") / math.sqrt(K)).to(torch.bfloat16)
     bias = torch.randn(N, device="cuda") * 0.1

@@ -213,3 +213,39 @@ def test_mha_deterministic(env):
     a = mha_device(qkv, plan, 4, 64).clone()
     b = mha_device(qkv, plan, 4, 64)
     assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("bn", [64, 128, 256, -128, -192, -256])
+@pytest.mark.parametrize("epi", [0, 2, 3])
+@pytest.mark.parametrize("M,N,K", [(2458, 768, 3072), (2458, 2304, 768), (300, 768, 128), (77, 768, 64),
+                                   (4915, 1024, 4096)])
+def test_gemm_streamk(env, bn, epi, M, N, K):
+    """Stream-K decomposition (forced on): split tiles are fixed up from fp32
+    partials in a fixed order -- results match the fp32 reference and are
+    bitwise reproducible run to run."""
+    bt, torch = env
+    from paper_2210_03052_b200 import _lib
+    from paper_2210_03052_b200.tensor import gemm_device
+
+    if N % abs(bn):
+        pytest.skip("N not a multiple of BN")
+    a = (torch.randn(M, K, device="cuda") * 0.5).to(torch.bfloat16)
+    w = (torch.randn(N, K, device="cuda") / math.sqrt(K)).to(torch.bfloat16)
+    bias = torch.randn(N, device="cuda") * 0.1
+    res = torch.randn(M, N, device="cuda").to(torch.bfloat16)
+    _lib.call("bt_debug_gemm_mode", 4)
+    try:
+        out = gemm_device(a, w, bias if epi else None, res if epi == 3 else None, epi, bn=bn)
+        out2 = gemm_device(a, w, bias if epi else None, res if epi == 3 else None, epi, bn=bn)
+    finally:
+        _lib.call("bt_debug_gemm_mode", 5)
+    ref = a.float() @ w.float().t()
+    if epi == 3:
+        ref = ref + res.float()
+    if epi:
+        ref = ref + bias
+    if epi == 2:
+        ref = _gelu(ref)
+    torch.cuda.synchronize()
+    assert rel_fro(out, ref) < 6e-3, (bn, epi, M, N, K, rel_fro(out, ref))
+    assert torch.equal(out, out2)
