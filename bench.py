@@ -338,8 +338,9 @@ def run_ours(args, wl):
     e2e = None
     if not args.no_e2e:
         x_pin = torch.from_numpy(x_host).pin_memory()
-        for _ in range(max(1, args.warmup)):
-            bt.forward(weights, seqs, x_pin, cfg)
+        y = None
+        for _ in range(max(2, args.warmup)):  # hold each result as the timed loop does, so the pinned
+            y = bt.forward(weights, seqs, x_pin, cfg)  # host allocator has both output buffers before timing
         torch.cuda.synchronize()
         if dist is not None:
             dist.barrier()
@@ -351,11 +352,14 @@ def run_ours(args, wl):
             y = bt.forward(weights, seqs, x_pin, cfg)
             t.append(time.perf_counter() - t0)
         e2e_ms = sum(t) * 1e3 / len(t)
+        log(f"[bench] e2e per-step ms: min {min(t) * 1e3:.3f} median {statistics.median(t) * 1e3:.3f} "
+            f"max {max(t) * 1e3:.3f}")
         e_t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
         if dist is not None:
             dist.all_reduce(e_t, op=dist.ReduceOp.MAX)
         e2e_ms = float(e_t.item())
         e2e = {"value": round(bs_global / (e2e_ms / 1e3), 2), "unit": "seq/s", "ms_per_step": round(e2e_ms, 4),
+               "ms_per_step_median": round(statistics.median(t) * 1e3, 4),
                # bytes that cross PCIe per step: the pack kernel reads only the valid input rows (and the
                # lengths) from pinned host memory; the unpack kernel writes the whole padded output
                "h2d_bytes_per_step": int(T * hidden * 4 + 4 * len(lens)) * world,
