@@ -266,7 +266,7 @@ def run_ours(args, wl):
     lengths_dev = torch.tensor(lens, dtype=torch.int32, device="cuda")
     out_dev = torch.empty_like(x_dev)
     flush = torch.ones(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # 256 MB > 126 MB L2
-    flush_sink = torch.empty(1, dtype=torch.float32, device="cuda")
+    flush_sink = torch.empty((), dtype=torch.float32, device="cuda")
 
     def flush_l2():
         # read (not write) 256 MB: evicts every L2 line without leaving dirty

@@ -84,23 +84,26 @@ __device__ __forceinline__ void store_out_row(const MhaParams& p, int grow, int 
 
 // ============================================================ kernel
 // One template serves both reference paths:
-//   RESIDENT = true   short path (attention.py:177-237): all K/V blocks of the
-//                     sequence-head are TMA-staged once and stay in shared
-//                     memory for both passes (<= NST*128 keys).
+//   RESIDENT = true   short path (attention.py:177-237): every K/V block of the
+//                     sequence-head is TMA-staged up front and stays in shared
+//                     memory (<= NST*128 keys): the tile-resident kernel.
 //   RESIDENT = false  long path (attention.py:240-296): 128-key K/V blocks
-//                     stream through an NST-deep ring, once per pass.
-// Both take the exact two-pass softmax of the reference: pass 1 computes the
-// row max over every key (the "partial max per 128-column tile + full
-// reduction" of the grouped path, tensor.py:166-173 / attention.py:104-122);
-// pass 2 forms P = exp(s - max) (masked past the sequence end), writes it
-// as bf16 to shared memory, and accumulates O += P V in TMEM with no
-// rescaling; O is divided by the row sum at the end.
+//                     stream through an NST-deep TMA ring; work per CTA is the
+//                     sequence's true length (grouped problem sizes).
+// Softmax: single pass, online.  For each 128-key block the softmax warps read
+// S = Q K^T from TMEM twice (block max, then exp), rescale their running output
+// o (fp32 registers, thread = query row) and row sum l by exp(m_old - m_new),
+// write P = exp(s - m_new) (bf16, UMMA K-major SW128) to shared memory, and the
+// MMA warp computes the block's P V into a TMEM partial that the threads fold
+// into o.  This is the reference's long-path algorithm -- per-128-column tile
+// partial (max, sum) combined by a full reduction, then exp on load -- with the
+// reduction carried as a running (max, sum) so P never reaches HBM and S is
+// computed once.  Keys past the sequence end are masked (p = 0).
 //
-// Warp roles (192 threads): warps 0-3 softmax / epilogue (thread = query row
-// = TMEM lane), warp 4 TMA producer, warp 5 MMA issuer; both issuer warps walk
-// their loops warp-uniformly and issue through elect.sync.  TMEM: S in
-// columns [0,128), O in [128,192) -> 256 columns, ~112 KB smem -> two CTAs per
-// SM, whose latency chains interleave.
+// Warp roles (192 threads): warps 0-3 softmax / epilogue, warp 4 TMA producer,
+// warp 5 MMA issuer; both issuer warps walk their loops warp-uniformly and
+// issue through elect.sync.  TMEM: S [0,128), P V partial [128,192) -> 256
+// columns; ~112 KB smem -> two CTAs per SM, whose latency chains interleave.
 template <bool RESIDENT, int NST>
 struct MhaCfg {
   static constexpr uint32_t Q_OFF = 0;
@@ -126,7 +129,6 @@ __global__ void __launch_bounds__(192) mha_fwd_kernel(const __grid_constant__ CU
   const int q0 = qt * MHA_QT;
   if (q0 >= work) return;  // CTA-uniform: this q tile is past the sequence
   const int nkb = (work + MHA_KB - 1) / MHA_KB;
-  const int n_items = 2 * nkb;  // pass 1 (max) then pass 2 (exp, P V) over the key blocks
 
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sQ = smem + Cfg::Q_OFF;
@@ -137,9 +139,8 @@ __global__ void __launch_bounds__(192) mha_fwd_kernel(const __grid_constant__ CU
   uint64_t* kv_full = bars + 1;         // [NST]
   uint64_t* kv_empty = bars + 1 + NST;  // [NST]
   uint64_t* s_full = bars + 1 + 2 * NST;
-  uint64_t* s_free = s_full + 1;
-  uint64_t* pv_done = s_full + 2;
-  uint64_t* o_full = s_full + 3;
+  uint64_t* s_free = s_full + 1;   // softmax done with S(j), P(j) is in smem
+  uint64_t* pv_done = s_full + 2;  // P(j) V(j) partial is in TMEM, sP free
   uint32_t* holder = reinterpret_cast<uint32_t*>(s_full + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -153,7 +154,6 @@ __global__ void __launch_bounds__(192) mha_fwd_kernel(const __grid_constant__ CU
     ptx::mbar_init(s_full, 1);
     ptx::mbar_init(s_free, 128);
     ptx::mbar_init(pv_done, 1);
-    ptx::mbar_init(o_full, 1);
     ptx::fence_mbar_init();
   }
   if (warp == 0) {
@@ -176,30 +176,16 @@ __global__ void __launch_bounds__(192) mha_fwd_kernel(const __grid_constant__ CU
       ptx::tma_load_2d(sQ, &tm, q_full, h * MHA_D, s0 + q0);
     }
     __syncwarp();
-    if constexpr (RESIDENT) {
-      for (int j = 0; j < nkb; ++j) {
-        if (ptx::elect_one()) {
-          uint8_t* kv = sKV + j * 2 * MHA_TILE;
-          ptx::mbar_arrive_expect_tx(&kv_full[j], 2 * MHA_TILE);
-          ptx::tma_load_2d(kv, &tm, &kv_full[j], p.hidden + h * MHA_D, s0 + j * MHA_KB);
-          ptx::tma_load_2d(kv + MHA_TILE, &tm, &kv_full[j], 2 * p.hidden + h * MHA_D, s0 + j * MHA_KB);
-        }
-        __syncwarp();
+    for (int j = 0; j < nkb; ++j) {
+      const int slot = RESIDENT ? j : j % NST;
+      if (!RESIDENT) ptx::mbar_wait(&kv_empty[slot], ((j / NST) & 1) ^ 1u);
+      if (ptx::elect_one()) {
+        uint8_t* kv = sKV + slot * 2 * MHA_TILE;
+        ptx::mbar_arrive_expect_tx(&kv_full[slot], 2 * MHA_TILE);
+        ptx::tma_load_2d(kv, &tm, &kv_full[slot], p.hidden + h * MHA_D, s0 + j * MHA_KB);
+        ptx::tma_load_2d(kv + MHA_TILE, &tm, &kv_full[slot], 2 * p.hidden + h * MHA_D, s0 + j * MHA_KB);
       }
-    } else {
-      for (int t = 0; t < n_items; ++t) {
-        const bool pass2 = t >= nkb;
-        const int j = pass2 ? t - nkb : t;
-        const int slot = t % NST;
-        ptx::mbar_wait(&kv_empty[slot], ((t / NST) & 1) ^ 1u);
-        if (ptx::elect_one()) {
-          uint8_t* kv = sKV + slot * 2 * MHA_TILE;
-          ptx::mbar_arrive_expect_tx(&kv_full[slot], pass2 ? 2 * MHA_TILE : MHA_TILE);
-          ptx::tma_load_2d(kv, &tm, &kv_full[slot], p.hidden + h * MHA_D, s0 + j * MHA_KB);
-          if (pass2) ptx::tma_load_2d(kv + MHA_TILE, &tm, &kv_full[slot], 2 * p.hidden + h * MHA_D, s0 + j * MHA_KB);
-        }
-        __syncwarp();
-      }
+      __syncwarp();
     }
   } else if (warp == 5) {
     // ------------------------------------------------ MMA issuer
@@ -211,13 +197,11 @@ __global__ void __launch_bounds__(192) mha_fwd_kernel(const __grid_constant__ CU
     ptx::mbar_wait(q_full, 0);
     if (lane == 0) MHA_TRACE(1);
     int prev_slot = 0;
-    for (int t = 0; t <= n_items; ++t) {
-      const bool pass2 = t >= nkb;
-      const int j = pass2 ? t - nkb : t;
-      const int slot = RESIDENT ? j : t % NST;
-      if (t > 0) ptx::mbar_wait(s_free, (t - 1) & 1);  // softmax done with S(t-1) / P(t-1) is in smem
-      if (t < n_items) {
-        ptx::mbar_wait(&kv_full[slot], RESIDENT ? 0u : static_cast<uint32_t>((t / NST) & 1));
+    for (int j = 0; j <= nkb; ++j) {
+      const int slot = RESIDENT ? j : j % NST;
+      if (j > 0) ptx::mbar_wait(s_free, (j - 1) & 1);  // softmax done with S(j-1); P(j-1) is in smem
+      if (j < nkb) {
+        ptx::mbar_wait(&kv_full[slot], RESIDENT ? 0u : static_cast<uint32_t>((j / NST) & 1));
         ptx::tc_fence_after();
         const uint64_t k_desc = ptx::sdesc_sw128(kv_base + slot * 2 * MHA_TILE, 1024, 16);
         if (ptx::elect_one()) {
@@ -225,24 +209,22 @@ __global__ void __launch_bounds__(192) mha_fwd_kernel(const __grid_constant__ CU
           for (int kk = 0; kk < MHA_D / 16; ++kk)
             ptx::mma_bf16_ss(tmem + S_COL, q_desc + 2 * kk, k_desc + 2 * kk, idesc_s, kk > 0);
           ptx::mma_commit(s_full);
-          if (!RESIDENT && !pass2) ptx::mma_commit(&kv_empty[slot]);  // K of this pass-1 block consumed
         }
         __syncwarp();
       } else {
         ptx::tc_fence_after();
       }
-      if (t > nkb) {
-        // P(t-1) V(t-1): 128 keys in 8 steps of 16; V block is MN-major (keys x d)
-        const int pj = t - 1 - nkb;
+      if (j > 0) {
+        // P(j-1) V(j-1) -> TMEM partial (fresh each block; the threads fold it in)
+        const int pj = j - 1;
         const int nks = min(MHA_KB, work - pj * MHA_KB + 15) / 16;
         const uint64_t v_desc = ptx::sdesc_sw128(kv_base + prev_slot * 2 * MHA_TILE + MHA_TILE, 1024, MHA_TILE);
         if (ptx::elect_one()) {
           for (int ks = 0; ks < nks; ++ks)
             ptx::mma_bf16_ss(tmem + O_COL, p_desc + (ks >> 2) * (MHA_TILE >> 4) + (ks & 3) * 2,
-                             v_desc + ks * ((16 * 128) >> 4), idesc_o, (pj | ks) != 0);
+                             v_desc + ks * ((16 * 128) >> 4), idesc_o, ks != 0);
           ptx::mma_commit(pv_done);
-          if (!RESIDENT) ptx::mma_commit(&kv_empty[prev_slot]);
-          if (t == n_items) ptx::mma_commit(o_full);
+          if (!RESIDENT) ptx::mma_commit(&kv_empty[prev_slot]);  // K and V of block j-1 consumed
         }
         __syncwarp();
       }
@@ -255,105 +237,127 @@ __global__ void __launch_bounds__(192) mha_fwd_kernel(const __grid_constant__ CU
     const int row = warp * 32 + lane;
     const bool warp_live = q0 + warp * 32 < work;
     const uint32_t trow = tmem + (static_cast<uint32_t>(warp * 32) << 16);
-    float mrow = -INFINITY, msc = 0.f, lsum = 0.f;
-    for (int t = 0; t < n_items; ++t) {
-      const bool pass2 = t >= nkb;
-      const int kbase = (pass2 ? t - nkb : t) * MHA_KB;
-      const int kvalid = min(MHA_KB, len - kbase);  // valid keys in this block (<= 0: all masked)
-      ptx::mbar_wait(s_full, t & 1);
-      ptx::tc_fence_after();
-      if (threadIdx.x == 0) MHA_TRACE(2 + 2 * t);
-      if (!pass2) {
-        if (warp_live) {
-#pragma unroll 1
-          for (int c = 0; c < kvalid; c += 64) {
-            uint32_t r0[32], r1[32];
-            ptx::tmem_ld32(trow + S_COL + c, r0);
-            ptx::tmem_ld32(trow + S_COL + c + 32, r1);
-            ptx::tmem_wait_ld(r0);
-            reg_tie(r1);
+    // o: running output row (fp32 pairs, FFMA2); every hot loop below uses
+    // paired fp32 ops / 3-input max -- the softmax is instruction-issue bound
+    unsigned long long o2[32];
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              if (c + i < kvalid) mrow = fmaxf(mrow, __uint_as_float(r0[i]));
-              if (c + 32 + i < kvalid) mrow = fmaxf(mrow, __uint_as_float(r1[i]));
-            }
-          }
-        }
-        if (t == nkb - 1) msc = mrow * p.sl2;
-      } else {
-        if (t > nkb) ptx::mbar_wait(pv_done, (t - 1 - nkb) & 1);  // P V of the previous block has read sP
-        if (warp_live) {
-#pragma unroll 1
-          for (int c = 0; c < MHA_KB; c += 64) {
-            uint32_t pk[32];
-            if (c < kvalid) {
-              uint32_t r0[32], r1[32];
-              ptx::tmem_ld32(trow + S_COL + c, r0);
-              ptx::tmem_ld32(trow + S_COL + c + 32, r1);
-              ptx::tmem_wait_ld(r0);
-              reg_tie(r1);
+    for (int i = 0; i < 32; ++i) o2[i] = 0ull;
+    float mrow = -INFINITY, lsum = 0.f, alpha_prev = 0.f;
+    // fold the TMEM partial P(j-1) V(j-1) into o (after rescaling o to m(j-1))
+    auto fold_partial = [&](float alpha) {
+      const unsigned long long a2 = ptx::f2(alpha, alpha);
 #pragma unroll
-              for (int i = 0; i < 32; i += 2) {
-                const float e0 = (c + i < kvalid) ? ptx::ex2_approx(fmaf(__uint_as_float(r0[i]), p.sl2, -msc)) : 0.f;
-                const float e1 =
-                    (c + i + 1 < kvalid) ? ptx::ex2_approx(fmaf(__uint_as_float(r0[i + 1]), p.sl2, -msc)) : 0.f;
-                lsum += e0 + e1;
-                pk[i / 2] = ptx::pack_bf16x2(e0, e1);
-              }
-              if (c + 32 < kvalid) {
+      for (int half = 0; half < 2; ++half) {
+        uint32_t r[32];
+        ptx::tmem_ld32(trow + O_COL + 32 * half, r);
+        ptx::tmem_wait_ld(r);
 #pragma unroll
-                for (int i = 0; i < 32; i += 2) {
-                  const float e0 =
-                      (c + 32 + i < kvalid) ? ptx::ex2_approx(fmaf(__uint_as_float(r1[i]), p.sl2, -msc)) : 0.f;
-                  const float e1 =
-                      (c + 33 + i < kvalid) ? ptx::ex2_approx(fmaf(__uint_as_float(r1[i + 1]), p.sl2, -msc)) : 0.f;
-                  lsum += e0 + e1;
-                  pk[16 + i / 2] = ptx::pack_bf16x2(e0, e1);
-                }
-              } else {
-#pragma unroll
-                for (int i = 0; i < 16; ++i) pk[16 + i] = 0u;
-              }
-            } else {
-#pragma unroll
-              for (int i = 0; i < 32; ++i) pk[i] = 0u;
-            }
-            // keys [c, c+64) == one 64-key column block of the K-major SW128 P tile
-            uint8_t* blk = sP + (c >> 6) * MHA_TILE + row * 128;
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-              *reinterpret_cast<uint4*>(blk + ((j ^ (row & 7)) << 4)) =
-                  make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
-          }
-        }
-        ptx::fence_proxy_async_smem();
+        for (int i = 0; i < 16; ++i)
+          o2[16 * half + i] = ptx::fma2(o2[16 * half + i], a2, ptx::f2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1])));
       }
+    };
+    const unsigned long long sl2x2 = ptx::f2(p.sl2, p.sl2);
+    for (int j = 0; j < nkb; ++j) {
+      const int kbase = j * MHA_KB;
+      const int kvalid = min(MHA_KB, len - kbase);  // valid keys in this block (<= 0: all masked)
+      ptx::mbar_wait(s_full, j & 1);
+      ptx::tc_fence_after();
+      if (threadIdx.x == 0) MHA_TRACE(2 + 2 * j);
+      float alpha = 1.f, msc = 0.f;
+      if (warp_live) {
+        // block max over the valid keys -> running max
+        float bmax = -INFINITY;
+#pragma unroll 1
+        for (int c = 0; c < kvalid; c += 32) {
+          uint32_t r[32];
+          ptx::tmem_ld32(trow + S_COL + c, r);
+          ptx::tmem_wait_ld(r);
+          if (c + 32 <= kvalid) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 2) bmax = ptx::max3(bmax, __uint_as_float(r[i]), __uint_as_float(r[i + 1]));
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (c + i < kvalid) bmax = fmaxf(bmax, __uint_as_float(r[i]));
+          }
+        }
+        const float mnew = fmaxf(mrow, bmax);
+        alpha = (mrow == -INFINITY) ? 0.f : ptx::ex2_approx((mrow - mnew) * p.sl2);
+        mrow = mnew;
+        msc = mnew * p.sl2;
+      }
+      if (j > 0) {
+        ptx::mbar_wait(pv_done, (j - 1) & 1);  // P(j-1) V(j-1) landed; sP is free
+        ptx::tc_fence_after();
+        if (warp_live) fold_partial(alpha_prev);
+      }
+      if (warp_live) {
+        const unsigned long long nm2 = ptx::f2(-msc, -msc);
+        unsigned long long bsum2 = 0ull;
+        float bsum_tail = 0.f;
+#pragma unroll 1
+        for (int c = 0; c < MHA_KB; c += 32) {
+          uint32_t pk[16];
+          if (c + 32 <= kvalid) {
+            uint32_t r[32];
+            ptx::tmem_ld32(trow + S_COL + c, r);
+            ptx::tmem_wait_ld(r);
+#pragma unroll
+            for (int i = 0; i < 32; i += 2) {
+              float x0, x1;
+              ptx::unf2(ptx::fma2(ptx::f2(__uint_as_float(r[i]), __uint_as_float(r[i + 1])), sl2x2, nm2), x0, x1);
+              const float e0 = ptx::ex2_approx(x0), e1 = ptx::ex2_approx(x1);
+              bsum2 = ptx::add2(bsum2, ptx::f2(e0, e1));
+              pk[i / 2] = ptx::pack_bf16x2(e0, e1);
+            }
+          } else if (c < kvalid) {
+            uint32_t r[32];
+            ptx::tmem_ld32(trow + S_COL + c, r);
+            ptx::tmem_wait_ld(r);
+#pragma unroll
+            for (int i = 0; i < 32; i += 2) {
+              const float e0 = (c + i < kvalid) ? ptx::ex2_approx(fmaf(__uint_as_float(r[i]), p.sl2, -msc)) : 0.f;
+              const float e1 =
+                  (c + i + 1 < kvalid) ? ptx::ex2_approx(fmaf(__uint_as_float(r[i + 1]), p.sl2, -msc)) : 0.f;
+              bsum_tail += e0 + e1;
+              pk[i / 2] = ptx::pack_bf16x2(e0, e1);
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) pk[i] = 0u;
+          }
+          store_p32(sP, row, c, pk);
+        }
+        float s0f, s1f;
+        ptx::unf2(bsum2, s0f, s1f);
+        lsum = lsum * alpha + (s0f + s1f + bsum_tail);
+        alpha_prev = alpha;
+      }
+      ptx::fence_proxy_async_smem();
       ptx::tc_fence_before();
       ptx::mbar_arrive(s_free);
-      if (threadIdx.x == 0) MHA_TRACE(3 + 2 * t);
+      if (threadIdx.x == 0) MHA_TRACE(3 + 2 * j);
     }
-    ptx::mbar_wait(o_full, 0);
+    ptx::mbar_wait(pv_done, (nkb - 1) & 1);
     ptx::tc_fence_after();
     if (threadIdx.x == 0) MHA_TRACE(30);
-    // O (128 x 64 fp32 in TMEM) -> scaled bf16 rows staged in sP (free: every
-    // P V has completed) -> coalesced 16-byte stores, 4 rows per warp instruction
+    // o / l -> bf16 rows staged in sP (free: the last P V has completed) ->
+    // coalesced 16-byte stores, 4 rows per warp instruction
     if (warp_live) {
-      uint32_t r0[32], r1[32];
-      ptx::tmem_ld32(trow + O_COL, r0);
-      ptx::tmem_ld32(trow + O_COL + 32, r1);
-      ptx::tmem_wait_ld(r0);
-      reg_tie(r1);
+      fold_partial(alpha_prev);
       const float inv = (q0 + row < len) ? 1.0f / lsum : 0.f;
+      const unsigned long long inv2 = ptx::f2(inv, inv);
       uint8_t* mine = sP + row * 128;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const uint32_t* src = (j < 4) ? r0 + 8 * j : r1 + 8 * (j - 4);
-        uint4 v;
-        v.x = ptx::pack_bf16x2(__uint_as_float(src[0]) * inv, __uint_as_float(src[1]) * inv);
-        v.y = ptx::pack_bf16x2(__uint_as_float(src[2]) * inv, __uint_as_float(src[3]) * inv);
-        v.z = ptx::pack_bf16x2(__uint_as_float(src[4]) * inv, __uint_as_float(src[5]) * inv);
-        v.w = ptx::pack_bf16x2(__uint_as_float(src[6]) * inv, __uint_as_float(src[7]) * inv);
-        *reinterpret_cast<uint4*>(mine + ((j ^ (row & 7)) << 4)) = v;
+      for (int jj = 0; jj < 8; ++jj) {
+        uint32_t w[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          float a, b2;
+          ptx::unf2(ptx::mul2(o2[4 * jj + e], inv2), a, b2);
+          w[e] = ptx::pack_bf16x2(a, b2);
+        }
+        *reinterpret_cast<uint4*>(mine + ((jj ^ (row & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
       }
       __syncwarp();
       ptx::griddep_wait();  // out may still be read by the previous kernel
@@ -361,10 +365,10 @@ __global__ void __launch_bounds__(192) mha_fwd_kernel(const __grid_constant__ CU
 #pragma unroll
       for (int it = 0; it < 8; ++it) {
         const int rr = warp * 32 + it * 4 + (lane >> 3);
-        const int j = lane & 7;
+        const int jj = lane & 7;
         if (q0 + rr < work) {
-          const uint4 v = *reinterpret_cast<const uint4*>(sP + rr * 128 + ((j ^ (rr & 7)) << 4));
-          *reinterpret_cast<uint4*>(p.out + static_cast<size_t>(s0 + q0 + rr) * p.hidden + h * MHA_D + j * 8) = v;
+          const uint4 v = *reinterpret_cast<const uint4*>(sP + rr * 128 + ((jj ^ (rr & 7)) << 4));
+          *reinterpret_cast<uint4*>(p.out + static_cast<size_t>(s0 + q0 + rr) * p.hidden + h * MHA_D + jj * 8) = v;
         }
       }
     }
