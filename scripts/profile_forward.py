@@ -30,9 +30,16 @@ def main():
     x = torch.from_numpy(harness.gen_input(seqs, heads * 64, 0)).cuda()
     lengths = torch.tensor(seqs.lengths, dtype=torch.int32, device="cuda")
     out = torch.empty_like(x)
+    # warm-up forwards (GEMM autotune, module load) outside the profiled range;
+    # run ncu with --profile-from-start off to capture only the last a.iters
+    for _ in range(2):
+        eng.forward_device(lengths, bs, seqs.total, x, out)
+    torch.cuda.synchronize()
+    torch.cuda.cudart().cudaProfilerStart()
     for _ in range(a.iters):
         eng.forward_device(lengths, bs, seqs.total, x, out)
     torch.cuda.synchronize()
+    torch.cuda.cudart().cudaProfilerStop()
     print("done", desc)
 
 
