@@ -202,8 +202,13 @@ BT_API int bt_mha_varlen_path(const void* qkv, const int32_t* seq_starts, int bs
 /* Debug hook: per-CTA globaltimer event trace of the GEMM kernels (64 u64
  * slots per CTA, see csrc/gemm_sm100.cu); NULL turns tracing off. */
 BT_API int bt_debug_gemm_trace(unsigned long long* buf);
-/* Debug hook: 0 normal, 1 = GEMMs skip the MMAs, 2 = GEMMs skip the TMA loads (results invalid in 1/2). */
+/* Debug hook: 0 normal, 1 = GEMMs skip the MMAs, 2 = GEMMs skip the TMA loads, 3 / 4 / 5 = stream-K
+ * off / on / automatic, 6 / 7 / 8 = epilogue probes: no output store / no TMEM loads / TMEM loads only
+ * (results invalid in 1, 2, 6, 7, 8). */
 BT_API int bt_debug_gemm_mode(int mode);
+/* Debug hook: install n cudaEvent_t (as void*) that the next bt_encoder_forward records after each
+ * launch group: [0] start, [1] plan + pack, 7 per layer, then unpack; NULL uninstalls. */
+BT_API int bt_debug_forward_events(void** events, int n);
 /* Debug hook: per-CTA globaltimer event trace of the MHA kernels (32 u64 slots per CTA). */
 BT_API int bt_debug_mha_trace(unsigned long long* buf);
 

@@ -20,6 +20,7 @@ int gemm_launch(const void* A, const void* Bt, const float* bias, const void* re
 int mha_launch(const void* qkv, const int32_t* seq_starts, int bs, int mx, int H, int d, int cutoff, int T, void* out,
                int force_path, cudaStream_t s, int padded);
 
+
 static inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
 struct LayerWs {
@@ -71,8 +72,20 @@ extern "C" size_t bt_layer_workspace_bytes(const bt_layer_cfg* cfg, int T) {
   return bt::layer_ws_bytes(k, cfg->ffn_scale * k, T < 1 ? 1 : T);
 }
 
-extern "C" int bt_encoder_layer(const bt_layer_weights* w, const bt_layer_cfg* cfg, const int32_t* seq_starts, int bs,
-                                int T, void* x_inout, void* ws, size_t ws_bytes, bt_stream_t stream) {
+namespace bt {
+// Debug hook (bt_debug_forward_events): when installed, the forward records
+// events[i] after each of its launches (plan/pack, then 7 per layer), so a
+// caller can attribute device time per kernel inside a real forward.
+static cudaEvent_t* g_fwd_events = nullptr;
+static int g_fwd_events_n = 0;
+static int g_fwd_event_idx = 0;
+static int mark(cudaStream_t s) {
+  if (g_fwd_events && g_fwd_event_idx < g_fwd_events_n) BT_CUDA_CHECK(cudaEventRecord(g_fwd_events[g_fwd_event_idx++], s));
+  return BT_OK;
+}
+// One post-LN layer.
+static int encoder_layer_impl(const bt_layer_weights* w, const bt_layer_cfg* cfg, const int32_t* seq_starts, int bs,
+                              int T, void* x_inout, void* ws, size_t ws_bytes, bt_stream_t stream) {
   BT_TRY(bt::check_cfg(cfg));
   BT_REQUIRE(w != nullptr, BT_ESHAPE, "null layer weights");
   BT_REQUIRE(T >= 1 && bs >= 1, BT_ESHAPE, "encoder_layer: T=%d bs=%d", T, bs);
@@ -85,14 +98,27 @@ extern "C" int bt_encoder_layer(const bt_layer_weights* w, const bt_layer_cfg* c
   auto* x = static_cast<__nv_bfloat16*>(x_inout);
 
   BT_TRY(bt::gemm_launch(x, w->qkv_w, w->qkv_b, nullptr, L.qkv, T, 3 * k, k, BT_EPI_BIAS, 0, s));
+  BT_TRY(mark(s));
   BT_TRY(bt::mha_launch(L.qkv, seq_starts, bs, cfg->max_seq_len, cfg->head_num, cfg->head_size, cfg->cutoff, T, L.ctx,
                         0, s, 0));
+  BT_TRY(mark(s));
   BT_TRY(bt::gemm_launch(L.ctx, w->ao_w, nullptr, nullptr, L.proj, T, k, k, BT_EPI_NONE, 0, s));
+  BT_TRY(mark(s));
   BT_TRY(bt_ln_bias_residual(L.proj, x, w->ao_b, w->ln0_g, w->ln0_b, w->ln0_eps, L.y0, T, k, stream));
+  BT_TRY(mark(s));
   BT_TRY(bt::gemm_launch(L.y0, w->w1, w->b1, nullptr, L.h1, T, f, k, BT_EPI_BIAS_GELU, 0, s));
+  BT_TRY(mark(s));
   BT_TRY(bt::gemm_launch(L.h1, w->w2, nullptr, nullptr, L.proj, T, k, f, BT_EPI_NONE, 0, s));
+  BT_TRY(mark(s));
   BT_TRY(bt_ln_bias_residual(L.proj, L.y0, w->b2, w->ln1_g, w->ln1_b, w->ln1_eps, x, T, k, stream));
+  BT_TRY(mark(s));
   return BT_OK;
+}
+}  // namespace bt
+
+extern "C" int bt_encoder_layer(const bt_layer_weights* w, const bt_layer_cfg* cfg, const int32_t* seq_starts, int bs,
+                                int T, void* x_inout, void* ws, size_t ws_bytes, bt_stream_t stream) {
+  return bt::encoder_layer_impl(w, cfg, seq_starts, bs, T, x_inout, ws, ws_bytes, stream);
 }
 
 extern "C" size_t bt_forward_workspace_bytes(const bt_layer_cfg* cfg, int bs, int T) {
@@ -123,11 +149,26 @@ extern "C" int bt_encoder_forward(const bt_layer_weights* layers, int n_layers, 
   void* lws = p;
   const size_t lws_bytes = bt_layer_workspace_bytes(cfg, T);
 
+  bt::g_fwd_event_idx = 0;
+  BT_TRY(bt::mark(bt::as_stream(stream)));
   BT_TRY(bt_plan_lengths(lengths, bs, mx, seq_starts, offsets, stream));
   BT_TRY(bt_pack(x_padded, BT_F32, offsets, T, k, x, BT_BF16, stream));
+  BT_TRY(bt::mark(bt::as_stream(stream)));
   for (int li = 0; li < n_layers; ++li)
-    BT_TRY(bt_encoder_layer(&layers[li], cfg, seq_starts, bs, T, x, lws, lws_bytes, stream));
+    BT_TRY(bt::encoder_layer_impl(&layers[li], cfg, seq_starts, bs, T, x, lws, lws_bytes, stream));
   BT_TRY(bt_unpack(x, BT_BF16, seq_starts, bs, mx, k, out_padded, BT_F32, stream));
+  BT_TRY(bt::mark(bt::as_stream(stream)));
+  return BT_OK;
+}
+
+// Debug hook: install (or clear, with NULL / 0) an array of n cudaEvent_t the
+// next bt_encoder_forward records after its launches: [0] start, [1] after
+// plan + pack, then 7 per layer (qkv, mha, attn-out, ln0, ffn1, ffn2,
+// ln1), then after unpack.
+extern "C" int bt_debug_forward_events(void** events, int n) {
+  bt::g_fwd_events = reinterpret_cast<cudaEvent_t*>(events);
+  bt::g_fwd_events_n = events ? n : 0;
+  bt::g_fwd_event_idx = 0;
   return BT_OK;
 }
 
@@ -152,7 +193,7 @@ extern "C" int bt_encoder_forward_packed(const bt_layer_weights* layers, int n_l
   BT_TRY(bt_plan_lengths(lengths, bs, mx, seq_starts, nullptr, stream));
   BT_TRY(bt_bias_act(x_packed, BT_F32, k, nullptr, x, BT_BF16, k, T, k, 0, stream));  // fp32 -> bf16
   for (int li = 0; li < n_layers; ++li)
-    BT_TRY(bt_encoder_layer(&layers[li], cfg, seq_starts, bs, T, x, lws, lws_bytes, stream));
+    BT_TRY(bt::encoder_layer_impl(&layers[li], cfg, seq_starts, bs, T, x, lws, lws_bytes, stream));
   BT_TRY(bt_bias_act(x, BT_BF16, k, nullptr, out_packed, BT_F32, k, T, k, 0, stream));  // bf16 -> fp32
   return BT_OK;
 }

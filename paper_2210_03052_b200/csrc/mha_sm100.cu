@@ -27,6 +27,7 @@ constexpr int MHA_SHORT_MAX_KEYS = 384;      // TMEM: 384 S columns + 64 O colum
 // globaltimer stamps per CTA, CTA index = linear block id.
 //   [0] prologue done  [1] Q landed (MMA warp)  [2+2t] S(t) ready (softmax)
 //   [3+2t] item t done (softmax)  [30] O ready  [31] output stored
+//   item t < 3: [16+4t] S in registers  [17+4t] max done  [18+4t] P V(t-1) done  [19+4t] P written
 __device__ unsigned long long* g_mha_trace = nullptr;
 #define MHA_TRACE(slot)                                                                                   \
   do {                                                                                                    \
@@ -45,6 +46,10 @@ struct MhaParams {
   int padded;      // 1: padded layout (reference mha_baseline, attention.py:135-174)
   int mx;          // max_seq_len (row stride of a sequence in the padded layout)
 };
+
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
 
 // Tie a register array to a preceding tcgen05.wait::ld.
 __device__ __forceinline__ void reg_tie(uint32_t (&r)[32]) {
@@ -90,20 +95,27 @@ __device__ __forceinline__ void store_out_row(const MhaParams& p, int grow, int 
 //   RESIDENT = false  long path (attention.py:240-296): 128-key K/V blocks
 //                     stream through an NST-deep TMA ring; work per CTA is the
 //                     sequence's true length (grouped problem sizes).
-// Softmax: single pass, online.  For each 128-key block the softmax warps read
-// S = Q K^T from TMEM twice (block max, then exp), rescale their running output
-// o (fp32 registers, thread = query row) and row sum l by exp(m_old - m_new),
-// write P = exp(s - m_new) (bf16, UMMA K-major SW128) to shared memory, and the
-// MMA warp computes the block's P V into a TMEM partial that the threads fold
-// into o.  This is the reference's long-path algorithm -- per-128-column tile
-// partial (max, sum) combined by a full reduction, then exp on load -- with the
-// reduction carried as a running (max, sum) so P never reaches HBM and S is
-// computed once.  Keys past the sequence end are masked (p = 0).
+// Softmax: single pass, online, with a lazily moved reference max.  For each
+// 128-key block a softmax thread (= query row = TMEM lane) loads its 128 S
+// values from TMEM ONCE into registers and releases the S columns at once, so
+// the MMA warp computes the next block's S while this block's exponentials
+// run.  P = 2^((s - m_ref) * scale * log2 e) goes to shared memory as bf16
+// (UMMA K-major SW128) and the MMA warp accumulates O += P V in TMEM across
+// blocks.  m_ref only moves when the row max exceeds it by more than 2^8 in
+// P units; then the thread rescales its O row in TMEM (ld / scale / st) and
+// its running sum.  O / l is exact for any reference point, so this is the
+// reference's long-path algorithm -- per-128-column tile partial (max, sum)
+// combined by a full reduction, then exp on load (tensor.py:166-173,
+// attention.py:104-122, grouped.py:202-206) -- with P never reaching HBM.
+// 3 of every 8 exponentials run as a polynomial on the FMA pipe (ex2_poly2)
+// so the SFU (16 ex2 / clk / SM) is not the softmax's bound.  Keys past the
+// sequence end are masked (p = 0).
 //
-// Warp roles (192 threads): warps 0-3 softmax / epilogue, warp 4 TMA producer,
-// warp 5 MMA issuer; both issuer warps walk their loops warp-uniformly and
-// issue through elect.sync.  TMEM: S [0,128), P V partial [128,192) -> 256
-// columns; ~112 KB smem -> two CTAs per SM, whose latency chains interleave.
+// Warp roles (384 threads): warps 0-7 softmax / epilogue (two threads per query
+// row, 64 keys each), warp 8 TMA producer, warp 9 MMA issuer, warps 10-11 idle
+// (they complete warpgroup 2 for setmaxnreg); both issuer warps walk their loops warp-uniformly and
+// issue through elect.sync.  TMEM: S [0,128), O [128,192) -> 256 columns;
+// ~112 KB smem -> two CTAs per SM, whose latency chains interleave.
 template <bool RESIDENT, int NST>
 struct MhaCfg {
   static constexpr uint32_t Q_OFF = 0;
@@ -113,10 +125,23 @@ struct MhaCfg {
   static constexpr size_t SMEM = BAR_OFF + 128;
 };
 
+#ifndef BT_MHA_POLY
+#define BT_MHA_POLY 6  // of every 16 exponentials, this many run as ex2_poly2 on the FMA pipe
+#endif
+constexpr float MHA_RESCALE_LOG2 = 8.0f;  // move m_ref once P would exceed 2^8
+// 384 threads x 2 CTAs/SM -> 80 registers each at launch (30720 per CTA).
+// The issuing warpgroup drops to 32 and the two softmax warpgroups rise to
+// 104 (256 x 104 + 128 x 32 = 30720): a thread holds 64 S values.
+constexpr int MHA_THREADS = 384;
+constexpr int MHA_REGS_ISSUE = 32;
+constexpr int MHA_REGS_SOFTMAX = 104;
+
 template <bool RESIDENT, int NST>
-__global__ void __launch_bounds__(192) mha_fwd_kernel(const __grid_constant__ CUtensorMap tm, const MhaParams p) {
+__global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_constant__ CUtensorMap tm,
+                                                                 const MhaParams p) {
   using Cfg = MhaCfg<RESIDENT, NST>;
-  const int qt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int qt = blockIdx.x, h = blockIdx.y;
+  const int b = blockIdx.z;
   const int sb = __ldg(p.seq_starts + b);
   const int len = __ldg(p.seq_starts + b + 1) - sb;
   // Packed layout: the sequence's rows start at seq_starts[b] and only its
@@ -138,9 +163,10 @@ __global__ void __launch_bounds__(192) mha_fwd_kernel(const __grid_constant__ CU
   uint64_t* q_full = bars;
   uint64_t* kv_full = bars + 1;         // [NST]
   uint64_t* kv_empty = bars + 1 + NST;  // [NST]
-  uint64_t* s_full = bars + 1 + 2 * NST;
-  uint64_t* s_free = s_full + 1;   // softmax done with S(j), P(j) is in smem
-  uint64_t* pv_done = s_full + 2;  // P(j) V(j) partial is in TMEM, sP free
+  uint64_t* s_full = bars + 1 + 2 * NST;  // S(j) in TMEM
+  uint64_t* s_read = s_full + 1;          // softmax has S(j) in registers: S columns free
+  uint64_t* p_full = s_full + 2;          // P(j) in smem, O rescaled: issue P(j) V(j)
+  uint64_t* pv_done = s_full + 3;         // P(j) V(j) accumulated into O: sP free
   uint32_t* holder = reinterpret_cast<uint32_t*>(s_full + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -152,7 +178,8 @@ __global__ void __launch_bounds__(192) mha_fwd_kernel(const __grid_constant__ CU
       ptx::mbar_init(&kv_empty[i], 1);
     }
     ptx::mbar_init(s_full, 1);
-    ptx::mbar_init(s_free, 128);
+    ptx::mbar_init(s_read, 256);
+    ptx::mbar_init(p_full, 256);
     ptx::mbar_init(pv_done, 1);
     ptx::fence_mbar_init();
   }
@@ -164,11 +191,15 @@ __global__ void __launch_bounds__(192) mha_fwd_kernel(const __grid_constant__ CU
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *holder;
-  constexpr uint32_t S_COL = 0, O_COL = 128;
+  // TMEM columns: S [0,128), O [128,192), row-partial exchange between the
+  // two threads of a row [192,198): max (2 parities x 2 halves), then sum
+  constexpr uint32_t S_COL = 0, O_COL = 128, X_COL = 192;
   ptx::griddep_launch_dependents();
   if (threadIdx.x == 0) MHA_TRACE(0);
 
-  if (warp == 4) {
+  if (warp >= 8) {
+    ptx::setmaxnreg_dec<MHA_REGS_ISSUE>();  // warpgroup 2: TMA (warp 8), MMA (warp 9), 2 idle warps
+  if (warp == 8) {
     // ------------------------------------------------ TMA producer
     ptx::griddep_wait();  // qkv is produced by the previous kernel
     if (ptx::elect_one()) {
@@ -187,7 +218,7 @@ __global__ void __launch_bounds__(192) mha_fwd_kernel(const __grid_constant__ CU
       }
       __syncwarp();
     }
-  } else if (warp == 5) {
+  } else if (warp == 9) {
     // ------------------------------------------------ MMA issuer
     constexpr uint32_t idesc_s = ptx::idesc_bf16(128, MHA_KB, false, false);  // Q K^T, both K-major
     constexpr uint32_t idesc_o = ptx::idesc_bf16(128, MHA_D, false, true);    // P (K-major) x V (MN-major)
@@ -196,175 +227,217 @@ __global__ void __launch_bounds__(192) mha_fwd_kernel(const __grid_constant__ CU
     const uint32_t kv_base = ptx::smem_u32(sKV);
     ptx::mbar_wait(q_full, 0);
     if (lane == 0) MHA_TRACE(1);
+    auto issue_pv = [&](int pj, int pslot) {
+      // O (+)= P(pj) V(pj); only the k-steps that hold keys of the problem
+      ptx::mbar_wait(p_full, pj & 1);
+      ptx::tc_fence_after();
+      const int nks = min(MHA_KB, work - pj * MHA_KB + 15) / 16;
+      const uint64_t v_desc = ptx::sdesc_sw128(kv_base + pslot * 2 * MHA_TILE + MHA_TILE, 1024, MHA_TILE);
+      if (ptx::elect_one()) {
+        for (int ks = 0; ks < nks; ++ks)
+          ptx::mma_bf16_ss(tmem + O_COL, p_desc + (ks >> 2) * (MHA_TILE >> 4) + (ks & 3) * 2,
+                           v_desc + ks * ((16 * 128) >> 4), idesc_o, (pj > 0 || ks > 0) ? 1u : 0u);
+        ptx::mma_commit(pv_done);
+        if (!RESIDENT) ptx::mma_commit(&kv_empty[pslot]);  // K and V of block pj consumed
+      }
+      __syncwarp();
+    };
     int prev_slot = 0;
-    for (int j = 0; j <= nkb; ++j) {
+    for (int j = 0; j < nkb; ++j) {
       const int slot = RESIDENT ? j : j % NST;
-      if (j > 0) ptx::mbar_wait(s_free, (j - 1) & 1);  // softmax done with S(j-1); P(j-1) is in smem
-      if (j < nkb) {
-        ptx::mbar_wait(&kv_full[slot], RESIDENT ? 0u : static_cast<uint32_t>((j / NST) & 1));
-        ptx::tc_fence_after();
-        const uint64_t k_desc = ptx::sdesc_sw128(kv_base + slot * 2 * MHA_TILE, 1024, 16);
-        if (ptx::elect_one()) {
+      ptx::mbar_wait(&kv_full[slot], RESIDENT ? 0u : static_cast<uint32_t>((j / NST) & 1));
+      if (j > 0) ptx::mbar_wait(s_read, (j - 1) & 1);  // S(j-1) is in the softmax registers
+      ptx::tc_fence_after();
+      const uint64_t k_desc = ptx::sdesc_sw128(kv_base + slot * 2 * MHA_TILE, 1024, 16);
+      if (ptx::elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < MHA_D / 16; ++kk)
-            ptx::mma_bf16_ss(tmem + S_COL, q_desc + 2 * kk, k_desc + 2 * kk, idesc_s, kk > 0);
-          ptx::mma_commit(s_full);
-        }
-        __syncwarp();
-      } else {
-        ptx::tc_fence_after();
+        for (int kk = 0; kk < MHA_D / 16; ++kk)
+          ptx::mma_bf16_ss(tmem + S_COL, q_desc + 2 * kk, k_desc + 2 * kk, idesc_s, kk > 0);
+        ptx::mma_commit(s_full);
       }
-      if (j > 0) {
-        // P(j-1) V(j-1) -> TMEM partial (fresh each block; the threads fold it in)
-        const int pj = j - 1;
-        const int nks = min(MHA_KB, work - pj * MHA_KB + 15) / 16;
-        const uint64_t v_desc = ptx::sdesc_sw128(kv_base + prev_slot * 2 * MHA_TILE + MHA_TILE, 1024, MHA_TILE);
-        if (ptx::elect_one()) {
-          for (int ks = 0; ks < nks; ++ks)
-            ptx::mma_bf16_ss(tmem + O_COL, p_desc + (ks >> 2) * (MHA_TILE >> 4) + (ks & 3) * 2,
-                             v_desc + ks * ((16 * 128) >> 4), idesc_o, ks != 0);
-          ptx::mma_commit(pv_done);
-          if (!RESIDENT) ptx::mma_commit(&kv_empty[prev_slot]);  // K and V of block j-1 consumed
-        }
-        __syncwarp();
-      }
+      __syncwarp();
+      if (j > 0) issue_pv(j - 1, prev_slot);
       prev_slot = slot;
     }
+    issue_pv(nkb - 1, prev_slot);
+  }
   } else {
-    // ------------------------------------------------ softmax (thread = query row = TMEM lane)
-    // Work is skipped warp-uniformly where it cannot matter: warps whose 32
-    // query rows all lie past the sequence end, and 32-key chunks past it.
-    const int row = warp * 32 + lane;
-    const bool warp_live = q0 + warp * 32 < work;
-    const uint32_t trow = tmem + (static_cast<uint32_t>(warp * 32) << 16);
-    // o: running output row (fp32 pairs, FFMA2); every hot loop below uses
-    // paired fp32 ops / 3-input max -- the softmax is instruction-issue bound
-    unsigned long long o2[32];
-#pragma unroll
-    for (int i = 0; i < 32; ++i) o2[i] = 0ull;
-    float mrow = -INFINITY, lsum = 0.f, alpha_prev = 0.f;
-    // fold the TMEM partial P(j-1) V(j-1) into o (after rescaling o to m(j-1))
-    auto fold_partial = [&](float alpha) {
-      const unsigned long long a2 = ptx::f2(alpha, alpha);
-#pragma unroll
-      for (int half = 0; half < 2; ++half) {
-        uint32_t r[32];
-        ptx::tmem_ld32(trow + O_COL + 32 * half, r);
-        ptx::tmem_wait_ld(r);
-#pragma unroll
-        for (int i = 0; i < 16; ++i)
-          o2[16 * half + i] = ptx::fma2(o2[16 * half + i], a2, ptx::f2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1])));
-      }
-    };
-    const unsigned long long sl2x2 = ptx::f2(p.sl2, p.sl2);
+    ptx::setmaxnreg_inc<MHA_REGS_SOFTMAX>();  // warpgroups 0-1: softmax
+    // ------------------------------------------------ softmax: a row of S is
+    // shared by two threads -- warp w (half 0: keys 0-63 of each block) and
+    // warp w+4 (half 1: keys 64-127) own TMEM lanes 32*(w%4)..+31.  Row max
+    // is combined through shared memory once per block; row sums stay
+    // per-thread partials until the end.  Warp-uniform skipping: warps whose
+    // 32 query rows lie past the sequence end, and key chunks past it.
+    const int quarter = warp & 3, half = warp >> 2;
+    const int row = quarter * 32 + lane;
+    const int pair_bar = 1 + quarter;  // named barrier of warps quarter and quarter + 4
+    const bool warp_live = q0 + quarter * 32 < work;
+    const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
+    const uint32_t s_my = trow + S_COL + half * 64;
+    const uint32_t o_my = trow + O_COL + half * 32;
+    const float sl2 = p.sl2;
+    float mref = -INFINITY, lsum = 0.f;
+    uint8_t* prow = sP + half * MHA_TILE + row * 128;  // my 64 keys = one K-major SW128 column block
     for (int j = 0; j < nkb; ++j) {
-      const int kbase = j * MHA_KB;
-      const int kvalid = min(MHA_KB, len - kbase);  // valid keys in this block (<= 0: all masked)
+      const int kvalid = min(MHA_KB, len - j * MHA_KB) - half * 64;  // valid keys among my 64 (may be <= 0)
       ptx::mbar_wait(s_full, j & 1);
       ptx::tc_fence_after();
       if (threadIdx.x == 0) MHA_TRACE(2 + 2 * j);
-      float alpha = 1.f, msc = 0.f;
+      uint32_t r0[32], r1[32];  // my 64 S values of this row
       if (warp_live) {
-        // block max over the valid keys -> running max
-        float bmax = -INFINITY;
-#pragma unroll 1
-        for (int c = 0; c < kvalid; c += 32) {
-          uint32_t r[32];
-          ptx::tmem_ld32(trow + S_COL + c, r);
-          ptx::tmem_wait_ld(r);
-          if (c + 32 <= kvalid) {
+        ptx::tmem_ld32(s_my, r0);
+        ptx::tmem_ld32(s_my + 32, r1);
+        ptx::tmem_wait_ld(r0);
+        reg_tie(r1);
+      }
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(s_read);  // the MMA warp may overwrite S with the next block
+      if (threadIdx.x == 0 && j < 3) MHA_TRACE(16 + 4 * j);
+#define SV(c, i) __uint_as_float((c) == 0 ? r0[i] : r1[i])
+      bool need = false;
+      float mnew = mref;
+      if (warp_live) {
+        if (kvalid < 64) {
+          // keys past the problem's end: s = -inf (out of the max; exp -> 0)
 #pragma unroll
-            for (int i = 0; i < 32; i += 2) bmax = ptx::max3(bmax, __uint_as_float(r[i]), __uint_as_float(r[i + 1]));
-          } else {
-#pragma unroll
-            for (int i = 0; i < 32; ++i)
-              if (c + i < kvalid) bmax = fmaxf(bmax, __uint_as_float(r[i]));
+          for (int i = 0; i < 32; ++i) {
+            if (i >= kvalid) r0[i] = 0xff800000u;
+            if (32 + i >= kvalid) r1[i] = 0xff800000u;
           }
         }
-        const float mnew = fmaxf(mrow, bmax);
-        alpha = (mrow == -INFINITY) ? 0.f : ptx::ex2_approx((mrow - mnew) * p.sl2);
-        mrow = mnew;
-        msc = mnew * p.sl2;
-      }
-      if (j > 0) {
-        ptx::mbar_wait(pv_done, (j - 1) & 1);  // P(j-1) V(j-1) landed; sP is free
+        float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 8) {
+            m4[0] = ptx::max3(m4[0], SV(c, i), SV(c, i + 1));
+            m4[1] = ptx::max3(m4[1], SV(c, i + 2), SV(c, i + 3));
+            m4[2] = ptx::max3(m4[2], SV(c, i + 4), SV(c, i + 5));
+            m4[3] = ptx::max3(m4[3], SV(c, i + 6), SV(c, i + 7));
+          }
+        }
+        // exchange the partial max with the row's other thread through TMEM
+        const float pmax = fmaxf(ptx::max3(m4[0], m4[1], m4[2]), m4[3]);
+        ptx::tmem_st1(trow + X_COL + 2 * (j & 1) + half, __float_as_uint(pmax));
+        ptx::tmem_wait_st();
+        ptx::tc_fence_before();
+        named_bar_sync(pair_bar, 64);
         ptx::tc_fence_after();
-        if (warp_live) fold_partial(alpha_prev);
+        const float bmax = fmaxf(pmax, __uint_as_float(ptx::tmem_ld1(trow + X_COL + 2 * (j & 1) + (half ^ 1))));
+        mnew = fmaxf(mref, bmax);
+        need = (mnew - mref) * sl2 > MHA_RESCALE_LOG2;  // true on the first block (mref = -inf)
       }
+      if (threadIdx.x == 0 && j < 3) MHA_TRACE(17 + 4 * j);
+      if (j > 0) {
+        ptx::mbar_wait(pv_done, (j - 1) & 1);  // P(j-1) V(j-1) is in O; sP is free
+        ptx::tc_fence_after();
+      }
+      if (threadIdx.x == 0 && j < 3) MHA_TRACE(18 + 4 * j);
       if (warp_live) {
-        const unsigned long long nm2 = ptx::f2(-msc, -msc);
-        unsigned long long bsum2 = 0ull;
-        float bsum_tail = 0.f;
-#pragma unroll 1
-        for (int c = 0; c < MHA_KB; c += 32) {
-          uint32_t pk[16];
-          if (c + 32 <= kvalid) {
-            uint32_t r[32];
-            ptx::tmem_ld32(trow + S_COL + c, r);
-            ptx::tmem_wait_ld(r);
+        // the reference max moves (rare): my 32 O columns are rescaled after
+        // P is written (S registers are dead by then), before P(j) V(j)
+        const bool any_resc = __any_sync(0xffffffffu, need && j > 0);
+        const float alpha = (need && mref != -INFINITY) ? ptx::ex2_approx((mref - mnew) * sl2) : 1.f;
+        if (need) mref = mnew;
+        const float msc = mref * sl2;
+        const unsigned long long sl2x2 = ptx::f2(sl2, sl2), nm2 = ptx::f2(-msc, -msc);
+        unsigned long long sum4[4] = {0ull, 0ull, 0ull, 0ull};  // 4 independent add chains
 #pragma unroll
-            for (int i = 0; i < 32; i += 2) {
-              float x0, x1;
-              ptx::unf2(ptx::fma2(ptx::f2(__uint_as_float(r[i]), __uint_as_float(r[i + 1])), sl2x2, nm2), x0, x1);
-              const float e0 = ptx::ex2_approx(x0), e1 = ptx::ex2_approx(x1);
-              bsum2 = ptx::add2(bsum2, ptx::f2(e0, e1));
-              pk[i / 2] = ptx::pack_bf16x2(e0, e1);
+        for (int c = 0; c < 2; ++c) {
+          // P for 32 keys: BT_MHA_POLY of every 16 exponentials on the FMA pipe,
+          // the rest on the SFU; K-major SW128 store (16 B chunks XOR-swizzled by row % 8)
+          const int cb = c * 4;  // first 16 B chunk of these 32 keys in the 128 B row
+          float ev[32];
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            float x0, x1;
+            ptx::unf2(ptx::fma2(ptx::f2(SV(c, i), SV(c, i + 1)), sl2x2, nm2), x0, x1);
+            if ((i & 15) < BT_MHA_POLY) {
+              ptx::ex2_poly2(x0, x1, ev[i], ev[i + 1]);
+              ev[i] = x0 >= -125.0f ? ev[i] : 0.f;  // masked key (x = -inf): exactly 0
+              ev[i + 1] = x1 >= -125.0f ? ev[i + 1] : 0.f;
+            } else {
+              ev[i] = ptx::ex2_approx(x0);  // ex2(-inf) = 0
+              ev[i + 1] = ptx::ex2_approx(x1);
             }
-          } else if (c < kvalid) {
-            uint32_t r[32];
-            ptx::tmem_ld32(trow + S_COL + c, r);
-            ptx::tmem_wait_ld(r);
-#pragma unroll
-            for (int i = 0; i < 32; i += 2) {
-              const float e0 = (c + i < kvalid) ? ptx::ex2_approx(fmaf(__uint_as_float(r[i]), p.sl2, -msc)) : 0.f;
-              const float e1 =
-                  (c + i + 1 < kvalid) ? ptx::ex2_approx(fmaf(__uint_as_float(r[i + 1]), p.sl2, -msc)) : 0.f;
-              bsum_tail += e0 + e1;
-              pk[i / 2] = ptx::pack_bf16x2(e0, e1);
-            }
-          } else {
-#pragma unroll
-            for (int i = 0; i < 16; ++i) pk[i] = 0u;
           }
-          store_p32(sP, row, c, pk);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uint32_t pk[4];
+#pragma unroll
+            for (int e = 0; e < 8; e += 2) {
+              sum4[e / 2] = ptx::add2(sum4[e / 2], ptx::f2(ev[8 * q + e], ev[8 * q + e + 1]));
+              pk[e / 2] = ptx::pack_bf16x2(ev[8 * q + e], ev[8 * q + e + 1]);
+            }
+            *reinterpret_cast<uint4*>(prow + (((cb + q) ^ (row & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          }
         }
+        const unsigned long long bsum2 = ptx::add2(ptx::add2(sum4[0], sum4[1]), ptx::add2(sum4[2], sum4[3]));
+        if (threadIdx.x == 0 && j < 3) MHA_TRACE(19 + 4 * j);
         float s0f, s1f;
         ptx::unf2(bsum2, s0f, s1f);
-        lsum = lsum * alpha + (s0f + s1f + bsum_tail);
-        alpha_prev = alpha;
+        lsum = lsum * alpha + (s0f + s1f);  // my keys' partial row sum
+        if (any_resc) {
+          // my 32 O columns *= 2^((m_old - m_new) * scale)
+          const unsigned long long a2 = ptx::f2(alpha, alpha);
+          uint32_t o[32];
+          ptx::tmem_ld32(o_my, o);
+          ptx::tmem_wait_ld(o);
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            float a, c;
+            ptx::unf2(ptx::mul2(ptx::f2(__uint_as_float(o[i]), __uint_as_float(o[i + 1])), a2), a, c);
+            o[i] = __float_as_uint(a);
+            o[i + 1] = __float_as_uint(c);
+          }
+          ptx::tmem_st32(o_my, o);
+          ptx::tmem_wait_st();
+        }
       }
       ptx::fence_proxy_async_smem();
       ptx::tc_fence_before();
-      ptx::mbar_arrive(s_free);
+      ptx::mbar_arrive(p_full);
       if (threadIdx.x == 0) MHA_TRACE(3 + 2 * j);
     }
+#undef SV
     ptx::mbar_wait(pv_done, (nkb - 1) & 1);
     ptx::tc_fence_after();
     if (threadIdx.x == 0) MHA_TRACE(30);
-    // o / l -> bf16 rows staged in sP (free: the last P V has completed) ->
+    // O / l -> bf16 rows staged in sP (free: the last P V has completed) ->
     // coalesced 16-byte stores, 4 rows per warp instruction
     if (warp_live) {
-      fold_partial(alpha_prev);
-      const float inv = (q0 + row < len) ? 1.0f / lsum : 0.f;
+      uint32_t o[32];
+      ptx::tmem_ld32(o_my, o);
+      ptx::tmem_wait_ld(o);
+      ptx::tmem_st1(trow + X_COL + 4 + half, __float_as_uint(lsum));
+      ptx::tmem_wait_st();
+      ptx::tc_fence_before();
+      named_bar_sync(pair_bar, 64);
+      ptx::tc_fence_after();
+      const float l = lsum + __uint_as_float(ptx::tmem_ld1(trow + X_COL + 4 + (half ^ 1)));
+      const float inv = (q0 + row < len) ? 1.0f / l : 0.f;
       const unsigned long long inv2 = ptx::f2(inv, inv);
       uint8_t* mine = sP + row * 128;
 #pragma unroll
-      for (int jj = 0; jj < 8; ++jj) {
+      for (int jj = 0; jj < 4; ++jj) {
         uint32_t w[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           float a, b2;
-          ptx::unf2(ptx::mul2(o2[4 * jj + e], inv2), a, b2);
+          ptx::unf2(ptx::mul2(ptx::f2(__uint_as_float(o[8 * jj + 2 * e]), __uint_as_float(o[8 * jj + 2 * e + 1])), inv2),
+                    a, b2);
           w[e] = ptx::pack_bf16x2(a, b2);
         }
-        *reinterpret_cast<uint4*>(mine + ((jj ^ (row & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
+        const int chunk = half * 4 + jj;
+        *reinterpret_cast<uint4*>(mine + ((chunk ^ (row & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
       }
-      __syncwarp();
+      named_bar_sync(pair_bar, 64);  // both halves of the pair's 32 rows are staged
       ptx::griddep_wait();  // out may still be read by the previous kernel
-      // lane -> (row in this warp's 32-row slab, 16 B chunk): 4 rows per instruction
+      // lane -> (row in this pair's 32-row slab, 16 B chunk); warp half h stores rows h*16..h*16+15
 #pragma unroll
-      for (int it = 0; it < 8; ++it) {
-        const int rr = warp * 32 + it * 4 + (lane >> 3);
+      for (int it = 0; it < 4; ++it) {
+        const int rr = quarter * 32 + half * 16 + it * 4 + (lane >> 3);
         const int jj = lane & 7;
         if (q0 + rr < work) {
           const uint4 v = *reinterpret_cast<const uint4*>(sP + rr * 128 + ((jj ^ (rr & 7)) << 4));
@@ -414,15 +487,15 @@ int mha_launch(const void* qkv, const int32_t* seq_starts, int bs, int mx, int H
   if (use_short && mx <= 2 * MHA_KB) {
     static bool set = false;
     if (!set) { BT_TRY(set_smem(mha_fwd_kernel<true, 2>, MhaCfg<true, 2>::SMEM)); set = true; }
-    BT_LAUNCH((mha_fwd_kernel<true, 2>), grid, dim3(192), MhaCfg<true, 2>::SMEM, s, 1, tm, p);
+    BT_LAUNCH((mha_fwd_kernel<true, 2>), grid, dim3(MHA_THREADS), MhaCfg<true, 2>::SMEM, s, 1, tm, p);
   } else if (use_short) {
     static bool set = false;
     if (!set) { BT_TRY(set_smem(mha_fwd_kernel<true, 3>, MhaCfg<true, 3>::SMEM)); set = true; }
-    BT_LAUNCH((mha_fwd_kernel<true, 3>), grid, dim3(192), MhaCfg<true, 3>::SMEM, s, 1, tm, p);
+    BT_LAUNCH((mha_fwd_kernel<true, 3>), grid, dim3(MHA_THREADS), MhaCfg<true, 3>::SMEM, s, 1, tm, p);
   } else {
     static bool set = false;
     if (!set) { BT_TRY(set_smem(mha_fwd_kernel<false, 2>, MhaCfg<false, 2>::SMEM)); set = true; }
-    BT_LAUNCH((mha_fwd_kernel<false, 2>), grid, dim3(192), MhaCfg<false, 2>::SMEM, s, 1, tm, p);
+    BT_LAUNCH((mha_fwd_kernel<false, 2>), grid, dim3(MHA_THREADS), MhaCfg<false, 2>::SMEM, s, 1, tm, p);
   }
   return BT_OK;
 }

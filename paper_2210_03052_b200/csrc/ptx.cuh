@@ -113,6 +113,16 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// Warpgroup register reallocation (all 4 warps of a warpgroup execute it).
+template <int N>
+__device__ __forceinline__ void setmaxnreg_inc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
+}
+template <int N>
+__device__ __forceinline__ void setmaxnreg_dec() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
+}
+
 // ---------------------------------------------------------------- tcgen05
 __device__ __forceinline__ void tmem_alloc(uint32_t* holder, uint32_t ncols) {  // whole warp
   asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(holder)),
@@ -168,6 +178,32 @@ __device__ __forceinline__ void tmem_wait_ld(uint32_t (&r)[32]) {
                :
                : "memory");
 }
+
+// registers -> TMEM: 32 lanes x 32 consecutive 32-bit columns (one row per thread)
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+// one 32-bit column: lane i of the warp <-> TMEM lane (base lane + i)
+__device__ __forceinline__ void tmem_st1(uint32_t taddr, uint32_t v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t tmem_ld1(uint32_t taddr) {
+  uint32_t v;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];\n\ttcgen05.wait::ld.sync.aligned;"
+               : "=r"(v)
+               : "r"(taddr)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 // UMMA shared-memory descriptor, SWIZZLE_128B (layout type 2), version 1.
 //   K-major operand:  rows of 128 B (64 bf16 along K), 8-row atoms of 1024 B,
@@ -313,11 +349,47 @@ __device__ __forceinline__ float max3(float a, float b, float c) {
   return d;
 }
 
+// 2^x on the FMA pipe for a pair (offloads the SFU, whose ex2 issues at
+// 16 / clk / SM): x = n + f with n = rint(x) (the 1.5 * 2^23 trick), 2^f by a
+// degree-3 polynomial on [-0.5, 0.5] (rel. error < 2.5e-4, below bf16's
+// 2^-9), 2^n added into the exponent field.  x is clamped to >= -125.
+__device__ __forceinline__ unsigned long long sub2(unsigned long long a, unsigned long long b) {
+  unsigned long long d;
+  asm("sub.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ void ex2_poly2(float x0, float x1, float& y0, float& y1) {
+  const unsigned long long magic = f2(12582912.0f, 12582912.0f);
+  const unsigned long long x = f2(fmaxf(x0, -125.0f), fmaxf(x1, -125.0f));
+  const unsigned long long t = add2(x, magic);
+  const unsigned long long fr = sub2(x, sub2(t, magic));
+  unsigned long long p = fma2(f2(0.05484628f, 0.05484628f), fr, f2(0.24180230f, 0.24180230f));
+  p = fma2(p, fr, f2(0.69324806f, 0.69324806f));
+  p = fma2(p, fr, f2(0.99998888f, 0.99998888f));
+  float p0, p1, t0, t1;
+  unf2(p, p0, p1);
+  unf2(t, t0, t1);
+  y0 = __int_as_float(__float_as_int(p0) + ((__float_as_int(t0) - 0x4B400000) << 23));
+  y1 = __int_as_float(__float_as_int(p1) + ((__float_as_int(t1) - 0x4B400000) << 23));
+}
+
 // tanh-form GELU (reference fusion.py:23-27)
 __device__ __forceinline__ float gelu_tanh(float x) {
   const float c = 0.7978845608028654f;  // sqrt(2/pi)
   const float a = 0.044715f;
   return 0.5f * x * (1.0f + tanh_approx(c * (x + a * x * x * x)));
+}
+// the same on a pair with paired fp32 ops: u = x (c + c a x^2), y = h + h tanh(u), h = x / 2
+__device__ __forceinline__ void gelu_tanh2(float& x0, float& x1) {
+  const float c = 0.7978845608028654f, ca = 0.7978845608028654f * 0.044715f;
+  const unsigned long long x = f2(x0, x1);
+  const unsigned long long x2 = mul2(x, x);
+  const unsigned long long u = mul2(x, fma2(x2, f2(ca, ca), f2(c, c)));
+  const unsigned long long hx = mul2(x, f2(0.5f, 0.5f));
+  float u0, u1;
+  unf2(u, u0, u1);
+  const unsigned long long t = f2(tanh_approx(u0), tanh_approx(u1));
+  unf2(fma2(hx, t, hx), x0, x1);
 }
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);

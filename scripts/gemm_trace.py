@@ -25,7 +25,7 @@ def main():
     W = (torch.randn(N, K, device="cuda") / math.sqrt(K)).to(torch.bfloat16)
     bias = torch.randn(N, device="cuda") * 0.1
     C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
-    for _ in range(3):
+    for _ in range(2000):  # warm: clocks up to their loaded level before the traced launch
         gemm_device(A, W, bias if epi else None, None, epi, out=C, bn=bn or None)
     buf = torch.zeros(148 * 64, dtype=torch.int64, device="cuda")
     _lib.call("bt_debug_gemm_trace", buf.data_ptr())

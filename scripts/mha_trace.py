@@ -22,7 +22,7 @@ def main():
     seqs = harness.gen_lengths(bs, mx, "fixed", seed=0, alpha=0.6)
     plan = plan_for_lengths(seqs)
     qkv = torch.randn(plan.valid_word_cnt, 3 * H * 64, device="cuda").to(torch.bfloat16)
-    for _ in range(3):
+    for _ in range(2000):  # warm: clocks up to their loaded level before the traced launch
         mha_device(qkv, plan, H, 64)
     nq = (mx + 127) // 128
     n = nq * H * bs
@@ -45,7 +45,7 @@ def main():
         qt, rest = c % nq, c // nq
         h, b = rest % H, rest // H
         s = f"cta q{qt} h{h} b{b} len {lens[b]}: start {r(row[0]):.2f} Q {r(row[1]):.2f} |"
-        for i in range(14):
+        for i in range(7):
             if row[2 + 2 * i] == 0:
                 break
             s += f" S{i} {r(row[2 + 2 * i]):.2f}-{r(row[3 + 2 * i]):.2f}"
@@ -55,11 +55,19 @@ def main():
     print(f"Q-load latency median {np.median(q_lat) / 1e3:.2f} us")
     s0 = t[used, 2] - t[used, 1]
     print(f"Q->S0 ready median {np.median(s0) / 1e3:.2f} us")
-    soft = [(t[c, 3 + 2 * i] - t[c, 2 + 2 * i]) / 1e3 for c in np.nonzero(used)[0] for i in range(14)
+    soft = [(t[c, 3 + 2 * i] - t[c, 2 + 2 * i]) / 1e3 for c in np.nonzero(used)[0] for i in range(7)
             if t[c, 2 + 2 * i] > 0 and t[c, 3 + 2 * i] > 0]
-    gaps = [(t[c, 2 + 2 * (i + 1)] - t[c, 3 + 2 * i]) / 1e3 for c in np.nonzero(used)[0] for i in range(13)
+    gaps = [(t[c, 2 + 2 * (i + 1)] - t[c, 3 + 2 * i]) / 1e3 for c in np.nonzero(used)[0] for i in range(6)
             if t[c, 2 + 2 * (i + 1)] > 0 and t[c, 3 + 2 * i] > 0]
     print(f"softmax per item median {np.median(soft):.2f} us; item-done -> next S ready median {np.median(gaps):.2f} us")
+    for j in range(3):
+        rows = [c for c in np.nonzero(used)[0] if t[c, 2 + 2 * j] > 0 and t[c, 19 + 4 * j] > 0]
+        if not rows:
+            break
+        d = lambda a, b: np.median([(t[c, b] - t[c, a]) / 1e3 for c in rows])  # noqa: E731
+        print(f"item {j} (n={len(rows)}): S ready->in regs {d(2 + 2 * j, 16 + 4 * j):.2f}  max {d(16 + 4 * j, 17 + 4 * j):.2f}"
+              f"  wait PV {d(17 + 4 * j, 18 + 4 * j):.2f}  exps+store {d(18 + 4 * j, 19 + 4 * j):.2f}"
+              f"  rescale+arrive {d(19 + 4 * j, 3 + 2 * j):.2f} us")
     fin = [(t[c, 31] - t[c, 30]) / 1e3 for c in np.nonzero(used)[0]]
     print(f"O ready -> stored median {np.median(fin):.2f} us")
 

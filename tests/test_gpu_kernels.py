@@ -249,3 +249,25 @@ def test_gemm_streamk(env, bn, epi, M, N, K):
     torch.cuda.synchronize()
     assert rel_fro(out, ref) < 6e-3, (bn, epi, M, N, K, rel_fro(out, ref))
     assert torch.equal(out, out2)
+
+
+@pytest.mark.parametrize("path,lens,mx", [(1, [384, 300, 140, 129], 384), (2, [700, 260, 131], 768)])
+def test_mha_reference_max_moves(env, path, lens, mx):
+    """Keys 128..255 of every sequence get 4x larger logits, so a row's max
+    jumps by more than 2^8 in P units after the first key block: the
+    kernel's lazily moved reference max must rescale O and l in place."""
+    bt, torch = env
+    from paper_2210_03052_b200.attention import mha_device
+
+    heads = 2
+    hid = heads * 64
+    plan = bt.plan_for_lengths(bt.SeqLengths.of(lens, mx))
+    qkv = _rand_qkv(torch, plan.valid_word_cnt, hid, seed=11)
+    s = plan.seq_starts
+    for b in range(len(lens)):
+        lo, hi = s[b] + 128, min(s[b] + 256, s[b + 1])
+        if hi > lo:
+            qkv[lo:hi, hid:2 * hid] *= 4  # exact in bf16
+    out = mha_device(qkv, plan, heads, 64, path=path)
+    ref = _oracle_mha(qkv, plan, heads, mx)
+    assert_close_bf16(out, ref, what=f"rescale path{path}")
