@@ -126,6 +126,15 @@ BT_API int bt_mha_padded(const void* qkv, const int32_t* seq_starts, int bs, int
 BT_API int bt_ln_bias_residual(const void* x, const void* residual, const float* bias, const float* gamma,
                         const float* beta, float eps, void* out, int T, int k, bt_stream_t stream);
 
+/* Fused attention-output / FFN2 projection + add-bias + residual + LayerNorm (encoder.py:385-388 and
+ * :404-407, i.e. gemm then fusion.py:79 add_bias_residual_layernorm):
+ *   out[M,N] = LN((A[M,K] Bt[N,K]^T + residual) + bias) * gamma + beta,  bf16 in / out, fp32 math.
+ * N in {512, 768, 1024}; one row block per thread-block cluster of N/128 CTAs (row statistics combined
+ * through distributed shared memory). */
+BT_API int bt_gemm_bias_residual_ln(const void* A, const void* Bt, const float* bias, const void* residual,
+                                    const float* gamma, const float* beta, float eps, void* out, int M, int N,
+                                    int K, bt_stream_t stream);
+
 /* ---- element-wise passes (fusion.py:23-76; unfused ladder variants) ---- */
 
 /* out[r, c] = act(x[r, c] + bias[c]) for r < rows, c < cols (act 0 = none,

@@ -12,6 +12,8 @@
 //   h2   = h1 W2                             GEMM #3
 //   x    = LN((h2 + y0) + b2)                fused add-bias+residual+LN
 
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace bt {
@@ -19,6 +21,22 @@ int gemm_launch(const void* A, const void* Bt, const float* bias, const void* re
                 int epi, int force_bn, cudaStream_t s);
 int mha_launch(const void* qkv, const int32_t* seq_starts, int bs, int mx, int H, int d, int cutoff, int T, void* out,
                int force_path, cudaStream_t s, int padded);
+bool gemm_ln_fits(int M, int N, int K);
+int gemm_ln_launch(const void* A, const void* Bt, const float* bias, const void* residual, const float* gamma,
+                   const float* beta, float eps, void* Y, int M, int N, int K, cudaStream_t s);
+// BT_FUSED_LN: 0 = GEMM + separate LayerNorm kernel everywhere, 1 (default) =
+// the fused GEMM+LN kernel after the attention-output GEMM (K = k), 2 = after
+// both projections (where gemm_ln_fits).  Measured at C2 (ms/step): 0.802 /
+// 0.787 / 0.809 -- at K = 4k the fused kernel's 128 x 128 tiles lose more
+// mainloop efficiency than the separate LayerNorm launch costs.
+static int fused_ln_mode() {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = getenv("BT_FUSED_LN");
+    mode = (e && e[0] >= '0' && e[0] <= '2') ? e[0] - '0' : 1;
+  }
+  return mode;
+}
 
 
 static inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
@@ -102,15 +120,25 @@ static int encoder_layer_impl(const bt_layer_weights* w, const bt_layer_cfg* cfg
   BT_TRY(bt::mha_launch(L.qkv, seq_starts, bs, cfg->max_seq_len, cfg->head_num, cfg->head_size, cfg->cutoff, T, L.ctx,
                         0, s, 0));
   BT_TRY(mark(s));
-  BT_TRY(bt::gemm_launch(L.ctx, w->ao_w, nullptr, nullptr, L.proj, T, k, k, BT_EPI_NONE, 0, s));
-  BT_TRY(mark(s));
-  BT_TRY(bt_ln_bias_residual(L.proj, x, w->ao_b, w->ln0_g, w->ln0_b, w->ln0_eps, L.y0, T, k, stream));
+  if (fused_ln_mode() >= 1 && gemm_ln_fits(T, k, k)) {  // y0 = LN((ctx Wo + x) + bo), one kernel
+    BT_TRY(gemm_ln_launch(L.ctx, w->ao_w, w->ao_b, x, w->ln0_g, w->ln0_b, w->ln0_eps, L.y0, T, k, k, s));
+    BT_TRY(mark(s));
+  } else {
+    BT_TRY(bt::gemm_launch(L.ctx, w->ao_w, nullptr, nullptr, L.proj, T, k, k, BT_EPI_NONE, 0, s));
+    BT_TRY(mark(s));
+    BT_TRY(bt_ln_bias_residual(L.proj, x, w->ao_b, w->ln0_g, w->ln0_b, w->ln0_eps, L.y0, T, k, stream));
+  }
   BT_TRY(mark(s));
   BT_TRY(bt::gemm_launch(L.y0, w->w1, w->b1, nullptr, L.h1, T, f, k, BT_EPI_BIAS_GELU, 0, s));
   BT_TRY(mark(s));
-  BT_TRY(bt::gemm_launch(L.h1, w->w2, nullptr, nullptr, L.proj, T, k, f, BT_EPI_NONE, 0, s));
-  BT_TRY(mark(s));
-  BT_TRY(bt_ln_bias_residual(L.proj, L.y0, w->b2, w->ln1_g, w->ln1_b, w->ln1_eps, x, T, k, stream));
+  if (fused_ln_mode() >= 2 && gemm_ln_fits(T, k, f)) {  // x = LN((h1 W2 + y0) + b2), one kernel
+    BT_TRY(gemm_ln_launch(L.h1, w->w2, w->b2, L.y0, w->ln1_g, w->ln1_b, w->ln1_eps, x, T, k, f, s));
+    BT_TRY(mark(s));
+  } else {
+    BT_TRY(bt::gemm_launch(L.h1, w->w2, nullptr, nullptr, L.proj, T, k, f, BT_EPI_NONE, 0, s));
+    BT_TRY(mark(s));
+    BT_TRY(bt_ln_bias_residual(L.proj, L.y0, w->b2, w->ln1_g, w->ln1_b, w->ln1_eps, x, T, k, stream));
+  }
   BT_TRY(mark(s));
   return BT_OK;
 }

@@ -70,6 +70,19 @@ def ln_device(x_bf16, residual_bf16, bias_f32, gamma_f32, beta_f32, eps: float, 
     return out
 
 
+def gemm_ln_device(a_bf16, bt_bf16, bias_f32, residual_bf16, gamma_f32, beta_f32, eps: float, out=None):
+    """Device LN((a bt^T + residual) + bias) in one fused kernel (bt_gemm_bias_residual_ln)."""
+    torch = _lib.require_device()
+    M, K = int(a_bf16.shape[0]), int(a_bf16.shape[1])
+    N = int(bt_bf16.shape[0])
+    if out is None:
+        out = torch.empty((M, N), dtype=torch.bfloat16, device=a_bf16.device)
+    _lib.call("bt_gemm_bias_residual_ln", a_bf16.data_ptr(), bt_bf16.data_ptr(), bias_f32.data_ptr(),
+              residual_bf16.data_ptr(), gamma_f32.data_ptr(), beta_f32.data_ptr(), float(eps), out.data_ptr(), M, N,
+              K, _lib.stream_ptr())
+    return out
+
+
 def add_bias_residual_layernorm(x, residual, bias, params: LayernormParams):
     """One-pass LN((x + residual) + bias) (reference fusion.py:79-98)."""
     xr, xc = rows_cols(x)

@@ -271,3 +271,25 @@ def test_mha_reference_max_moves(env, path, lens, mx):
     out = mha_device(qkv, plan, heads, 64, path=path)
     ref = _oracle_mha(qkv, plan, heads, mx)
     assert_close_bf16(out, ref, what=f"rescale path{path}")
+
+
+@pytest.mark.parametrize("M,N,K", [(2458, 768, 768), (2458, 768, 3072), (1, 768, 64), (300, 1024, 1024),
+                                   (129, 512, 256), (4915, 1024, 4096)])
+def test_gemm_bias_residual_ln(env, M, N, K):
+    """Fused projection + add-bias + residual + LayerNorm (one cluster of N/128
+    CTAs per 128-row block, row statistics over DSMEM) vs torch fp32 of
+    LN((A W^T + R) + b) on the same bf16 operands."""
+    bt, torch = env
+    from paper_2210_03052_b200.fusion import gemm_ln_device
+
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    A = (torch.randn(M, K, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
+    W = (torch.randn(N, K, device="cuda", generator=g) / math.sqrt(K)).to(torch.bfloat16)
+    R = (torch.randn(M, N, device="cuda", generator=g) * 2 + 0.5).to(torch.bfloat16)
+    b = torch.randn(N, device="cuda", generator=g) * 0.1
+    gamma = 1 + torch.randn(N, device="cuda", generator=g) * 0.1
+    beta = torch.randn(N, device="cuda", generator=g) * 0.1
+    out = gemm_ln_device(A, W, b, R, gamma, beta, 1e-12)
+    z = (A.float() @ W.float().t() + R.float()) + b
+    ref = torch.nn.functional.layer_norm(z, (N,), gamma, beta, eps=1e-12)
+    assert_close_bf16(out, ref, what=f"gemm_ln {M}x{N}x{K}")
