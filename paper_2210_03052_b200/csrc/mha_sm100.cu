@@ -118,10 +118,10 @@ __device__ __forceinline__ void store_out_row(const MhaParams& p, int grow, int 
 // ~112 KB smem -> two CTAs per SM, whose latency chains interleave.
 template <bool RESIDENT, int NST>
 struct MhaCfg {
-  static constexpr uint32_t Q_OFF = 0;
-  static constexpr uint32_t KV_OFF = MHA_TILE;                      // slot s: K at +32K*s, V at +32K*s+16K
-  static constexpr uint32_t P_OFF = KV_OFF + NST * 2 * MHA_TILE;     // 128 x 128 bf16 = 2 tiles
-  static constexpr uint32_t BAR_OFF = P_OFF + 2 * MHA_TILE;
+  static constexpr uint32_t Q_OFF = 0;                               // Q tile; output staging at the end
+  static constexpr uint32_t KV_OFF = MHA_TILE;                       // slot s: K at +32K*s, V at +32K*s+16K
+  static constexpr uint32_t XCH_OFF = KV_OFF + NST * 2 * MHA_TILE;   // [3][2][128] fp32 row partials
+  static constexpr uint32_t BAR_OFF = XCH_OFF + 3 * 2 * 128 * 4;
   static constexpr size_t SMEM = BAR_OFF + 128;
 };
 
@@ -140,8 +140,7 @@ template <bool RESIDENT, int NST>
 __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_constant__ CUtensorMap tm,
                                                                  const MhaParams p) {
   using Cfg = MhaCfg<RESIDENT, NST>;
-  const int qt = blockIdx.x, h = blockIdx.y;
-  const int b = blockIdx.z;
+  const int qt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
   const int sb = __ldg(p.seq_starts + b);
   const int len = __ldg(p.seq_starts + b + 1) - sb;
   // Packed layout: the sequence's rows start at seq_starts[b] and only its
@@ -158,15 +157,15 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sQ = smem + Cfg::Q_OFF;
   uint8_t* sKV = smem + Cfg::KV_OFF;
-  uint8_t* sP = smem + Cfg::P_OFF;
+  float* xch = reinterpret_cast<float*>(smem + Cfg::XCH_OFF);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::BAR_OFF);
   uint64_t* q_full = bars;
   uint64_t* kv_full = bars + 1;         // [NST]
   uint64_t* kv_empty = bars + 1 + NST;  // [NST]
   uint64_t* s_full = bars + 1 + 2 * NST;  // S(j) in TMEM
   uint64_t* s_read = s_full + 1;          // softmax has S(j) in registers: S columns free
-  uint64_t* p_full = s_full + 2;          // P(j) in smem, O rescaled: issue P(j) V(j)
-  uint64_t* pv_done = s_full + 3;         // P(j) V(j) accumulated into O: sP free
+  uint64_t* p_full = s_full + 2;          // P(j) in TMEM, O rescaled: issue P(j) V(j)
+  uint64_t* pv_done = s_full + 3;         // P(j) V(j) accumulated into O: P columns free
   uint32_t* holder = reinterpret_cast<uint32_t*>(s_full + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -191,9 +190,10 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *holder;
-  // TMEM columns: S [0,128), O [128,192), row-partial exchange between the
-  // two threads of a row [192,198): max (2 parities x 2 halves), then sum
-  constexpr uint32_t S_COL = 0, O_COL = 128, X_COL = 192;
+  // TMEM columns: S [0,128) fp32; P [128,192) = 128 keys as packed bf16 pairs,
+  // the A operand of P V (FA4-style: P never touches shared memory, which
+  // would otherwise carry 64 KB of extra traffic per block); O [192,256)
+  constexpr uint32_t S_COL = 0, P_COL = 128, O_COL = 192;
   ptx::griddep_launch_dependents();
   if (threadIdx.x == 0) MHA_TRACE(0);
 
@@ -221,9 +221,8 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
   } else if (warp == 9) {
     // ------------------------------------------------ MMA issuer
     constexpr uint32_t idesc_s = ptx::idesc_bf16(128, MHA_KB, false, false);  // Q K^T, both K-major
-    constexpr uint32_t idesc_o = ptx::idesc_bf16(128, MHA_D, false, true);    // P (K-major) x V (MN-major)
+    constexpr uint32_t idesc_o = ptx::idesc_bf16(128, MHA_D, false, true);    // P (TMEM, K-major) x V (MN-major)
     const uint64_t q_desc = ptx::sdesc_sw128(ptx::smem_u32(sQ), 1024, 16);
-    const uint64_t p_desc = ptx::sdesc_sw128(ptx::smem_u32(sP), 1024, 16);
     const uint32_t kv_base = ptx::smem_u32(sKV);
     ptx::mbar_wait(q_full, 0);
     if (lane == 0) MHA_TRACE(1);
@@ -235,8 +234,8 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
       const uint64_t v_desc = ptx::sdesc_sw128(kv_base + pslot * 2 * MHA_TILE + MHA_TILE, 1024, MHA_TILE);
       if (ptx::elect_one()) {
         for (int ks = 0; ks < nks; ++ks)
-          ptx::mma_bf16_ss(tmem + O_COL, p_desc + (ks >> 2) * (MHA_TILE >> 4) + (ks & 3) * 2,
-                           v_desc + ks * ((16 * 128) >> 4), idesc_o, (pj > 0 || ks > 0) ? 1u : 0u);
+          ptx::mma_bf16_ts(tmem + O_COL, tmem + P_COL + 8 * ks, v_desc + ks * ((16 * 128) >> 4), idesc_o,
+                           (pj > 0 || ks > 0) ? 1u : 0u);
         ptx::mma_commit(pv_done);
         if (!RESIDENT) ptx::mma_commit(&kv_empty[pslot]);  // K and V of block pj consumed
       }
@@ -268,17 +267,17 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
     // warp w+4 (half 1: keys 64-127) own TMEM lanes 32*(w%4)..+31.  Row max
     // is combined through shared memory once per block; row sums stay
     // per-thread partials until the end.  Warp-uniform skipping: warps whose
-    // 32 query rows lie past the sequence end, and key chunks past it.
+    // 32 query rows lie past the sequence end.
     const int quarter = warp & 3, half = warp >> 2;
     const int row = quarter * 32 + lane;
     const int pair_bar = 1 + quarter;  // named barrier of warps quarter and quarter + 4
     const bool warp_live = q0 + quarter * 32 < work;
     const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
     const uint32_t s_my = trow + S_COL + half * 64;
+    const uint32_t p_my = trow + P_COL + half * 32;
     const uint32_t o_my = trow + O_COL + half * 32;
     const float sl2 = p.sl2;
     float mref = -INFINITY, lsum = 0.f;
-    uint8_t* prow = sP + half * MHA_TILE + row * 128;  // my 64 keys = one K-major SW128 column block
     for (int j = 0; j < nkb; ++j) {
       const int kvalid = min(MHA_KB, len - j * MHA_KB) - half * 64;  // valid keys among my 64 (may be <= 0)
       ptx::mbar_wait(s_full, j & 1);
@@ -296,7 +295,7 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
       if (threadIdx.x == 0 && j < 3) MHA_TRACE(16 + 4 * j);
 #define SV(c, i) __uint_as_float((c) == 0 ? r0[i] : r1[i])
       bool need = false;
-      float mnew = mref;
+      float mnew = mref, alpha = 1.f;
       if (warp_live) {
         if (kvalid < 64) {
           // keys past the problem's end: s = -inf (out of the max; exp -> 0)
@@ -317,69 +316,62 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
             m4[3] = ptx::max3(m4[3], SV(c, i + 6), SV(c, i + 7));
           }
         }
-        // exchange the partial max with the row's other thread through TMEM
-        const float pmax = fmaxf(ptx::max3(m4[0], m4[1], m4[2]), m4[3]);
-        ptx::tmem_st1(trow + X_COL + 2 * (j & 1) + half, __float_as_uint(pmax));
-        ptx::tmem_wait_st();
-        ptx::tc_fence_before();
+        // exchange the partial max with the row's other thread
+        float* x = xch + (j & 1) * 256;
+        x[half * 128 + row] = fmaxf(ptx::max3(m4[0], m4[1], m4[2]), m4[3]);
         named_bar_sync(pair_bar, 64);
-        ptx::tc_fence_after();
-        const float bmax = fmaxf(pmax, __uint_as_float(ptx::tmem_ld1(trow + X_COL + 2 * (j & 1) + (half ^ 1))));
+        const float bmax = fmaxf(x[row], x[128 + row]);
         mnew = fmaxf(mref, bmax);
         need = (mnew - mref) * sl2 > MHA_RESCALE_LOG2;  // true on the first block (mref = -inf)
+        alpha = (need && mref != -INFINITY) ? ptx::ex2_approx((mref - mnew) * sl2) : 1.f;
+        if (need) mref = mnew;
+        if (threadIdx.x == 0 && j < 3) MHA_TRACE(17 + 4 * j);
       }
-      if (threadIdx.x == 0 && j < 3) MHA_TRACE(17 + 4 * j);
       if (j > 0) {
-        ptx::mbar_wait(pv_done, (j - 1) & 1);  // P(j-1) V(j-1) is in O; sP is free
+        ptx::mbar_wait(pv_done, (j - 1) & 1);  // P(j-1) V(j-1) is in O; the P columns are free
         ptx::tc_fence_after();
       }
       if (threadIdx.x == 0 && j < 3) MHA_TRACE(18 + 4 * j);
       if (warp_live) {
-        // the reference max moves (rare): my 32 O columns are rescaled after
-        // P is written (S registers are dead by then), before P(j) V(j)
-        const bool any_resc = __any_sync(0xffffffffu, need && j > 0);
-        const float alpha = (need && mref != -INFINITY) ? ptx::ex2_approx((mref - mnew) * sl2) : 1.f;
-        if (need) mref = mnew;
         const float msc = mref * sl2;
         const unsigned long long sl2x2 = ptx::f2(sl2, sl2), nm2 = ptx::f2(-msc, -msc);
         unsigned long long sum4[4] = {0ull, 0ull, 0ull, 0ull};  // 4 independent add chains
+        // P = 2^((s - m_ref) * scale * log2 e): BT_MHA_POLY of every 16 on the
+        // FMA pipe, the rest on the SFU; one branch-free block over 64 keys
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
-          // P for 32 keys: BT_MHA_POLY of every 16 exponentials on the FMA pipe,
-          // the rest on the SFU; K-major SW128 store (16 B chunks XOR-swizzled by row % 8)
-          const int cb = c * 4;  // first 16 B chunk of these 32 keys in the 128 B row
-          float ev[32];
+          uint32_t pp[16];  // 32 keys as bf16 pairs -> P columns half*32 + 16c .. +15
+          if (32 * c >= kvalid) {  // warp-uniform: no valid key in these 32 -> P = 0, no exponentials
+#pragma unroll
+            for (int i = 0; i < 16; ++i) pp[i] = 0u;
+            ptx::tmem_st16(p_my + 16 * c, pp);
+            continue;
+          }
 #pragma unroll
           for (int i = 0; i < 32; i += 2) {
-            float x0, x1;
+            float x0, x1, e0, e1;
             ptx::unf2(ptx::fma2(ptx::f2(SV(c, i), SV(c, i + 1)), sl2x2, nm2), x0, x1);
             if ((i & 15) < BT_MHA_POLY) {
-              ptx::ex2_poly2(x0, x1, ev[i], ev[i + 1]);
-              ev[i] = x0 >= -125.0f ? ev[i] : 0.f;  // masked key (x = -inf): exactly 0
-              ev[i + 1] = x1 >= -125.0f ? ev[i + 1] : 0.f;
+              ptx::ex2_poly2(x0, x1, e0, e1);
+              e0 = x0 >= -125.0f ? e0 : 0.f;  // masked key (x = -inf): exactly 0
+              e1 = x1 >= -125.0f ? e1 : 0.f;
             } else {
-              ev[i] = ptx::ex2_approx(x0);  // ex2(-inf) = 0
-              ev[i + 1] = ptx::ex2_approx(x1);
+              e0 = ptx::ex2_approx(x0);  // ex2(-inf) = 0
+              e1 = ptx::ex2_approx(x1);
             }
+            sum4[(i >> 1) & 3] = ptx::add2(sum4[(i >> 1) & 3], ptx::f2(e0, e1));
+            pp[i / 2] = ptx::pack_bf16x2(e0, e1);
           }
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            uint32_t pk[4];
-#pragma unroll
-            for (int e = 0; e < 8; e += 2) {
-              sum4[e / 2] = ptx::add2(sum4[e / 2], ptx::f2(ev[8 * q + e], ev[8 * q + e + 1]));
-              pk[e / 2] = ptx::pack_bf16x2(ev[8 * q + e], ev[8 * q + e + 1]);
-            }
-            *reinterpret_cast<uint4*>(prow + (((cb + q) ^ (row & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-          }
+          ptx::tmem_st16(p_my + 16 * c, pp);
         }
         const unsigned long long bsum2 = ptx::add2(ptx::add2(sum4[0], sum4[1]), ptx::add2(sum4[2], sum4[3]));
-        if (threadIdx.x == 0 && j < 3) MHA_TRACE(19 + 4 * j);
         float s0f, s1f;
         ptx::unf2(bsum2, s0f, s1f);
         lsum = lsum * alpha + (s0f + s1f);  // my keys' partial row sum
-        if (any_resc) {
-          // my 32 O columns *= 2^((m_old - m_new) * scale)
+      }
+      if (warp_live) {
+        if (__any_sync(0xffffffffu, need && j > 0)) {
+          // the reference max moved (rare): my 32 O columns *= 2^((m_old - m_new) * scale)
           const unsigned long long a2 = ptx::f2(alpha, alpha);
           uint32_t o[32];
           ptx::tmem_ld32(o_my, o);
@@ -392,10 +384,10 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
             o[i + 1] = __float_as_uint(c);
           }
           ptx::tmem_st32(o_my, o);
-          ptx::tmem_wait_st();
         }
+        ptx::tmem_wait_st();
       }
-      ptx::fence_proxy_async_smem();
+      if (threadIdx.x == 0 && j < 3) MHA_TRACE(19 + 4 * j);
       ptx::tc_fence_before();
       ptx::mbar_arrive(p_full);
       if (threadIdx.x == 0) MHA_TRACE(3 + 2 * j);
@@ -404,21 +396,19 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
     ptx::mbar_wait(pv_done, (nkb - 1) & 1);
     ptx::tc_fence_after();
     if (threadIdx.x == 0) MHA_TRACE(30);
-    // O / l -> bf16 rows staged in sP (free: the last P V has completed) ->
-    // coalesced 16-byte stores, 4 rows per warp instruction
+    // O / l -> bf16 rows staged in the Q tile (free: every MMA has completed)
+    // -> coalesced 16-byte stores, 4 rows per warp instruction
     if (warp_live) {
       uint32_t o[32];
       ptx::tmem_ld32(o_my, o);
-      ptx::tmem_wait_ld(o);
-      ptx::tmem_st1(trow + X_COL + 4 + half, __float_as_uint(lsum));
-      ptx::tmem_wait_st();
-      ptx::tc_fence_before();
+      float* x = xch + 2 * 256;  // its own region: the pair's last max exchange may still be read
+      x[half * 128 + row] = lsum;
       named_bar_sync(pair_bar, 64);
-      ptx::tc_fence_after();
-      const float l = lsum + __uint_as_float(ptx::tmem_ld1(trow + X_COL + 4 + (half ^ 1)));
+      const float l = x[row] + x[128 + row];
+      ptx::tmem_wait_ld(o);
       const float inv = (q0 + row < len) ? 1.0f / l : 0.f;
       const unsigned long long inv2 = ptx::f2(inv, inv);
-      uint8_t* mine = sP + row * 128;
+      uint8_t* mine = sQ + row * 128;
 #pragma unroll
       for (int jj = 0; jj < 4; ++jj) {
         uint32_t w[4];
@@ -440,7 +430,7 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
         const int rr = quarter * 32 + half * 16 + it * 4 + (lane >> 3);
         const int jj = lane & 7;
         if (q0 + rr < work) {
-          const uint4 v = *reinterpret_cast<const uint4*>(sP + rr * 128 + ((jj ^ (rr & 7)) << 4));
+          const uint4 v = *reinterpret_cast<const uint4*>(sQ + rr * 128 + ((jj ^ (rr & 7)) << 4));
           *reinterpret_cast<uint4*>(p.out + static_cast<size_t>(s0 + q0 + rr) * p.hidden + h * MHA_D + jj * 8) = v;
         }
       }

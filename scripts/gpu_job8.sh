@@ -1,0 +1,5 @@
+cd $GRAFT_REPO_ROOT
+timeout 300 python -m pytest tests/test_gpu_kernels.py -x -q -k mha 2>&1 | tail -2
+python scripts/mha_trace.py c2 | tail -6
+for c in c2 c3; do python bench.py --config $c --no-cpu-baseline --no-e2e 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$c step', d['ms_per_step'], 'mha', d['kernels']['mha']['us'], d['kernels']['mha']['frac'])"; done
+python bench.py --config c5 --steps 3 --warmup 3 --no-cpu-baseline --no-e2e 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('c5 step', d['ms_per_step'], 'mha', d['kernels']['mha']['us'], d['kernels']['mha']['frac'])"
