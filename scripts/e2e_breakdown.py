@@ -24,7 +24,7 @@ def main():
     eng = bt.engine_for(w, cfg)
     T, bs, mx, k = seqs.total, 16, 256, 768
     out = torch.empty((bs * mx, k), dtype=torch.float32, pin_memory=True)
-    graph, run, xp, yp, _, _ = eng._graph_entry(seqs, cfg, eng._cfg_c)
+    graph, run, xp, yp = eng._graph_entry(seqs, cfg, eng._cfg_c)[:4]
     lengths_h = np.ascontiguousarray(np.asarray(seqs.lengths, dtype=np.int32))
     lp = lengths_h.ctypes.data
     s = _lib.stream_ptr()
