@@ -11,8 +11,10 @@
 
 namespace bt {
 
+// Register-resident parameters: best while they fit with >= 2 CTAs per SM
+// (k <= 768: 126 registers); wider rows use the shared-memory variant.
 template <int NCH, bool HOIST>
-__global__ void __launch_bounds__(256) ln_bias_residual_kernel(const __nv_bfloat16* __restrict__ x,
+__global__ void __launch_bounds__(256) ln_bias_residual_regs_kernel(const __nv_bfloat16* __restrict__ x,
                                                                const __nv_bfloat16* __restrict__ res,
                                                                const float* __restrict__ bias,
                                                                const float* __restrict__ gamma,
@@ -120,16 +122,137 @@ __global__ void __launch_bounds__(256) ln_bias_residual_kernel(const __nv_bfloat
   }
 }
 
+// Parameters (bias, gamma, beta: 3 x k fp32) are staged in shared memory once
+// per CTA -- before griddepcontrol.wait, so the copy overlaps the previous
+// kernel's tail -- rather than held in registers: at k = 1024 holding them cost
+// 162 registers per thread and left one 256-thread CTA (8 warps) per SM,
+// too few loads in flight to cover HBM latency (C5: 0.40-0.54 of HBM).
+template <int NCH>
+__global__ void __launch_bounds__(256) ln_bias_residual_kernel(const __nv_bfloat16* __restrict__ x,
+                                                               const __nv_bfloat16* __restrict__ res,
+                                                               const float* __restrict__ bias,
+                                                               const float* __restrict__ gamma,
+                                                               const float* __restrict__ beta, float eps,
+                                                               __nv_bfloat16* __restrict__ out, int T, int k) {
+  extern __shared__ float4 sparams[];  // [3][k / 4]: bias (0 if none), gamma, beta
+  const int lane = threadIdx.x & 31;
+  const int wpb = blockDim.x >> 5;
+  const int nchunk = k >> 3;
+  const int k4 = k >> 2;
+  const float inv_k = 1.0f / static_cast<float>(k);
+  for (int i = threadIdx.x; i < k4; i += blockDim.x) {
+    sparams[i] = bias ? __ldg(reinterpret_cast<const float4*>(bias) + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+    sparams[k4 + i] = __ldg(reinterpret_cast<const float4*>(gamma) + i);
+    sparams[2 * k4 + i] = __ldg(reinterpret_cast<const float4*>(beta) + i);
+  }
+  __syncthreads();
+  ptx::griddep_launch_dependents();
+  ptx::griddep_wait();
+  for (int row = blockIdx.x * wpb + (threadIdx.x >> 5); row < T; row += gridDim.x * wpb) {
+    const size_t base = static_cast<size_t>(row) * k;
+    uint4 xv[NCH], rv[NCH];
+#pragma unroll
+    for (int i = 0; i < NCH; ++i) {  // issue every load of the row before using any
+      const int c = lane + 32 * i;
+      xv[i] = make_uint4(0, 0, 0, 0);
+      rv[i] = make_uint4(0, 0, 0, 0);
+      if (c < nchunk) {
+        xv[i] = __ldg(reinterpret_cast<const uint4*>(x + base) + c);
+        if (res) rv[i] = __ldg(reinterpret_cast<const uint4*>(res + base) + c);
+      }
+    }
+    float z[NCH][8];
+    float sum = 0.f;
+#pragma unroll
+    for (int i = 0; i < NCH; ++i) {
+      const int c = lane + 32 * i;
+      const __nv_bfloat162* xh = reinterpret_cast<const __nv_bfloat162*>(&xv[i]);
+      const __nv_bfloat162* rh = reinterpret_cast<const __nv_bfloat162*>(&rv[i]);
+      float4 b0 = make_float4(0.f, 0.f, 0.f, 0.f), b1 = b0;
+      if (c < nchunk) {
+        b0 = sparams[2 * c];
+        b1 = sparams[2 * c + 1];
+      }
+      const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 xf = __bfloat1622float2(xh[e]);
+        const float2 rf = __bfloat1622float2(rh[e]);
+        z[i][2 * e] = (xf.x + rf.x) + bb[2 * e];  // (x + residual) + bias, fusion.py:96
+        z[i][2 * e + 1] = (xf.y + rf.y) + bb[2 * e + 1];
+      }
+      if (c < nchunk) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) sum += z[i][e];
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    const float mean = sum * inv_k;
+    float sq = 0.f;
+#pragma unroll
+    for (int i = 0; i < NCH; ++i) {
+      if (lane + 32 * i < nchunk) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float d = z[i][e] - mean;
+          sq += d * d;
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+    const float rstd = 1.0f / sqrtf(sq * inv_k + eps);
+#pragma unroll
+    for (int i = 0; i < NCH; ++i) {
+      const int c = lane + 32 * i;
+      if (c < nchunk) {
+        const float4 g0 = sparams[k4 + 2 * c], g1 = sparams[k4 + 2 * c + 1];
+        const float4 e0 = sparams[2 * k4 + 2 * c], e1 = sparams[2 * k4 + 2 * c + 1];
+        const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+        const float ee[8] = {e0.x, e0.y, e0.z, e0.w, e1.x, e1.y, e1.z, e1.w};
+        uint4 o;
+        uint32_t* ow = reinterpret_cast<uint32_t*>(&o);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float y0 = gg[2 * e] * ((z[i][2 * e] - mean) * rstd) + ee[2 * e];
+          const float y1 = gg[2 * e + 1] * ((z[i][2 * e + 1] - mean) * rstd) + ee[2 * e + 1];
+          ow[e] = ptx::pack_bf16x2(y0, y1);
+        }
+        reinterpret_cast<uint4*>(out + base)[c] = o;
+      }
+    }
+  }
+}
+
 template <int NCH>
 static int launch_ln(const __nv_bfloat16* x, const __nv_bfloat16* r, const float* b, const float* g, const float* be,
                       float eps, __nv_bfloat16* out, int T, int k, cudaStream_t s) {
   const int threads = 256, wpb = threads / 32;
+  if constexpr (NCH <= 3) {
+    const int sms0 = num_sms() > 0 ? num_sms() : 148;
+    long long grid0 = (T + wpb - 1) / wpb;
+    if (grid0 > sms0 * 8LL) grid0 = sms0 * 8LL;
+    if (grid0 < 1) grid0 = 1;
+    BT_LAUNCH((ln_bias_residual_regs_kernel<NCH, true>), dim3(static_cast<int>(grid0)), dim3(threads), 0, s, 1, x, r,
+              b, g, be, eps, out, T, k);
+    return BT_OK;
+  }
   const int sms = num_sms() > 0 ? num_sms() : 148;
+  const size_t smem = static_cast<size_t>(3) * k * sizeof(float);
+  auto kern = ln_bias_residual_kernel<NCH>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    BT_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * 4096 * 4));
+    attr_set = true;
+  }
+  int per_sm = 0;
+  BT_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
   long long grid = (T + wpb - 1) / wpb;
-  if (grid > sms * 8LL) grid = sms * 8LL;
+  const long long cap = static_cast<long long>(sms) * (per_sm > 0 ? per_sm : 1);
+  if (grid > cap) grid = cap;  // resident grid, rows grid-strided
   if (grid < 1) grid = 1;
-  BT_LAUNCH((ln_bias_residual_kernel<NCH, (NCH <= 4)>), dim3(static_cast<int>(grid)), dim3(threads), 0, s, 1, x, r, b,
-            g, be, eps, out, T, k);
+  BT_LAUNCH(kern, dim3(static_cast<int>(grid)), dim3(threads), smem, s, 1, x, r, b, g, be, eps, out, T, k);
   return BT_OK;
 }
 
