@@ -352,9 +352,7 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
             float x0, x1, e0, e1;
             ptx::unf2(ptx::fma2(ptx::f2(SV(c, i), SV(c, i + 1)), sl2x2, nm2), x0, x1);
             if ((i & 15) < BT_MHA_POLY) {
-              ptx::ex2_poly2(x0, x1, e0, e1);
-              e0 = x0 >= -125.0f ? e0 : 0.f;  // masked key (x = -inf): exactly 0
-              e1 = x1 >= -125.0f ? e1 : 0.f;
+              ptx::ex2_poly2(x0, x1, e0, e1);  // masked key (x = -inf): exactly 0
             } else {
               e0 = ptx::ex2_approx(x0);  // ex2(-inf) = 0
               e1 = ptx::ex2_approx(x1);

@@ -373,7 +373,9 @@ __device__ __forceinline__ float max3(float a, float b, float c) {
 // 2^x on the FMA pipe for a pair (offloads the SFU, whose ex2 issues at
 // 16 / clk / SM): x = n + f with n = rint(x) (the 1.5 * 2^23 trick), 2^f by a
 // degree-3 polynomial on [-0.5, 0.5] (rel. error < 2.5e-4, below bf16's
-// 2^-9), 2^n added into the exponent field.  x is clamped to >= -125.
+// 2^-9), times 2^n built directly as a float from the biased exponent n + 127
+// (one IMAD: (bits(t) + C) << 23).  x <= -127 (e.g. a masked -inf) gives a
+// biased exponent of 0, i.e. a scale of exactly +0, so the result is 0.
 __device__ __forceinline__ unsigned long long sub2(unsigned long long a, unsigned long long b) {
   unsigned long long d;
   asm("sub.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
@@ -381,17 +383,18 @@ __device__ __forceinline__ unsigned long long sub2(unsigned long long a, unsigne
 }
 __device__ __forceinline__ void ex2_poly2(float x0, float x1, float& y0, float& y1) {
   const unsigned long long magic = f2(12582912.0f, 12582912.0f);
-  const unsigned long long x = f2(fmaxf(x0, -125.0f), fmaxf(x1, -125.0f));
+  const unsigned long long x = f2(fmaxf(x0, -127.0f), fmaxf(x1, -127.0f));
   const unsigned long long t = add2(x, magic);
   const unsigned long long fr = sub2(x, sub2(t, magic));
   unsigned long long p = fma2(f2(0.05484628f, 0.05484628f), fr, f2(0.24180230f, 0.24180230f));
   p = fma2(p, fr, f2(0.69324806f, 0.69324806f));
   p = fma2(p, fr, f2(0.99998888f, 0.99998888f));
-  float p0, p1, t0, t1;
-  unf2(p, p0, p1);
+  float t0, t1;
   unf2(t, t0, t1);
-  y0 = __int_as_float(__float_as_int(p0) + ((__float_as_int(t0) - 0x4B400000) << 23));
-  y1 = __int_as_float(__float_as_int(p1) + ((__float_as_int(t1) - 0x4B400000) << 23));
+  // bits(t) - 0x4B400000 = n;  (n + 127) << 23 = float bits of 2^n (0 for n = -127)
+  const float s0 = __int_as_float((__float_as_int(t0) - (0x4B400000 - 127)) << 23);
+  const float s1 = __int_as_float((__float_as_int(t1) - (0x4B400000 - 127)) << 23);
+  unf2(mul2(p, f2(s0, s1)), y0, y1);
 }
 
 // tanh-form GELU (reference fusion.py:23-27)
