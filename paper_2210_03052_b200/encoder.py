@@ -341,6 +341,7 @@ class BertEncoderB200:
         self._cfg_c = layer_cfg_c(self.config)
         self._ws = None
         self._graphs = {}
+        self._io_stream = None
 
     def layer(self, i: int) -> DeviceLayer:
         return self._layers[i]
@@ -431,19 +432,25 @@ class BertEncoderB200:
         graph, run, xp, yp, _, _ = self._graph_entry(seqs, cfg, cfg_c)
         lengths_h = np.ascontiguousarray(np.asarray(seqs.lengths, dtype=np.int32))
         lp = lengths_h.ctypes.data
-        s = _lib.stream_ptr()
-        _lib.call("bt_copy_rows", xp.data_ptr(), x_pinned.data_ptr(), lp, bs, mx, k * 4, 1, s)
-        if graph is not None:
-            graph.replay()
-        else:
-            run()
-        _lib.call("bt_copy_rows", out_pinned.data_ptr(), yp.data_ptr(), lp, bs, mx, k * 4, 0, s)
+        torch = self.torch
+        if self._io_stream is None:
+            self._io_stream = torch.cuda.Stream()  # not the legacy default stream: batched DMA submission
+        io = self._io_stream
+        io.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(io):
+            s = _lib.stream_ptr()
+            _lib.call("bt_copy_rows", xp.data_ptr(), x_pinned.data_ptr(), lp, bs, mx, k * 4, 1, s)
+            if graph is not None:
+                graph.replay()
+            else:
+                run()
+            _lib.call("bt_copy_rows", out_pinned.data_ptr(), yp.data_ptr(), lp, bs, mx, k * 4, 0, s)
         # padded rows of the output are exact zeros (packing.py:158-159)
         o = out_pinned.numpy().reshape(bs, mx, k)
         for b, n in enumerate(seqs.lengths):
             if n < mx:
                 o[b, n:] = 0.0
-        self.torch.cuda.current_stream().synchronize()
+        io.synchronize()
         return out_pinned
 
     def layer_device(self, li: int, x_bf16, plan: PackingPlan, stream=None):
