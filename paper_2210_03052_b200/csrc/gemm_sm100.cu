@@ -35,6 +35,7 @@
 // reference EpilogueHook (tensor.py:74-106): none / add_bias / add_bias_gelu
 // (fusion.py:30-35) / bias+residual.
 
+#include <cstdio>
 #include <cstdlib>
 #include <map>
 
@@ -728,6 +729,15 @@ __global__ void spin_kernel(long long cycles) {
   }
 }
 
+static bool autotune_verbose() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("BT_AUTOTUNE_VERBOSE");
+    on = (e && e[0] == '1') ? 1 : 0;
+  }
+  return on != 0;
+}
+
 static bool autotune_enabled() {
   static int on = -1;
   if (on < 0) {
@@ -774,6 +784,9 @@ static int autotune(const void* A, const void* Bt, const float* bias, const void
         BT_CUDA_CHECK(cudaEventElapsedTime(&t, e0, e1));
         ms = t < ms ? t : ms;
       }
+      if (autotune_verbose())
+        fprintf(stderr, "[bt autotune] M=%d N=%d K=%d epi=%d pair=%d bn=%d sk=%d: %.2f us\n", M, N, K, epi, c.pair,
+                c.bn, sk, ms * 1e3f / 5);
       if (ms < best_ms * 0.98f) {  // prefer earlier (larger-tile) candidates on near ties
         best_ms = ms;
         best = ch;
