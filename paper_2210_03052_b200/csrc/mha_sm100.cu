@@ -61,32 +61,6 @@ __device__ __forceinline__ void reg_tie(uint32_t (&r)[32]) {
                  "+r"(r[29]), "+r"(r[30]), "+r"(r[31]));
 }
 
-// Write 32 consecutive bf16 P values (packed in 16 u32) of row `row`,
-// starting at key column `c` (multiple of 32), into the K-major SW128 layout:
-// 64-key column blocks of 128 rows x 128 B, 16 B chunks XOR-swizzled by row%8.
-__device__ __forceinline__ void store_p32(uint8_t* sP, int row, int c, const uint32_t (&pk)[16]) {
-  uint8_t* blk = sP + (c >> 6) * MHA_TILE + row * 128;
-  const int chunk0 = (c & 63) >> 3;
-#pragma unroll
-  for (int t = 0; t < 4; ++t) {
-    const int phys = (chunk0 + t) ^ (row & 7);
-    *reinterpret_cast<uint4*>(blk + phys * 16) = make_uint4(pk[4 * t], pk[4 * t + 1], pk[4 * t + 2], pk[4 * t + 3]);
-  }
-}
-
-__device__ __forceinline__ void store_out_row(const MhaParams& p, int grow, int h, const float (&o)[64], float inv) {
-  uint4* dst = reinterpret_cast<uint4*>(p.out + static_cast<size_t>(grow) * p.hidden + h * MHA_D);
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    uint4 v;
-    v.x = ptx::pack_bf16x2(o[8 * q + 0] * inv, o[8 * q + 1] * inv);
-    v.y = ptx::pack_bf16x2(o[8 * q + 2] * inv, o[8 * q + 3] * inv);
-    v.z = ptx::pack_bf16x2(o[8 * q + 4] * inv, o[8 * q + 5] * inv);
-    v.w = ptx::pack_bf16x2(o[8 * q + 6] * inv, o[8 * q + 7] * inv);
-    dst[q] = v;
-  }
-}
-
 // ============================================================ kernel
 // One template serves both reference paths:
 //   RESIDENT = true   short path (attention.py:177-237): every K/V block of the

@@ -324,22 +324,6 @@ __device__ __forceinline__ float ex2_approx(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-// 2^x on the FMA / ALU pipes (no MUFU): round-to-nearest split x = n + f,
-// f in [-0.5, 0.5], cubic minimax for 2^f (max rel err 2.1e-4, well below the
-// bf16 rounding of P), exponent added as an integer.  Used for part of the
-// softmax exponentials so the MUFU unit is not the bottleneck (d = 64 attention
-// is exp-bound on Blackwell).  Valid for x <= 0 (softmax arguments).
-__device__ __forceinline__ float ex2_poly(float x) {
-  x = fmaxf(x, -126.0f);
-  const float t = x + 12582912.0f;  // 1.5 * 2^23: integer part lands in the low mantissa bits
-  const int n = __float_as_int(t) - 0x4B400000;
-  const float f = x - (t - 12582912.0f);
-  float p = fmaf(0.05484628f, f, 0.24180230f);
-  p = fmaf(p, f, 0.69324806f);
-  p = fmaf(p, f, 0.99998888f);
-  return __int_as_float(__float_as_int(p) + (n << 23));
-}
-
 // ----------------------------------------- paired fp32 ops (FFMA2 / FADD2)
 __device__ __forceinline__ unsigned long long f2(float lo, float hi) {
   unsigned long long r;
