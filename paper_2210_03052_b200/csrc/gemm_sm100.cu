@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(GemmCfg<PAIR, BN, EW>::THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
-      ptx::mbar_init(&tempty[a], PAIR * EW * 32);  // (leader's) every epilogue thread of the pair
+      ptx::mbar_init(&tempty[a], PAIR);  // (leader's) one arrival per CTA of the pair, after its epilogue warps
     }
     ptx::fence_mbar_init();
   }
@@ -526,11 +526,17 @@ __global__ void __launch_bounds__(GemmCfg<PAIR, BN, EW>::THREADS, 1)
             for (int q = 1; q <= ncontrib; ++q) p.flags[(unit + q) * 2 + rank] = 0;  // ready for the next launch
         }
       }
+      // this CTA's epilogue warps are done reading the accumulator: ONE thread
+      // releases it (a cluster-scope arrive costs a GPU-scope membar; 256
+      // threads each paying it showed up in the stall profile)
       ptx::tc_fence_before();
-      if constexpr (PAIR == 2)
-        ptx::mbar_arrive_cluster(tempty_leader + acc * 8);
-      else
-        ptx::mbar_arrive(&tempty[acc]);
+      named_bar_sync(2, EW * 32);
+      if (ew == 0 && lane == 0) {
+        if constexpr (PAIR == 2)
+          ptx::mbar_arrive_cluster(tempty_leader + acc * 8);
+        else
+          ptx::mbar_arrive(&tempty[acc]);
+      }
       if (threadIdx.x == 64) BT_TRACE(5 + 6 * it, gtimer());
       ++it;
     }
