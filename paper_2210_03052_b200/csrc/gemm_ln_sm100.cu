@@ -278,14 +278,46 @@ static int launch_gln(const CUtensorMap& ta, const CUtensorMap& tb, const CUtens
   return BT_OK;
 }
 
+// How many CL-CTA clusters of this kernel the device runs at once (clusters
+// must fit inside a GPC: on B200, 22 clusters of 6 but only 15 of 8).
+template <int CL>
+static int max_active_clusters() {
+  static int n = -1;
+  if (n < 0) {
+    auto kern = gemm_ln_kernel<CL>;
+    n = 0;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(GlnCfg::SMEM)) ==
+        cudaSuccess) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(CL * 16);
+      cfg.blockDim = dim3(GLN_THREADS);
+      cfg.dynamicSmemBytes = GlnCfg::SMEM;
+      cudaLaunchAttribute a[1];
+      a[0].id = cudaLaunchAttributeClusterDimension;
+      a[0].val.clusterDim.x = CL;
+      a[0].val.clusterDim.y = 1;
+      a[0].val.clusterDim.z = 1;
+      cfg.attrs = a;
+      cfg.numAttrs = 1;
+      if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) n = 0;
+    }
+    (void)cudaGetLastError();
+  }
+  return n;
+}
+
 // Whether the fused kernel applies (N = 128 * CL, CL in {4, 6, 8}) and its
 // row blocks fit one wave of clusters.
 bool gemm_ln_fits(int M, int N, int K) {
   if (N % GLN_BN || K % GLN_BK || K < GLN_BK) return false;
   const int cl = N / GLN_BN;
-  if (cl != 4 && cl != 6 && cl != 8) return false;
-  const int sms = num_sms() > 0 ? num_sms() : 148;
-  return static_cast<long long>((M + 127) / 128) * cl <= sms;
+  const int rbs = (M + 127) / 128;
+  switch (cl) {
+    case 4: return rbs <= max_active_clusters<4>();
+    case 6: return rbs <= max_active_clusters<6>();
+    case 8: return rbs <= max_active_clusters<8>();
+    default: return false;
+  }
 }
 
 int gemm_ln_launch(const void* A, const void* Bt, const float* bias, const void* residual, const float* gamma,
