@@ -24,8 +24,8 @@
 //
 // The proj tensor never reaches memory and the separate LayerNorm launch
 // (and its re-read of proj and residual) disappears.  Used when the row
-// blocks fit in one wave (CL * ceil(M/128) <= #SMs); otherwise the encoder
-// keeps GEMM + ln_bias_residual_kernel.
+// blocks fit one wave of clusters (cudaOccupancyMaxActiveClusters); otherwise
+// the encoder keeps GEMM + ln_bias_residual_kernel.
 
 #include "common.cuh"
 #include "ptx.cuh"
