@@ -189,6 +189,9 @@ def time_kernels(torch, bt, eng, shard_seqs, x_dev, reps: int = 30):
     upad = torch.empty((bs * mx, k), dtype=torch.float32, device="cuda")
     lf = harness.layer_flops(shard_seqs.lengths, k, cfg.ffn_scale)
 
+    fused_ln0 = bool(_lib.load().bt_fused_attn_out_ln(T, k))  # what the forward runs for this shape
+    from paper_2210_03052_b200.fusion import gemm_ln_device
+
     ops = {
         "plan": (lambda: _lib.call("bt_plan_lengths", lengths_dev.data_ptr(), bs, mx, starts.data_ptr(),
                                    offs.data_ptr(), _lib.stream_ptr()), 1, "hbm",
@@ -201,6 +204,9 @@ def time_kernels(torch, bt, eng, shard_seqs, x_dev, reps: int = 30):
         "gemm_attn_out": (lambda: gemm_device(ctx, L0.ao_w, out=proj), cfg.layers, "tensor", lf["gemm1"], 1),
         "ln0": (lambda: ln_device(proj, x, L0.ao_b, L0.ln0_g, L0.ln0_b, 1e-12, out=y0), cfg.layers, "hbm",
                 harness.kernel_bytes("ln", T, k), 1),
+        # the forward's kernel when it fuses attn-out GEMM + bias + residual + LN0 (replaces the two above)
+        "gemm_attn_out_ln": (lambda: gemm_ln_device(ctx, L0.ao_w, L0.ao_b, x, L0.ln0_g, L0.ln0_b, 1e-12, out=y0),
+                             cfg.layers, "tensor", lf["gemm1"], 1),
         "gemm_ffn1_gelu": (lambda: gemm_device(y0, L0.w1, L0.b1, None, _lib.EPI_BIAS_GELU, out=h1), cfg.layers,
                            "tensor", lf["gemm2"], 1),
         "gemm_ffn2": (lambda: gemm_device(h1, L0.w2, out=h2), cfg.layers, "tensor", lf["gemm3"], 1),
@@ -210,6 +216,8 @@ def time_kernels(torch, bt, eng, shard_seqs, x_dev, reps: int = 30):
                                      mx, k, upad.data_ptr(), _lib.BT_F32, _lib.stream_ptr()), 1, "hbm",
                    harness.kernel_bytes("unpack", T, k, bs, mx), 1),
     }
+    for name in (("gemm_attn_out", "ln0") if fused_ln0 else ("gemm_attn_out_ln",)):
+        ops.pop(name)
     res = {}
     s = torch.cuda.current_stream()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")

@@ -126,6 +126,10 @@ BT_API int bt_mha_padded(const void* qkv, const int32_t* seq_starts, int bs, int
 BT_API int bt_ln_bias_residual(const void* x, const void* residual, const float* bias, const float* gamma,
                         const float* beta, float eps, void* out, int T, int k, bt_stream_t stream);
 
+/* 1 if bt_encoder_layer / bt_encoder_forward use bt_gemm_bias_residual_ln after the attention-output
+ * projection for T tokens of hidden size k (else GEMM + bt_ln_bias_residual). */
+BT_API int bt_fused_attn_out_ln(int T, int k);
+
 /* Fused attention-output / FFN2 projection + add-bias + residual + LayerNorm (encoder.py:385-388 and
  * :404-407, i.e. gemm then fusion.py:79 add_bias_residual_layernorm):
  *   out[M,N] = LN((A[M,K] Bt[N,K]^T + residual) + bias) * gamma + beta,  bf16 in / out, fp32 math.

@@ -145,6 +145,12 @@ static int encoder_layer_impl(const bt_layer_weights* w, const bt_layer_cfg* cfg
 }
 }  // namespace bt
 
+// 1 when the forward fuses the attention-output GEMM with add-bias + residual
+// + LayerNorm for this token count and hidden size (bench / tooling query).
+extern "C" int bt_fused_attn_out_ln(int T, int k) {
+  return (bt::fused_ln_mode() >= 1 && bt::gemm_ln_fits(T, k, k)) ? 1 : 0;
+}
+
 extern "C" int bt_encoder_layer(const bt_layer_weights* w, const bt_layer_cfg* cfg, const int32_t* seq_starts, int bs,
                                 int T, void* x_inout, void* ws, size_t ws_bytes, bt_stream_t stream) {
   return bt::encoder_layer_impl(w, cfg, seq_starts, bs, T, x_inout, ws, ws_bytes, stream);

@@ -13,14 +13,17 @@
 //   warp 0      TMA producer: A / B k-blocks -> 4-stage 128B-swizzled ring;
 //               the residual tile (128 x 128 bf16) once, on its own barrier
 //   warp 1      TMEM allocator + single-thread MMA issuer (elect.sync)
-//   warps 2-5   epilogue, thread = row: v = (acc + residual) + bias kept in
-//               128 registers; the CTA's per-row (mean, M2) go to every CTA
-//               of the cluster through DSMEM (st.shared::cluster), one
-//               cluster barrier, then each CTA combines the CL partials with
-//               the parallel-variance formula (mean = avg of means, M2 = sum
-//               M2_i + n sum (mean_i - mean)^2 -- exact, no one-pass
-//               E[x^2] - E[x]^2), normalises its 128 columns and writes bf16
-//               through shared memory with TMA stores.
+//   warps 2-9   epilogue, two threads per row (warp w: TMEM lanes 32*(w%4),
+//               columns 64*((w-2)/4) .. +63): v = (acc + residual) + bias in
+//               64 registers; each thread's (mean, M2) over its 64 columns
+//               goes to every CTA of the cluster through DSMEM
+//               (st.shared::cluster), one cluster barrier, then the 2*CL
+//               partials of a row are combined with the parallel-variance
+//               formula (mean = avg of means, M2 = sum M2_i + n sum (mean_i -
+//               mean)^2 -- exact, no one-pass E[x^2] - E[x]^2), normalised and
+//               written as bf16 through shared memory with TMA stores.
+//               bias / gamma / beta are staged in shared memory while the
+//               mainloop runs.
 //
 // The proj tensor never reaches memory and the separate LayerNorm launch
 // (and its re-read of proj and residual) disappears.  Used when the row
@@ -36,15 +39,16 @@ namespace bt {
 constexpr int GLN_BN = 128;
 constexpr int GLN_BK = 64;
 constexpr int GLN_STAGES = 4;
-constexpr int GLN_THREADS = 192;
+constexpr int GLN_THREADS = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue
 constexpr uint32_t GLN_TILE = 128 * GLN_BK * 2;  // 16 KB: one 128 x 64 bf16 operand tile
 
 struct GlnCfg {
   static constexpr uint32_t A_OFF = 0;
   static constexpr uint32_t B_OFF = A_OFF + GLN_STAGES * GLN_TILE;
   static constexpr uint32_t R_OFF = B_OFF + GLN_STAGES * GLN_TILE;  // residual in, Y out: 2 boxes of 128 x 64
-  static constexpr uint32_t ST_OFF = R_OFF + 2 * GLN_TILE;           // [8][128] float2 (mean, M2)
-  static constexpr uint32_t BAR_OFF = ST_OFF + 8 * 128 * 8;
+  static constexpr uint32_t ST_OFF = R_OFF + 2 * GLN_TILE;           // [16][128] float2 (mean, M2) partials
+  static constexpr uint32_t PRM_OFF = ST_OFF + 16 * 128 * 8;         // bias, gamma, beta: 3 x 128 fp32
+  static constexpr uint32_t BAR_OFF = PRM_OFF + 3 * 128 * 4;
   static constexpr size_t SMEM = 1024 + BAR_OFF + 256;
 };
 
@@ -58,6 +62,19 @@ struct GlnParams {
 
 __device__ __forceinline__ void st_cluster_f2(uint32_t addr, float a, float b) {
   asm volatile("st.shared::cluster.v2.f32 [%0], {%1, %2};" ::"r"(addr), "f"(a), "f"(b) : "memory");
+}
+
+__device__ __forceinline__ void named_bar_sync_gln(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+// tie a register array to a preceding tcgen05.wait::ld
+__device__ __forceinline__ void gln_reg_tie(uint32_t (&r)[32]) {
+  asm volatile(""
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                 "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]),
+                 "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]),
+                 "+r"(r[29]), "+r"(r[30]), "+r"(r[31]));
 }
 
 // byte offset of 16 B chunk j (0..15 over 128 columns) of row r in the two
@@ -168,71 +185,86 @@ __global__ void __launch_bounds__(GLN_THREADS, 1)
 
   // ---------------- epilogue part 1: v = (acc + residual) + bias, local row stats
   const int quarter = warp & 3;
+  const int half = (warp - 2) >> 2;  // epilogue warps: column half 0 / 1
   const int row = quarter * 32 + lane;
-  float v[128];
+  float* prm = reinterpret_cast<float*>(smem + GlnCfg::PRM_OFF);  // [0,128) bias, [128,256) gamma, [256,384) beta
+  float v[64];
   if (warp >= 2) {
+    {  // stage this CTA's 128 columns of the parameters (overlaps the mainloop)
+      const int t = threadIdx.x - 64;  // 0..255
+      if (t < 128) {
+        prm[t] = __ldg(p.bias + n0 + t);
+      } else {
+        prm[128 + (t - 128)] = __ldg(p.gamma + n0 + (t - 128));
+        prm[256 + (t - 128)] = __ldg(p.beta + n0 + (t - 128));
+      }
+      named_bar_sync_gln(1, 256);
+    }
     ptx::mbar_wait(rfull, 0);
     ptx::mbar_wait(tfull, 0);
     ptx::tc_fence_after();
-    const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
+    const uint32_t tcol = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + half * 64;
+    uint32_t r0[32], r1[32];
+    ptx::tmem_ld32(tcol, r0);
+    ptx::tmem_ld32(tcol + 32, r1);
+    ptx::tmem_wait_ld(r0);
+    gln_reg_tie(r1);
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      uint32_t r[32];
-      ptx::tmem_ld32(trow + 32 * c, r);
-      ptx::tmem_wait_ld(r);
+    for (int q = 0; q < 8; ++q) {  // 8 columns per 16 B residual chunk
+      const int c0 = half * 64 + 8 * q;  // column within the CTA's 128
+      const uint4 rv = *reinterpret_cast<const uint4*>(sR + r_off(row, c0 >> 3));
+      const __nv_bfloat162* rh = reinterpret_cast<const __nv_bfloat162*>(&rv);
+      const float4 b0 = *reinterpret_cast<const float4*>(prm + c0);
+      const float4 b1 = *reinterpret_cast<const float4*>(prm + c0 + 4);
+      const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint4 rv = *reinterpret_cast<const uint4*>(sR + r_off(row, 4 * c + q));
-        const __nv_bfloat162* rh = reinterpret_cast<const __nv_bfloat162*>(&rv);
-        const float4 b0 = __ldg(reinterpret_cast<const float4*>(p.bias + n0 + 32 * c + 8 * q));
-        const float4 b1 = __ldg(reinterpret_cast<const float4*>(p.bias + n0 + 32 * c + 8 * q) + 1);
-        const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float2 rf = __bfloat1622float2(rh[e]);
-          const int i = 32 * c + 8 * q + 2 * e;
-          v[i] = (__uint_as_float(r[8 * q + 2 * e]) + rf.x) + bb[2 * e];  // (x + residual) + bias, fusion.py:96
-          v[i + 1] = (__uint_as_float(r[8 * q + 2 * e + 1]) + rf.y) + bb[2 * e + 1];
-        }
+      for (int e = 0; e < 4; ++e) {
+        const float2 rf = __bfloat1622float2(rh[e]);
+        const int i = 8 * q + 2 * e;
+        const uint32_t a0 = i < 32 ? r0[i] : r1[i - 32];
+        const uint32_t a1 = i + 1 < 32 ? r0[i + 1] : r1[i + 1 - 32];
+        v[i] = (__uint_as_float(a0) + rf.x) + bb[2 * e];  // (x + residual) + bias, fusion.py:96
+        v[i + 1] = (__uint_as_float(a1) + rf.y) + bb[2 * e + 1];
       }
     }
     float s4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-    for (int i = 0; i < 128; ++i) s4[i & 3] += v[i];
-    const float mean_l = ((s4[0] + s4[1]) + (s4[2] + s4[3])) * (1.0f / GLN_BN);
+    for (int i = 0; i < 64; ++i) s4[i & 3] += v[i];
+    const float mean_l = ((s4[0] + s4[1]) + (s4[2] + s4[3])) * (1.0f / 64);
     float q4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-    for (int i = 0; i < 128; ++i) {
+    for (int i = 0; i < 64; ++i) {
       const float d = v[i] - mean_l;
       q4[i & 3] = fmaf(d, d, q4[i & 3]);
     }
     const float m2_l = (q4[0] + q4[1]) + (q4[2] + q4[3]);
-    const uint32_t mine = ptx::smem_u32(&stats[rank * 128 + row]);
+    const uint32_t mine = ptx::smem_u32(&stats[(2 * rank + half) * 128 + row]);
 #pragma unroll
     for (int r = 0; r < CL; ++r) st_cluster_f2(ptx::mapa_shared(mine, r), mean_l, m2_l);
   }
   ptx::cluster_sync();  // every CTA's row partials have landed in every CTA
 
   if (warp >= 2) {
-    // ---------------- epilogue part 2: combine, normalise, store
+    // ---------------- epilogue part 2: combine the 2*CL partials (n = 64 each), normalise, store
     float mean = 0.f;
 #pragma unroll
-    for (int r = 0; r < CL; ++r) mean += stats[r * 128 + row].x;
-    mean *= 1.0f / CL;
+    for (int r = 0; r < 2 * CL; ++r) mean += stats[r * 128 + row].x;
+    mean *= 1.0f / (2 * CL);
     float m2 = 0.f;
 #pragma unroll
-    for (int r = 0; r < CL; ++r) {
+    for (int r = 0; r < 2 * CL; ++r) {
       const float2 st = stats[r * 128 + row];
       const float d = st.x - mean;
-      m2 += st.y + static_cast<float>(GLN_BN) * d * d;
+      m2 += st.y + 64.0f * d * d;
     }
     const float rstd = 1.0f / sqrtf(m2 * (1.0f / (GLN_BN * CL)) + p.eps);
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const float4 g0 = __ldg(reinterpret_cast<const float4*>(p.gamma + n0 + 8 * j));
-      const float4 g1 = __ldg(reinterpret_cast<const float4*>(p.gamma + n0 + 8 * j) + 1);
-      const float4 e0 = __ldg(reinterpret_cast<const float4*>(p.beta + n0 + 8 * j));
-      const float4 e1 = __ldg(reinterpret_cast<const float4*>(p.beta + n0 + 8 * j) + 1);
+    for (int j = 0; j < 8; ++j) {
+      const int c0 = half * 64 + 8 * j;
+      const float4 g0 = *reinterpret_cast<const float4*>(prm + 128 + c0);
+      const float4 g1 = *reinterpret_cast<const float4*>(prm + 128 + c0 + 4);
+      const float4 e0 = *reinterpret_cast<const float4*>(prm + 256 + c0);
+      const float4 e1 = *reinterpret_cast<const float4*>(prm + 256 + c0 + 4);
       const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
       const float ee[8] = {e0.x, e0.y, e0.z, e0.w, e1.x, e1.y, e1.z, e1.w};
       uint32_t w[4];
@@ -242,14 +274,13 @@ __global__ void __launch_bounds__(GLN_THREADS, 1)
         w[e] = ptx::pack_bf16x2(gg[2 * e] * ((v[i] - mean) * rstd) + ee[2 * e],
                                 gg[2 * e + 1] * ((v[i + 1] - mean) * rstd) + ee[2 * e + 1]);
       }
-      *reinterpret_cast<uint4*>(sR + r_off(row, j)) = make_uint4(w[0], w[1], w[2], w[3]);
+      *reinterpret_cast<uint4*>(sR + r_off(row, c0 >> 3)) = make_uint4(w[0], w[1], w[2], w[3]);
     }
     ptx::fence_proxy_async_smem();
     __syncwarp();
     if (lane == 0 && row_base + quarter * 32 < p.M) {
-      // this warp's 32-row slab of both 64-column boxes
-      ptx::tma_store_2d(&tmY, sR + quarter * 32 * 128, n0, row_base + quarter * 32);
-      ptx::tma_store_2d(&tmY, sR + GLN_TILE + quarter * 32 * 128, n0 + 64, row_base + quarter * 32);
+      // this warp's 32-row slab of its 64-column box
+      ptx::tma_store_2d(&tmY, sR + half * GLN_TILE + quarter * 32 * 128, n0 + 64 * half, row_base + quarter * 32);
       ptx::bulk_commit_group();
       ptx::bulk_wait_group<0>();
     }
