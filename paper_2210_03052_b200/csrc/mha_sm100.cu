@@ -134,13 +134,14 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
   float* xch = reinterpret_cast<float*>(smem + Cfg::XCH_OFF);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::BAR_OFF);
   uint64_t* q_full = bars;
-  uint64_t* kv_full = bars + 1;         // [NST]
+  uint64_t* kv_full = bars + 1;         // [NST] K block landed
   uint64_t* kv_empty = bars + 1 + NST;  // [NST]
   uint64_t* s_full = bars + 1 + 2 * NST;  // S(j) in TMEM
   uint64_t* s_read = s_full + 1;          // softmax has S(j) in registers: S columns free
   uint64_t* p_full = s_full + 2;          // P(j) in TMEM, O rescaled: issue P(j) V(j)
   uint64_t* pv_done = s_full + 3;         // P(j) V(j) accumulated into O: P columns free
-  uint32_t* holder = reinterpret_cast<uint32_t*>(s_full + 4);
+  uint64_t* v_full = s_full + 4;          // [NST] V block landed (S(j) needs only K(j))
+  uint32_t* holder = reinterpret_cast<uint32_t*>(v_full + NST);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -149,6 +150,7 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
     for (int i = 0; i < NST; ++i) {
       ptx::mbar_init(&kv_full[i], 1);
       ptx::mbar_init(&kv_empty[i], 1);
+      ptx::mbar_init(&v_full[i], 1);
     }
     ptx::mbar_init(s_full, 1);
     ptx::mbar_init(s_read, 256);
@@ -181,16 +183,33 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
       ptx::tma_load_2d(sQ, &tm, q_full, h * MHA_D, s0 + q0);
     }
     __syncwarp();
-    for (int j = 0; j < nkb; ++j) {
-      const int slot = RESIDENT ? j : j % NST;
-      if (!RESIDENT) ptx::mbar_wait(&kv_empty[slot], ((j / NST) & 1) ^ 1u);
+    // K blocks on their own barriers ahead of V: S(j) = Q K(j)^T can start
+    // before V(j) (needed only by P(j) V(j)) has landed
+    auto load_k = [&](int j, int slot) {
       if (ptx::elect_one()) {
-        uint8_t* kv = sKV + slot * 2 * MHA_TILE;
-        ptx::mbar_arrive_expect_tx(&kv_full[slot], 2 * MHA_TILE);
-        ptx::tma_load_2d(kv, &tm, &kv_full[slot], p.hidden + h * MHA_D, s0 + j * MHA_KB);
-        ptx::tma_load_2d(kv + MHA_TILE, &tm, &kv_full[slot], 2 * p.hidden + h * MHA_D, s0 + j * MHA_KB);
+        ptx::mbar_arrive_expect_tx(&kv_full[slot], MHA_TILE);
+        ptx::tma_load_2d(sKV + slot * 2 * MHA_TILE, &tm, &kv_full[slot], p.hidden + h * MHA_D, s0 + j * MHA_KB);
       }
       __syncwarp();
+    };
+    auto load_v = [&](int j, int slot) {
+      if (ptx::elect_one()) {
+        ptx::mbar_arrive_expect_tx(&v_full[slot], MHA_TILE);
+        ptx::tma_load_2d(sKV + slot * 2 * MHA_TILE + MHA_TILE, &tm, &v_full[slot], 2 * p.hidden + h * MHA_D,
+                         s0 + j * MHA_KB);
+      }
+      __syncwarp();
+    };
+    if (RESIDENT) {
+      for (int j = 0; j < nkb; ++j) load_k(j, j);
+      for (int j = 0; j < nkb; ++j) load_v(j, j);
+    } else {
+      for (int j = 0; j < nkb; ++j) {
+        const int slot = j % NST;
+        ptx::mbar_wait(&kv_empty[slot], ((j / NST) & 1) ^ 1u);
+        load_k(j, slot);
+        load_v(j, slot);
+      }
     }
   } else if (warp == 9) {
     // ------------------------------------------------ MMA issuer
@@ -202,6 +221,7 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
     if (lane == 0) MHA_TRACE(1);
     auto issue_pv = [&](int pj, int pslot) {
       // O (+)= P(pj) V(pj); only the k-steps that hold keys of the problem
+      ptx::mbar_wait(&v_full[pslot], RESIDENT ? 0u : static_cast<uint32_t>((pj / NST) & 1));
       ptx::mbar_wait(p_full, pj & 1);
       ptx::tc_fence_after();
       const int nks = min(MHA_KB, work - pj * MHA_KB + 15) / 16;
