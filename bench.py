@@ -190,6 +190,8 @@ def time_kernels(torch, bt, eng, shard_seqs, x_dev, reps: int = 30):
     lf = harness.layer_flops(shard_seqs.lengths, k, cfg.ffn_scale)
 
     fused_ln0 = bool(_lib.load().bt_fused_attn_out_ln(T, k))  # what the forward runs for this shape
+    sched = torch.empty(2 * bs, dtype=torch.int32, device="cuda")
+    _lib.call("bt_plan_sched", plan.seq_starts_dev.data_ptr(), bs, mx, sched.data_ptr(), _lib.stream_ptr())
     from paper_2210_03052_b200.fusion import gemm_ln_device
 
     ops = {
@@ -200,7 +202,10 @@ def time_kernels(torch, bt, eng, shard_seqs, x_dev, reps: int = 30):
                  harness.kernel_bytes("pack", T, k), 1),
         "gemm_qkv": (lambda: gemm_device(x, L0.qkv_w, L0.qkv_b, None, _lib.EPI_BIAS, out=qkv), cfg.layers, "tensor",
                      lf["gemm0"], 1),
-        "mha": (lambda: mha_device(qkv, plan, H, 64, cutoff=cfg.cutoff, out=ctx), cfg.layers, "tensor", lf["mha"], 1),
+        # the forward's MHA launch: CTAs in the longest-first schedule of bt_plan_sched
+        "mha": (lambda: _lib.call("bt_mha_varlen_sched", qkv.data_ptr(), plan.seq_starts_dev.data_ptr(),
+                                  sched.data_ptr(), bs, mx, H, 64, cfg.cutoff, ctx.data_ptr(), T,
+                                  _lib.stream_ptr()), cfg.layers, "tensor", lf["mha"], 1),
         "gemm_attn_out": (lambda: gemm_device(ctx, L0.ao_w, out=proj), cfg.layers, "tensor", lf["gemm1"], 1),
         "ln0": (lambda: ln_device(proj, x, L0.ao_b, L0.ln0_g, L0.ln0_b, 1e-12, out=y0), cfg.layers, "hbm",
                 harness.kernel_bytes("ln", T, k), 1),

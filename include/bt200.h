@@ -126,6 +126,13 @@ BT_API int bt_mha_padded(const void* qkv, const int32_t* seq_starts, int bs, int
 BT_API int bt_ln_bias_residual(const void* x, const void* residual, const float* bias, const float* gamma,
                         const float* beta, float eps, void* out, int T, int k, bt_stream_t stream);
 
+/* MHA work schedule for a plan: sched[bs] int2 (start row, length) of the sequences ordered by
+ * descending 128-key block count, so the fused MHA dispatches the longest problems first. */
+BT_API int bt_plan_sched(const int32_t* seq_starts, int bs, int mx, void* sched, bt_stream_t stream);
+/* bt_mha_varlen with the CTA order of a bt_plan_sched schedule (what bt_encoder_forward runs). */
+BT_API int bt_mha_varlen_sched(const void* qkv, const int32_t* seq_starts, const void* sched, int bs, int mx, int H,
+                               int d, int cutoff, void* out, int T, bt_stream_t stream);
+
 /* 1 if bt_encoder_layer / bt_encoder_forward use bt_gemm_bias_residual_ln after the attention-output
  * projection for T tokens of hidden size k (else GEMM + bt_ln_bias_residual). */
 BT_API int bt_fused_attn_out_ln(int T, int k);

@@ -21,7 +21,7 @@ namespace bt {
 int gemm_launch(const void* A, const void* Bt, const float* bias, const void* residual, void* C, int M, int N, int K,
                 int epi, int force_bn, cudaStream_t s);
 int mha_launch(const void* qkv, const int32_t* seq_starts, int bs, int mx, int H, int d, int cutoff, int T, void* out,
-               int force_path, cudaStream_t s, int padded);
+               int force_path, cudaStream_t s, int padded, const void* sched);
 bool gemm_ln_fits(int M, int N, int K);
 int gemm_ln_launch(const void* A, const void* Bt, const float* bias, const void* residual, const float* gamma,
                    const float* beta, float eps, void* Y, int M, int N, int K, cudaStream_t s);
@@ -83,6 +83,7 @@ extern "C" int bt_ln_bias_residual(const void* x, const void* residual, const fl
 extern "C" int bt_pack(const void*, int, const int32_t*, int, int, void*, int, bt_stream_t);
 extern "C" int bt_unpack(const void*, int, const int32_t*, int, int, int, void*, int, bt_stream_t);
 extern "C" int bt_plan_lengths(const int32_t*, int, int, int32_t*, int32_t*, bt_stream_t);
+extern "C" int bt_plan_sched(const int32_t*, int, int, void*, bt_stream_t);
 extern "C" int bt_bias_act(const void*, int, int, const float*, void*, int, int, int, int, int, bt_stream_t);
 
 extern "C" size_t bt_layer_workspace_bytes(const bt_layer_cfg* cfg, int T) {
@@ -103,8 +104,10 @@ static int mark(cudaStream_t s) {
   return BT_OK;
 }
 // One post-LN layer.
+// `sched` (optional): the MHA work schedule of the batch (bt_plan_sched).
 static int encoder_layer_impl(const bt_layer_weights* w, const bt_layer_cfg* cfg, const int32_t* seq_starts, int bs,
-                              int T, void* x_inout, void* ws, size_t ws_bytes, bt_stream_t stream) {
+                              int T, void* x_inout, void* ws, size_t ws_bytes, bt_stream_t stream,
+                              const void* sched = nullptr) {
   BT_TRY(bt::check_cfg(cfg));
   BT_REQUIRE(w != nullptr, BT_ESHAPE, "null layer weights");
   BT_REQUIRE(T >= 1 && bs >= 1, BT_ESHAPE, "encoder_layer: T=%d bs=%d", T, bs);
@@ -119,7 +122,7 @@ static int encoder_layer_impl(const bt_layer_weights* w, const bt_layer_cfg* cfg
   BT_TRY(bt::gemm_launch(x, w->qkv_w, w->qkv_b, nullptr, L.qkv, T, 3 * k, k, BT_EPI_BIAS, 0, s));
   BT_TRY(mark(s));
   BT_TRY(bt::mha_launch(L.qkv, seq_starts, bs, cfg->max_seq_len, cfg->head_num, cfg->head_size, cfg->cutoff, T, L.ctx,
-                        0, s, 0));
+                        0, s, 0, sched));
   BT_TRY(mark(s));
   if (fused_ln_mode() >= 1 && gemm_ln_fits(T, k, k)) {  // y0 = LN((ctx Wo + x) + bo), one kernel
     BT_TRY(gemm_ln_launch(L.ctx, w->ao_w, w->ao_b, x, w->ln0_g, w->ln0_b, w->ln0_eps, L.y0, T, k, k, s));
@@ -160,8 +163,8 @@ extern "C" size_t bt_forward_workspace_bytes(const bt_layer_cfg* cfg, int bs, in
   if (!cfg) return 0;
   const int k = cfg->head_num * cfg->head_size;
   const size_t t = static_cast<size_t>(T < 1 ? 1 : T);
-  return bt::align_up((bs + 1) * sizeof(int32_t)) + bt::align_up(t * sizeof(int32_t)) + bt::align_up(t * k * 2) +
-         bt_layer_workspace_bytes(cfg, T);
+  return bt::align_up((bs + 1) * sizeof(int32_t)) + bt::align_up(bs * 8) + bt::align_up(t * sizeof(int32_t)) +
+         bt::align_up(t * k * 2) + bt_layer_workspace_bytes(cfg, T);
 }
 
 extern "C" int bt_encoder_forward(const bt_layer_weights* layers, int n_layers, const bt_layer_cfg* cfg,
@@ -177,6 +180,8 @@ extern "C" int bt_encoder_forward(const bt_layer_weights* layers, int n_layers, 
   uint8_t* p = static_cast<uint8_t*>(ws);
   auto* seq_starts = reinterpret_cast<int32_t*>(p);
   p += bt::align_up((bs + 1) * sizeof(int32_t));
+  void* sched = p;
+  p += bt::align_up(bs * 8);
   auto* offsets = reinterpret_cast<int32_t*>(p);
   p += bt::align_up(static_cast<size_t>(T) * sizeof(int32_t));
   void* x = p;
@@ -187,10 +192,11 @@ extern "C" int bt_encoder_forward(const bt_layer_weights* layers, int n_layers, 
   bt::g_fwd_event_idx = 0;
   BT_TRY(bt::mark(bt::as_stream(stream)));
   BT_TRY(bt_plan_lengths(lengths, bs, mx, seq_starts, offsets, stream));
+  BT_TRY(bt_plan_sched(seq_starts, bs, mx, sched, stream));
   BT_TRY(bt_pack(x_padded, BT_F32, offsets, T, k, x, BT_BF16, stream));
   BT_TRY(bt::mark(bt::as_stream(stream)));
   for (int li = 0; li < n_layers; ++li)
-    BT_TRY(bt::encoder_layer_impl(&layers[li], cfg, seq_starts, bs, T, x, lws, lws_bytes, stream));
+    BT_TRY(bt::encoder_layer_impl(&layers[li], cfg, seq_starts, bs, T, x, lws, lws_bytes, stream, sched));
   BT_TRY(bt_unpack(x, BT_BF16, seq_starts, bs, mx, k, out_padded, BT_F32, stream));
   BT_TRY(bt::mark(bt::as_stream(stream)));
   return BT_OK;
@@ -220,15 +226,18 @@ extern "C" int bt_encoder_forward_packed(const bt_layer_weights* layers, int n_l
   uint8_t* p = static_cast<uint8_t*>(ws);
   auto* seq_starts = reinterpret_cast<int32_t*>(p);
   p += bt::align_up((bs + 1) * sizeof(int32_t));
+  void* sched = p;
+  p += bt::align_up(bs * 8);
   p += bt::align_up(static_cast<size_t>(T) * sizeof(int32_t));  // offsets (unused: input already packed)
   void* x = p;
   p += bt::align_up(static_cast<size_t>(T) * k * 2);
   void* lws = p;
   const size_t lws_bytes = bt_layer_workspace_bytes(cfg, T);
   BT_TRY(bt_plan_lengths(lengths, bs, mx, seq_starts, nullptr, stream));
+  BT_TRY(bt_plan_sched(seq_starts, bs, mx, sched, stream));
   BT_TRY(bt_bias_act(x_packed, BT_F32, k, nullptr, x, BT_BF16, k, T, k, 0, stream));  // fp32 -> bf16
   for (int li = 0; li < n_layers; ++li)
-    BT_TRY(bt::encoder_layer_impl(&layers[li], cfg, seq_starts, bs, T, x, lws, lws_bytes, stream));
+    BT_TRY(bt::encoder_layer_impl(&layers[li], cfg, seq_starts, bs, T, x, lws, lws_bytes, stream, sched));
   BT_TRY(bt_bias_act(x, BT_BF16, k, nullptr, out_packed, BT_F32, k, T, k, 0, stream));  // bf16 -> fp32
   return BT_OK;
 }

@@ -45,6 +45,7 @@ struct MhaParams {
   float sl2;       // softmax scale * log2(e)
   int padded;      // 1: padded layout (reference mha_baseline, attention.py:135-174)
   int mx;          // max_seq_len (row stride of a sequence in the padded layout)
+  const int2* sched;  // optional (packed layout): CTA z -> (start row, length), longest first
 };
 
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
@@ -115,8 +116,15 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
                                                                  const MhaParams p) {
   using Cfg = MhaCfg<RESIDENT, NST>;
   const int qt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
-  const int sb = __ldg(p.seq_starts + b);
-  const int len = __ldg(p.seq_starts + b + 1) - sb;
+  int sb, len;
+  if (p.sched) {  // longest problems first (plan_sched_kernel)
+    const int2 e = __ldg(p.sched + b);
+    sb = e.x;
+    len = e.y;
+  } else {
+    sb = __ldg(p.seq_starts + b);
+    len = __ldg(p.seq_starts + b + 1) - sb;
+  }
   // Packed layout: the sequence's rows start at seq_starts[b] and only its
   // len rows / keys are touched.  Padded layout (the reference's unfused
   // baseline): rows start at b*mx and the whole mx x mx rectangle is
@@ -445,7 +453,7 @@ static int set_smem(K kern, size_t bytes) {
 }
 
 int mha_launch(const void* qkv, const int32_t* seq_starts, int bs, int mx, int H, int d, int cutoff, int T,
-               void* out, int force_path, cudaStream_t s, int padded) {
+               void* out, int force_path, cudaStream_t s, int padded, const void* sched) {
   BT_REQUIRE(d == MHA_D, BT_ECONFIG, "fused MHA supports head_size 64, got %d", d);
   BT_REQUIRE(bs >= 1 && mx >= 1 && H >= 1 && T >= 1, BT_ESHAPE, "mha: bad shape bs=%d mx=%d H=%d T=%d", bs, mx, H, T);
   const int hidden = H * d;
@@ -458,6 +466,7 @@ int mha_launch(const void* qkv, const int32_t* seq_starts, int bs, int mx, int H
   p.sl2 = 1.4426950408889634f / sqrtf(static_cast<float>(d));
   p.padded = padded;
   p.mx = mx;
+  p.sched = padded ? nullptr : static_cast<const int2*>(sched);
   BT_REQUIRE(!padded || T == bs * mx, BT_ESHAPE, "padded mha: qkv must have bs*mx = %d rows, got %d", bs * mx, T);
   const dim3 grid((mx + MHA_QT - 1) / MHA_QT, H, bs);
   // dispatch_mha rule (attention.py:309-314); the resident (short) kernel
@@ -492,16 +501,21 @@ extern "C" int bt_debug_mha_trace(unsigned long long* buf) {
 extern "C" int bt_mha_varlen(const void* qkv, const int32_t* seq_starts, int bs, int mx, int H, int d, int cutoff,
                              int split_seq_len, void* out, int T, bt_stream_t stream) {
   BT_REQUIRE(split_seq_len >= 1, BT_ESHAPE, "split_seq_len must be >= 1, got %d", split_seq_len);
-  return bt::mha_launch(qkv, seq_starts, bs, mx, H, d, cutoff, T, out, 0, bt::as_stream(stream), 0);
+  return bt::mha_launch(qkv, seq_starts, bs, mx, H, d, cutoff, T, out, 0, bt::as_stream(stream), 0, nullptr);
+}
+
+extern "C" int bt_mha_varlen_sched(const void* qkv, const int32_t* seq_starts, const void* sched, int bs, int mx,
+                                   int H, int d, int cutoff, void* out, int T, bt_stream_t stream) {
+  return bt::mha_launch(qkv, seq_starts, bs, mx, H, d, cutoff, T, out, 0, bt::as_stream(stream), 0, sched);
 }
 
 extern "C" int bt_mha_padded(const void* qkv, const int32_t* seq_starts, int bs, int mx, int H, int d, void* out,
                              bt_stream_t stream) {
-  return bt::mha_launch(qkv, seq_starts, bs, mx, H, d, 384, bs * mx, out, 0, bt::as_stream(stream), 1);
+  return bt::mha_launch(qkv, seq_starts, bs, mx, H, d, 384, bs * mx, out, 0, bt::as_stream(stream), 1, nullptr);
 }
 
 // Test hook: force the short (1) or long (2) kernel regardless of cutoff.
 extern "C" int bt_mha_varlen_path(const void* qkv, const int32_t* seq_starts, int bs, int mx, int H, int d,
                                   void* out, int T, int path, bt_stream_t stream) {
-  return bt::mha_launch(qkv, seq_starts, bs, mx, H, d, 384, T, out, path, bt::as_stream(stream), 0);
+  return bt::mha_launch(qkv, seq_starts, bs, mx, H, d, 384, T, out, path, bt::as_stream(stream), 0, nullptr);
 }

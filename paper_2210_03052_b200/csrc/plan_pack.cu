@@ -318,6 +318,42 @@ static int launch_unpack(const void* in, const int32_t* starts, int bs, int mx, 
 
 using namespace bt;
 
+namespace bt {
+// MHA work schedule: the sequences as (start row, length) sorted by
+// descending 128-key block count (a counting sort; ties in any order -- the
+// order only decides which CTAs the hardware dispatches first, never a
+// result).  The MHA reads one int2 per CTA from it, so the longest attention
+// problems start in the first wave and the short ones fill the tail (LPT),
+// at no extra load latency per CTA.  One CTA.
+constexpr int SCHED_MAX_BUCKETS = 1024;
+__global__ void __launch_bounds__(1024) plan_sched_kernel(const int32_t* __restrict__ seq_starts, int bs, int nbk,
+                                                           int2* __restrict__ sched) {
+  __shared__ int cnt[SCHED_MAX_BUCKETS];
+  ptx::griddep_launch_dependents();
+  ptx::griddep_wait();
+  for (int i = threadIdx.x; i < nbk; i += blockDim.x) cnt[i] = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < bs; i += blockDim.x) {
+    const int len = seq_starts[i + 1] - seq_starts[i];
+    atomicAdd(&cnt[min(nbk - 1, max(0, nbk - (len + 127) / 128))], 1);  // longest -> bucket 0
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int run = 0;
+    for (int i = 0; i < nbk; ++i) {
+      const int c = cnt[i];
+      cnt[i] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < bs; i += blockDim.x) {
+    const int st = seq_starts[i], len = seq_starts[i + 1] - st;
+    sched[atomicAdd(&cnt[min(nbk - 1, max(0, nbk - (len + 127) / 128))], 1)] = make_int2(st, len);
+  }
+}
+}  // namespace bt
+
 extern "C" {
 
 int bt_version(void) { return 1; }
@@ -354,6 +390,15 @@ int bt_plan_lengths(const int32_t* lengths, int bs, int mx, int32_t* seq_starts,
     BT_LAUNCH(plan_offsets_kernel, dim3(bs < sms * 4 ? bs : sms * 4), dim3(256), 0, s, 1, (const int32_t*)seq_starts,
               bs, mx, offsets);
   }
+  return BT_OK;
+}
+
+int bt_plan_sched(const int32_t* seq_starts, int bs, int mx, void* sched, bt_stream_t stream) {
+  BT_REQUIRE(bs >= 1 && mx >= 1 && seq_starts && sched, BT_ESHAPE, "plan_sched: bad arguments");
+  const int nbk = (mx + 127) / 128;
+  BT_REQUIRE(nbk <= SCHED_MAX_BUCKETS, BT_ESHAPE, "plan_sched: max_seq_len %d too large", mx);
+  BT_LAUNCH(plan_sched_kernel, dim3(1), dim3(1024), 0, as_stream(stream), 1, seq_starts, bs, nbk,
+            static_cast<int2*>(sched));
   return BT_OK;
 }
 

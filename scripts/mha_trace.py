@@ -18,7 +18,7 @@ def main():
     from paper_2210_03052_b200.packing import plan_for_lengths
 
     _lib.require_device()
-    bs, mx, H = {"c2": (16, 256, 12), "c3": (16, 512, 16)}[sys.argv[1]]
+    bs, mx, H = {"c2": (16, 256, 12), "c3": (16, 512, 16), "c5": (2048, 512, 16)}[sys.argv[1]]
     seqs = harness.gen_lengths(bs, mx, "fixed", seed=0, alpha=0.6)
     plan = plan_for_lengths(seqs)
     qkv = torch.randn(plan.valid_word_cnt, 3 * H * 64, device="cuda").to(torch.bfloat16)

@@ -293,3 +293,30 @@ def test_gemm_bias_residual_ln(env, M, N, K):
     z = (A.float() @ W.float().t() + R.float()) + b
     ref = torch.nn.functional.layer_norm(z, (N,), gamma, beta, eps=1e-12)
     assert_close_bf16(out, ref, what=f"gemm_ln {M}x{N}x{K}")
+
+
+def test_mha_sched_order_is_result_neutral(env):
+    """The longest-first CTA schedule (bt_plan_sched) changes only the
+    dispatch order: outputs are bitwise those of the natural order, and the
+    schedule lists every sequence once, by descending key-block count."""
+    bt, torch = env
+    from paper_2210_03052_b200 import _lib
+    from paper_2210_03052_b200.attention import mha_device
+
+    lens = [5, 300, 129, 1, 512, 128, 257, 77]
+    mx, H = 512, 2
+    plan = bt.plan_for_lengths(bt.SeqLengths.of(lens, mx))
+    T = plan.valid_word_cnt
+    qkv = _rand_qkv(torch, T, H * 64, seed=5)
+    sched = torch.empty(2 * len(lens), dtype=torch.int32, device="cuda")
+    _lib.call("bt_plan_sched", plan.seq_starts_dev.data_ptr(), len(lens), mx, sched.data_ptr(), _lib.stream_ptr())
+    out = torch.empty(T, H * 64, device="cuda", dtype=torch.bfloat16)
+    _lib.call("bt_mha_varlen_sched", qkv.data_ptr(), plan.seq_starts_dev.data_ptr(), sched.data_ptr(), len(lens), mx,
+              H, 64, 384, out.data_ptr(), T, _lib.stream_ptr())
+    ref = mha_device(qkv, plan, H, 64)
+    assert torch.equal(out, ref)
+    pairs = sched.view(-1, 2).cpu().numpy()
+    starts = plan.seq_starts
+    assert sorted(map(tuple, pairs)) == sorted((int(starts[b]), lens[b]) for b in range(len(lens)))
+    blocks = [(l + 127) // 128 for _, l in pairs]
+    assert blocks == sorted(blocks, reverse=True)
