@@ -269,12 +269,19 @@ def run_ours(args, wl):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local_rank)
+    # one process per GPU; BT_BENCH_BACKEND=gloo lets a multi-rank run share one GPU to exercise the
+    # sharding / reduction logic where only one GPU is available (NCCL needs distinct devices)
+    backend = os.environ.get("BT_BENCH_BACKEND", "nccl")
+    dev = local_rank % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(dev)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
     _lib.require_device()
     peaks = load_peaks()
 
@@ -342,7 +349,7 @@ def run_ours(args, wl):
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local_rank) as clk:
+    with ClockSampler(dev) as clk:
         for i in range(args.steps):
             flush_l2()  # evict L2 between timed steps (outside the events)
             evs[i][0].record(stream)
@@ -352,7 +359,7 @@ def run_ours(args, wl):
     if dist is not None:
         dist.barrier()
     ms_local = sum(a.elapsed_time(b) for a, b in evs)
-    ms_t = torch.tensor([ms_local], dtype=torch.float64, device="cuda")
+    ms_t = torch.tensor([ms_local], dtype=torch.float64, device="cuda" if backend == "nccl" else "cpu")
     if dist is not None:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms_total = float(ms_t.item())
@@ -384,7 +391,7 @@ def run_ours(args, wl):
         e2e_ms = sum(t) * 1e3 / len(t)
         log(f"[bench] e2e per-step ms: min {min(t) * 1e3:.3f} median {statistics.median(t) * 1e3:.3f} "
             f"max {max(t) * 1e3:.3f}")
-        e_t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
+        e_t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda" if backend == "nccl" else "cpu")
         if dist is not None:
             dist.all_reduce(e_t, op=dist.ReduceOp.MAX)
         e2e_ms = float(e_t.item())
