@@ -229,6 +229,8 @@ BT_API int bt_debug_gemm_mode(int mode);
 /* Debug hook: install n cudaEvent_t (as void*) that the next bt_encoder_forward records after each
  * launch group: [0] start, [1] plan + pack, 7 per layer, then unpack; NULL uninstalls. */
 BT_API int bt_debug_forward_events(void** events, int n);
+/* Test hook: query tiles per fused-MHA CTA (0 = automatic: 4 for launches of many waves, else 1). */
+BT_API int bt_debug_mha_qg(int qg);
 /* Debug hook: per-CTA globaltimer event trace of the MHA kernels (32 u64 slots per CTA). */
 BT_API int bt_debug_mha_trace(unsigned long long* buf);
 

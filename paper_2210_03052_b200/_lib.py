@@ -77,6 +77,7 @@ SIGNATURES = {
     "bt_debug_gemm_trace": (_I, [_P]),
     "bt_debug_gemm_mode": (_I, [_I]),
     "bt_debug_mha_trace": (_I, [_P]),
+    "bt_debug_mha_qg": (_I, [_I]),
     "bt_debug_forward_events": (_I, [_P, _I]),
     "bt_mha_varlen_path": (_I, [_P, _P, _I, _I, _I, _I, _P, _I, _I, _S]),
 }

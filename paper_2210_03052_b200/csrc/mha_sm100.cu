@@ -11,6 +11,8 @@
 //
 // Q/K/V biases are already applied by the QKV GEMM epilogue.  d = 64.
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "ptx.cuh"
 #include "tma_host.cuh"
@@ -45,6 +47,7 @@ struct MhaParams {
   float sl2;       // softmax scale * log2(e)
   int padded;      // 1: padded layout (reference mha_baseline, attention.py:135-174)
   int mx;          // max_seq_len (row stride of a sequence in the padded layout)
+  int qg;          // query tiles per CTA (kernels with a separate output staging tile)
   const int2* sched;  // optional (packed layout): CTA z -> (start row, length), longest first
 };
 
@@ -91,13 +94,19 @@ __device__ __forceinline__ void reg_tie(uint32_t (&r)[32]) {
 // (they complete warpgroup 2 for setmaxnreg); both issuer warps walk their loops warp-uniformly and
 // issue through elect.sync.  TMEM: S [0,128), O [128,192) -> 256 columns;
 // ~112 KB smem -> two CTAs per SM, whose latency chains interleave.
-template <bool RESIDENT, int NST>
+template <bool RESIDENT, int NST, bool MULTI>
 struct MhaCfg {
-  static constexpr uint32_t Q_OFF = 0;                               // Q tile; output staging at the end
+  // MULTI (NST == 2 only: no room next to 2 CTAs per SM otherwise): a
+  // separate output staging tile, so a CTA can loop over several query tiles
+  // (the next Q is loaded while this tile's output is stored).  Otherwise one
+  // query tile per CTA, output staged in the Q tile.
+  static constexpr bool LOOP = MULTI && NST == 2;
+  static constexpr uint32_t Q_OFF = 0;
   static constexpr uint32_t KV_OFF = MHA_TILE;                       // slot s: K at +32K*s, V at +32K*s+16K
-  static constexpr uint32_t XCH_OFF = KV_OFF + NST * 2 * MHA_TILE;   // [3][2][128] fp32 row partials
+  static constexpr uint32_t OUT_OFF = KV_OFF + NST * 2 * MHA_TILE;   // output staging (LOOP) else == Q
+  static constexpr uint32_t XCH_OFF = OUT_OFF + (LOOP ? MHA_TILE : 0);  // [3][2][128] fp32 row partials
   static constexpr uint32_t BAR_OFF = XCH_OFF + 3 * 2 * 128 * 4;
-  static constexpr size_t SMEM = BAR_OFF + 128;
+  static constexpr size_t SMEM = BAR_OFF + 160;
 };
 
 #ifndef BT_MHA_POLY
@@ -111,11 +120,11 @@ constexpr int MHA_THREADS = 384;
 constexpr int MHA_REGS_ISSUE = 32;
 constexpr int MHA_REGS_SOFTMAX = 104;
 
-template <bool RESIDENT, int NST>
+template <bool RESIDENT, int NST, bool MULTI>
 __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_constant__ CUtensorMap tm,
                                                                  const MhaParams p) {
-  using Cfg = MhaCfg<RESIDENT, NST>;
-  const int qt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  using Cfg = MhaCfg<RESIDENT, NST, MULTI>;
+  const int h = blockIdx.y, b = blockIdx.z;
   int sb, len;
   if (p.sched) {  // longest problems first (plan_sched_kernel)
     const int2 e = __ldg(p.sched + b);
@@ -132,13 +141,17 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
   // of attention.py:162-163) and query rows >= len written as zeros.
   const int s0 = p.padded ? b * p.mx : sb;
   const int work = p.padded ? p.mx : len;
-  const int q0 = qt * MHA_QT;
-  if (q0 >= work) return;  // CTA-uniform: this q tile is past the sequence
+  // this CTA's query tiles: qt0, qt0 + 1, ... (p.qg per CTA when Cfg::LOOP)
+  const int qg = Cfg::LOOP ? p.qg : 1;
+  const int qt0 = blockIdx.x * qg;
+  if (qt0 * MHA_QT >= work) return;  // CTA-uniform: past the sequence
+  const int nqt = Cfg::LOOP ? min(qg, (work + MHA_QT - 1) / MHA_QT - qt0) : 1;
   const int nkb = (work + MHA_KB - 1) / MHA_KB;
 
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sQ = smem + Cfg::Q_OFF;
   uint8_t* sKV = smem + Cfg::KV_OFF;
+  uint8_t* sOut = smem + (Cfg::LOOP ? Cfg::OUT_OFF : Cfg::Q_OFF);
   float* xch = reinterpret_cast<float*>(smem + Cfg::XCH_OFF);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::BAR_OFF);
   uint64_t* q_full = bars;
@@ -149,7 +162,9 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
   uint64_t* p_full = s_full + 2;          // P(j) in TMEM, O rescaled: issue P(j) V(j)
   uint64_t* pv_done = s_full + 3;         // P(j) V(j) accumulated into O: P columns free
   uint64_t* v_full = s_full + 4;          // [NST] V block landed (S(j) needs only K(j))
-  uint32_t* holder = reinterpret_cast<uint32_t*>(v_full + NST);
+  uint64_t* q_empty = v_full + NST;       // the tile's last S MMA has read Q
+  uint64_t* o_free = q_empty + 1;         // the softmax warps have read O (next tile may overwrite it)
+  uint32_t* holder = reinterpret_cast<uint32_t*>(o_free + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -164,6 +179,8 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
     ptx::mbar_init(s_read, 256);
     ptx::mbar_init(p_full, 256);
     ptx::mbar_init(pv_done, 1);
+    ptx::mbar_init(q_empty, 1);
+    ptx::mbar_init(o_free, 256);
     ptx::fence_mbar_init();
   }
   if (warp == 0) {
@@ -186,11 +203,6 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
   if (warp == 8) {
     // ------------------------------------------------ TMA producer
     ptx::griddep_wait();  // qkv is produced by the previous kernel
-    if (ptx::elect_one()) {
-      ptx::mbar_arrive_expect_tx(q_full, MHA_TILE);
-      ptx::tma_load_2d(sQ, &tm, q_full, h * MHA_D, s0 + q0);
-    }
-    __syncwarp();
     // K blocks on their own barriers ahead of V: S(j) = Q K(j)^T can start
     // before V(j) (needed only by P(j) V(j)) has landed
     auto load_k = [&](int j, int slot) {
@@ -208,15 +220,26 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
       }
       __syncwarp();
     };
-    if (RESIDENT) {
-      for (int j = 0; j < nkb; ++j) load_k(j, j);
-      for (int j = 0; j < nkb; ++j) load_v(j, j);
-    } else {
-      for (int j = 0; j < nkb; ++j) {
-        const int slot = j % NST;
-        ptx::mbar_wait(&kv_empty[slot], ((j / NST) & 1) ^ 1u);
-        load_k(j, slot);
-        load_v(j, slot);
+    int kvg = 0;  // K/V blocks loaded so far (ring position across query tiles)
+    for (int t = 0; t < nqt; ++t) {
+      if (t > 0) ptx::mbar_wait(q_empty, (t - 1) & 1);  // the previous tile's S MMAs are done with sQ
+      if (ptx::elect_one()) {
+        ptx::mbar_arrive_expect_tx(q_full, MHA_TILE);
+        ptx::tma_load_2d(sQ, &tm, q_full, h * MHA_D, s0 + (qt0 + t) * MHA_QT);
+      }
+      __syncwarp();
+      if (RESIDENT) {
+        if (t == 0) {  // K / V stay resident for every query tile of the CTA
+          for (int j = 0; j < nkb; ++j) load_k(j, j);
+          for (int j = 0; j < nkb; ++j) load_v(j, j);
+        }
+      } else {
+        for (int j = 0; j < nkb; ++j, ++kvg) {
+          const int slot = kvg % NST;
+          ptx::mbar_wait(&kv_empty[slot], ((kvg / NST) & 1) ^ 1u);
+          load_k(j, slot);
+          load_v(j, slot);
+        }
       }
     }
   } else if (warp == 9) {
@@ -225,42 +248,53 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
     constexpr uint32_t idesc_o = ptx::idesc_bf16(128, MHA_D, false, true);    // P (TMEM, K-major) x V (MN-major)
     const uint64_t q_desc = ptx::sdesc_sw128(ptx::smem_u32(sQ), 1024, 16);
     const uint32_t kv_base = ptx::smem_u32(sKV);
-    ptx::mbar_wait(q_full, 0);
-    if (lane == 0) MHA_TRACE(1);
-    auto issue_pv = [&](int pj, int pslot) {
-      // O (+)= P(pj) V(pj); only the k-steps that hold keys of the problem
-      ptx::mbar_wait(&v_full[pslot], RESIDENT ? 0u : static_cast<uint32_t>((pj / NST) & 1));
-      ptx::mbar_wait(p_full, pj & 1);
+    auto issue_pv = [&](int g, int jt, int t, int pslot, uint32_t kvpar) {
+      // O (+)= P(g) V(g): item g is block jt of query tile t; only the
+      // k-steps that hold keys of the problem
+      ptx::mbar_wait(&v_full[pslot], kvpar);
+      ptx::mbar_wait(p_full, g & 1);
+      if (jt == 0 && t > 0) ptx::mbar_wait(o_free, (t - 1) & 1);  // the previous tile's O has been read
       ptx::tc_fence_after();
-      const int nks = min(MHA_KB, work - pj * MHA_KB + 15) / 16;
+      const int nks = min(MHA_KB, work - jt * MHA_KB + 15) / 16;
       const uint64_t v_desc = ptx::sdesc_sw128(kv_base + pslot * 2 * MHA_TILE + MHA_TILE, 1024, MHA_TILE);
       if (ptx::elect_one()) {
         for (int ks = 0; ks < nks; ++ks)
           ptx::mma_bf16_ts(tmem + O_COL, tmem + P_COL + 8 * ks, v_desc + ks * ((16 * 128) >> 4), idesc_o,
-                           (pj > 0 || ks > 0) ? 1u : 0u);
+                           (jt > 0 || ks > 0) ? 1u : 0u);
         ptx::mma_commit(pv_done);
-        if (!RESIDENT) ptx::mma_commit(&kv_empty[pslot]);  // K and V of block pj consumed
+        if (!RESIDENT) ptx::mma_commit(&kv_empty[pslot]);  // K and V of this block consumed
       }
       __syncwarp();
     };
-    int prev_slot = 0;
-    for (int j = 0; j < nkb; ++j) {
-      const int slot = RESIDENT ? j : j % NST;
-      ptx::mbar_wait(&kv_full[slot], RESIDENT ? 0u : static_cast<uint32_t>((j / NST) & 1));
-      if (j > 0) ptx::mbar_wait(s_read, (j - 1) & 1);  // S(j-1) is in the softmax registers
-      ptx::tc_fence_after();
-      const uint64_t k_desc = ptx::sdesc_sw128(kv_base + slot * 2 * MHA_TILE, 1024, 16);
-      if (ptx::elect_one()) {
+    int g = 0, kvg = 0;  // items issued (S), K/V ring position
+    int prev_jt = 0, prev_t = 0, prev_slot = 0;
+    uint32_t prev_par = 0;
+    for (int t = 0; t < nqt; ++t) {
+      ptx::mbar_wait(q_full, t & 1);
+      if (lane == 0 && t == 0) MHA_TRACE(1);
+      for (int j = 0; j < nkb; ++j, ++g, ++kvg) {
+        const int slot = RESIDENT ? j : kvg % NST;
+        const uint32_t par = RESIDENT ? 0u : static_cast<uint32_t>((kvg / NST) & 1);
+        ptx::mbar_wait(&kv_full[slot], par);
+        if (g > 0) ptx::mbar_wait(s_read, (g - 1) & 1);  // S(g-1) is in the softmax registers
+        ptx::tc_fence_after();
+        const uint64_t k_desc = ptx::sdesc_sw128(kv_base + slot * 2 * MHA_TILE, 1024, 16);
+        if (ptx::elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < MHA_D / 16; ++kk)
-          ptx::mma_bf16_ss(tmem + S_COL, q_desc + 2 * kk, k_desc + 2 * kk, idesc_s, kk > 0);
-        ptx::mma_commit(s_full);
+          for (int kk = 0; kk < MHA_D / 16; ++kk)
+            ptx::mma_bf16_ss(tmem + S_COL, q_desc + 2 * kk, k_desc + 2 * kk, idesc_s, kk > 0);
+          ptx::mma_commit(s_full);
+          if (j == nkb - 1) ptx::mma_commit(q_empty);  // this tile's Q is no longer read
+        }
+        __syncwarp();
+        if (g > 0) issue_pv(g - 1, prev_jt, prev_t, prev_slot, prev_par);
+        prev_jt = j;
+        prev_t = t;
+        prev_slot = slot;
+        prev_par = par;
       }
-      __syncwarp();
-      if (j > 0) issue_pv(j - 1, prev_slot);
-      prev_slot = slot;
     }
-    issue_pv(nkb - 1, prev_slot);
+    issue_pv(g - 1, prev_jt, prev_t, prev_slot, prev_par);
   }
   } else {
     ptx::setmaxnreg_inc<MHA_REGS_SOFTMAX>();  // warpgroups 0-1: softmax
@@ -273,18 +307,21 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
     const int quarter = warp & 3, half = warp >> 2;
     const int row = quarter * 32 + lane;
     const int pair_bar = 1 + quarter;  // named barrier of warps quarter and quarter + 4
-    const bool warp_live = q0 + quarter * 32 < work;
     const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
     const uint32_t s_my = trow + S_COL + half * 64;
     const uint32_t p_my = trow + P_COL + half * 32;
     const uint32_t o_my = trow + O_COL + half * 32;
     const float sl2 = p.sl2;
+    int g = 0;  // items consumed, across query tiles
+    for (int t = 0; t < nqt; ++t) {
+    const int q0 = (qt0 + t) * MHA_QT;
+    const bool warp_live = q0 + quarter * 32 < work;
     float mref = -INFINITY, lsum = 0.f;
-    for (int j = 0; j < nkb; ++j) {
+    for (int j = 0; j < nkb; ++j, ++g) {
       const int kvalid = min(MHA_KB, len - j * MHA_KB) - half * 64;  // valid keys among my 64 (may be <= 0)
-      ptx::mbar_wait(s_full, j & 1);
+      ptx::mbar_wait(s_full, g & 1);
       ptx::tc_fence_after();
-      if (threadIdx.x == 0) MHA_TRACE(2 + 2 * j);
+      if (threadIdx.x == 0 && t == 0) MHA_TRACE(2 + 2 * j);
       uint32_t r0[32], r1[32];  // my 64 S values of this row
       if (warp_live) {
         ptx::tmem_ld32(s_my, r0);
@@ -294,7 +331,7 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
       }
       ptx::tc_fence_before();
       ptx::mbar_arrive(s_read);  // the MMA warp may overwrite S with the next block
-      if (threadIdx.x == 0 && j < 3) MHA_TRACE(16 + 4 * j);
+      if (threadIdx.x == 0 && t == 0 && j < 3) MHA_TRACE(16 + 4 * j);
 #define SV(c, i) __uint_as_float((c) == 0 ? r0[i] : r1[i])
       bool need = false;
       float mnew = mref, alpha = 1.f;
@@ -319,7 +356,7 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
           }
         }
         // exchange the partial max with the row's other thread
-        float* x = xch + (j & 1) * 256;
+        float* x = xch + (g & 1) * 256;
         x[half * 128 + row] = fmaxf(ptx::max3(m4[0], m4[1], m4[2]), m4[3]);
         named_bar_sync(pair_bar, 64);
         const float bmax = fmaxf(x[row], x[128 + row]);
@@ -327,13 +364,13 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
         need = (mnew - mref) * sl2 > MHA_RESCALE_LOG2;  // true on the first block (mref = -inf)
         alpha = (need && mref != -INFINITY) ? ptx::ex2_approx((mref - mnew) * sl2) : 1.f;
         if (need) mref = mnew;
-        if (threadIdx.x == 0 && j < 3) MHA_TRACE(17 + 4 * j);
+        if (threadIdx.x == 0 && t == 0 && j < 3) MHA_TRACE(17 + 4 * j);
       }
       if (j > 0) {
-        ptx::mbar_wait(pv_done, (j - 1) & 1);  // P(j-1) V(j-1) is in O; the P columns are free
+        ptx::mbar_wait(pv_done, (g - 1) & 1);  // P(g-1) V(g-1) is in O; the P columns are free
         ptx::tc_fence_after();
       }
-      if (threadIdx.x == 0 && j < 3) MHA_TRACE(18 + 4 * j);
+      if (threadIdx.x == 0 && t == 0 && j < 3) MHA_TRACE(18 + 4 * j);
       if (warp_live) {
         const float msc = mref * sl2;
         const unsigned long long sl2x2 = ptx::f2(sl2, sl2), nm2 = ptx::f2(-msc, -msc);
@@ -387,17 +424,17 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
         }
         ptx::tmem_wait_st();
       }
-      if (threadIdx.x == 0 && j < 3) MHA_TRACE(19 + 4 * j);
+      if (threadIdx.x == 0 && t == 0 && j < 3) MHA_TRACE(19 + 4 * j);
       ptx::tc_fence_before();
       ptx::mbar_arrive(p_full);
-      if (threadIdx.x == 0) MHA_TRACE(3 + 2 * j);
+      if (threadIdx.x == 0 && t == 0) MHA_TRACE(3 + 2 * j);
     }
 #undef SV
-    ptx::mbar_wait(pv_done, (nkb - 1) & 1);
+    ptx::mbar_wait(pv_done, (g - 1) & 1);  // this tile's last P V
     ptx::tc_fence_after();
-    if (threadIdx.x == 0) MHA_TRACE(30);
-    // O / l -> bf16 rows staged in the Q tile (free: every MMA has completed)
-    // -> coalesced 16-byte stores, 4 rows per warp instruction
+    if (threadIdx.x == 0 && t == 0) MHA_TRACE(30);
+    // O / l -> bf16 rows staged in shared memory -> coalesced 16-byte stores,
+    // 4 rows per warp instruction
     if (warp_live) {
       uint32_t o[32];
       ptx::tmem_ld32(o_my, o);
@@ -408,7 +445,7 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
       ptx::tmem_wait_ld(o);
       const float inv = (q0 + row < len) ? 1.0f / l : 0.f;
       const unsigned long long inv2 = ptx::f2(inv, inv);
-      uint8_t* mine = sQ + row * 128;
+      uint8_t* mine = sOut + row * 128;
 #pragma unroll
       for (int jj = 0; jj < 4; ++jj) {
         uint32_t w[4];
@@ -430,11 +467,17 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
         const int rr = quarter * 32 + half * 16 + it * 4 + (lane >> 3);
         const int jj = lane & 7;
         if (q0 + rr < work) {
-          const uint4 v = *reinterpret_cast<const uint4*>(sQ + rr * 128 + ((jj ^ (rr & 7)) << 4));
+          const uint4 v = *reinterpret_cast<const uint4*>(sOut + rr * 128 + ((jj ^ (rr & 7)) << 4));
           *reinterpret_cast<uint4*>(p.out + static_cast<size_t>(s0 + q0 + rr) * p.hidden + h * MHA_D + jj * 8) = v;
         }
       }
+      if (t + 1 < nqt) named_bar_sync(pair_bar, 64);  // the pair's rows are stored: sOut free for the next tile
     }
+    if (t + 1 < nqt) {
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(o_free);  // O of this tile has been read: the next tile's first P V may overwrite it
+    }
+    }  // query tiles
     if (threadIdx.x == 0) MHA_TRACE(31);
   }
 
@@ -452,6 +495,19 @@ static int set_smem(K kern, size_t bytes) {
   return BT_OK;
 }
 
+// Query tiles per CTA: BT_MHA_QG (1..8) or bt_debug_mha_qg override the
+// policy (A/B measurement, tests).
+static int g_mha_qg_override = 0;
+static int mha_qtiles_per_cta(int nqt, bool many_waves) {
+  static int forced = -1;
+  if (forced < 0) {
+    const char* e = getenv("BT_MHA_QG");
+    forced = (e && e[0] >= '1' && e[0] <= '8') ? e[0] - '0' : 0;
+  }
+  const int qg = g_mha_qg_override ? g_mha_qg_override : forced ? forced : (many_waves ? 4 : 1);
+  return qg < nqt ? qg : nqt;
+}
+
 int mha_launch(const void* qkv, const int32_t* seq_starts, int bs, int mx, int H, int d, int cutoff, int T,
                void* out, int force_path, cudaStream_t s, int padded, const void* sched) {
   BT_REQUIRE(d == MHA_D, BT_ECONFIG, "fused MHA supports head_size 64, got %d", d);
@@ -467,31 +523,58 @@ int mha_launch(const void* qkv, const int32_t* seq_starts, int bs, int mx, int H
   p.padded = padded;
   p.mx = mx;
   p.sched = padded ? nullptr : static_cast<const int2*>(sched);
+  p.qg = 1;
   BT_REQUIRE(!padded || T == bs * mx, BT_ESHAPE, "padded mha: qkv must have bs*mx = %d rows, got %d", bs * mx, T);
-  const dim3 grid((mx + MHA_QT - 1) / MHA_QT, H, bs);
+  const int nqt = (mx + MHA_QT - 1) / MHA_QT;
   // dispatch_mha rule (attention.py:309-314); the resident (short) kernel
   // holds at most 384 keys on chip.
   bool use_short = mx <= cutoff && mx <= MHA_SHORT_MAX_KEYS;
   if (force_path == 1) use_short = true;
   if (force_path == 2) use_short = false;
   BT_REQUIRE(!use_short || mx <= MHA_SHORT_MAX_KEYS, BT_ECONFIG, "short MHA holds <= 384 keys, mx=%d", mx);
+  // Query tiles per CTA: with many waves of CTAs (large batches) a CTA walks
+  // all tiles of its sequence-head, sharing K / V and overlapping the next
+  // tile's Q load with the previous tile's output store; with few waves the
+  // longer per-CTA chain would cost more than that saves, so one tile per CTA.
+  const int sms = num_sms() > 0 ? num_sms() : 148;
+  const long long ctas1 = static_cast<long long>(nqt) * H * bs;
+  const int qg = mha_qtiles_per_cta(nqt, ctas1 > 16LL * 2 * sms);
+  p.qg = qg;
+  const dim3 grid_multi((nqt + qg - 1) / qg, H, bs), grid_one(nqt, H, bs);
+#define BT_MHA_GO(R, N, M, G)                                                                                 \
+  do {                                                                                                        \
+    static bool set = false;                                                                                  \
+    if (!set) {                                                                                               \
+      BT_TRY(set_smem(mha_fwd_kernel<R, N, M>, MhaCfg<R, N, M>::SMEM));                                       \
+      set = true;                                                                                             \
+    }                                                                                                         \
+    BT_LAUNCH((mha_fwd_kernel<R, N, M>), G, dim3(MHA_THREADS), MhaCfg<R, N, M>::SMEM, s, 1, tm, p);           \
+  } while (0)
   if (use_short && mx <= 2 * MHA_KB) {
-    static bool set = false;
-    if (!set) { BT_TRY(set_smem(mha_fwd_kernel<true, 2>, MhaCfg<true, 2>::SMEM)); set = true; }
-    BT_LAUNCH((mha_fwd_kernel<true, 2>), grid, dim3(MHA_THREADS), MhaCfg<true, 2>::SMEM, s, 1, tm, p);
+    if (qg > 1)
+      BT_MHA_GO(true, 2, true, grid_multi);
+    else
+      BT_MHA_GO(true, 2, false, grid_one);
   } else if (use_short) {
-    static bool set = false;
-    if (!set) { BT_TRY(set_smem(mha_fwd_kernel<true, 3>, MhaCfg<true, 3>::SMEM)); set = true; }
-    BT_LAUNCH((mha_fwd_kernel<true, 3>), grid, dim3(MHA_THREADS), MhaCfg<true, 3>::SMEM, s, 1, tm, p);
+    BT_MHA_GO(true, 3, false, grid_one);
   } else {
-    static bool set = false;
-    if (!set) { BT_TRY(set_smem(mha_fwd_kernel<false, 2>, MhaCfg<false, 2>::SMEM)); set = true; }
-    BT_LAUNCH((mha_fwd_kernel<false, 2>), grid, dim3(MHA_THREADS), MhaCfg<false, 2>::SMEM, s, 1, tm, p);
+    if (qg > 1)
+      BT_MHA_GO(false, 2, true, grid_multi);
+    else
+      BT_MHA_GO(false, 2, false, grid_one);
   }
+#undef BT_MHA_GO
   return BT_OK;
 }
 
 }  // namespace bt
+
+// Test hook: force the query tiles per MHA CTA (0 = automatic policy).
+extern "C" int bt_debug_mha_qg(int qg) {
+  BT_REQUIRE(qg >= 0 && qg <= 8, BT_ECONFIG, "bt_debug_mha_qg: 0..8");
+  bt::g_mha_qg_override = qg;
+  return BT_OK;
+}
 
 extern "C" int bt_debug_mha_trace(unsigned long long* buf) {
   BT_CUDA_CHECK(cudaMemcpyToSymbol(bt::g_mha_trace, &buf, sizeof(buf)));

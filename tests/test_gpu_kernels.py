@@ -320,3 +320,25 @@ def test_mha_sched_order_is_result_neutral(env):
     assert sorted(map(tuple, pairs)) == sorted((int(starts[b]), lens[b]) for b in range(len(lens)))
     blocks = [(l + 127) // 128 for _, l in pairs]
     assert blocks == sorted(blocks, reverse=True)
+
+
+@pytest.mark.parametrize("lens,mx", [([512, 300, 129, 1, 450, 257], 512), ([256, 140, 9, 255], 256),
+                                     ([1000, 3, 700], 1024)])
+def test_mha_query_tiles_per_cta(env, lens, mx):
+    """The multi-tile MHA variant (a CTA walks several query tiles of its
+    sequence-head; chosen automatically for launches of many waves) is bitwise
+    the single-tile kernel, which the other tests pin to the oracle."""
+    bt, torch = env
+    from paper_2210_03052_b200 import _lib
+    from paper_2210_03052_b200.attention import mha_device
+
+    plan = bt.plan_for_lengths(bt.SeqLengths.of(lens, mx))
+    qkv = _rand_qkv(torch, plan.valid_word_cnt, 2 * 64, seed=13)
+    try:
+        _lib.call("bt_debug_mha_qg", 1)
+        one = mha_device(qkv, plan, 2, 64).clone()
+        for qg in (2, 4, 8):
+            _lib.call("bt_debug_mha_qg", qg)
+            assert torch.equal(mha_device(qkv, plan, 2, 64), one), f"qg={qg}"
+    finally:
+        _lib.call("bt_debug_mha_qg", 0)
