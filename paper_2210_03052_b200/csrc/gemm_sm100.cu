@@ -38,6 +38,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <map>
+#include <mutex>
 
 #include "common.cuh"
 #include "ptx.cuh"
@@ -564,8 +565,16 @@ struct StreamKWorkspace {
   int* flags = nullptr;
 };
 
-static int streamk_workspace(StreamKWorkspace** out) {
-  static StreamKWorkspace ws;
+// Host state shared by every caller thread (autotune cache, stream-K fix-up
+// buffers) is guarded by one mutex.  Fix-up buffers are per CUDA stream: two
+// stream-K GEMMs can only run at once on different streams, and then they
+// must not share flags / partials.
+static std::mutex g_gemm_host_mu;
+
+static int streamk_workspace(cudaStream_t s, StreamKWorkspace** out) {
+  static std::map<cudaStream_t, StreamKWorkspace> per_stream;
+  std::lock_guard<std::mutex> lock(g_gemm_host_mu);
+  StreamKWorkspace& ws = per_stream[s];
   if (!ws.partials) {
     // one fp32 128 x 256 partial per (unit, rank) + one flag each; flags
     // start at 0 and every finisher resets the flags it consumed
@@ -689,7 +698,7 @@ static int gemm_run(const void* A, const void* Bt, const float* bias, const void
   int units = p.num_tiles < slots ? p.num_tiles : slots;
   if (ch.streamk) {
     StreamKWorkspace* ws = nullptr;
-    BT_TRY(streamk_workspace(&ws));
+    BT_TRY(streamk_workspace(s, &ws));
     p.partials = ws->partials;
     p.flags = ws->flags;
     units = slots < MAX_UNITS ? slots : MAX_UNITS;
@@ -818,16 +827,25 @@ int gemm_launch(const void* A, const void* Bt, const float* bias, const void* re
   GemmChoice ch = choose_tile(M, N, K, sms);
   if (force == 0 && g_force_streamk < 0 && g_gemm_dbg == 0 && autotune_enabled()) {
     const TuneKey key{N, K, epi, (M + 255) / 256};
-    auto& cache = tune_cache();
-    auto it = cache.find(key);
-    if (it != cache.end()) {
-      ch = it->second;
-    } else {
+    bool hit = false;
+    {
+      std::lock_guard<std::mutex> lock(g_gemm_host_mu);
+      auto& cache = tune_cache();
+      auto it = cache.find(key);
+      if (it != cache.end()) {
+        ch = it->second;
+        hit = true;
+      }
+    }
+    if (!hit) {
       cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
       BT_CUDA_CHECK(cudaStreamIsCapturing(s, &cs));
       if (cs == cudaStreamCaptureStatusNone) {
+        static std::mutex tune_mu;  // one autotune at a time (it times launches on an idle device)
+        std::lock_guard<std::mutex> tl(tune_mu);
         BT_TRY(autotune(A, Bt, bias, residual, C, M, N, K, epi, s, &ch));
-        cache[key] = ch;
+        std::lock_guard<std::mutex> lock(g_gemm_host_mu);
+        tune_cache()[key] = ch;
       }
     }
   }

@@ -341,6 +341,10 @@ class BertEncoderB200:
         self._cfg_c = layer_cfg_c(self.config)
         self._ws = None
         self._graphs = {}
+        # one forward at a time per engine: the workspace, the cached graphs
+        # and their I/O buffers are shared state (the service runs requests on
+        # a thread pool)
+        self._lock = threading.RLock()
         self._io_stream = None
 
     def layer(self, i: int) -> DeviceLayer:
@@ -355,26 +359,28 @@ class BertEncoderB200:
                        config: ModelConfig | None = None):
         """Device forward: int32 lengths [bs], fp32 padded input [bs*mx, k] ->
         fp32 padded output (exact-zero padded rows).  No host sync."""
-        cfg = config or self.config
-        cfg_c = self._cfg_c if config is None else layer_cfg_c(cfg)
-        ws_bytes = int(_lib.load().bt_forward_workspace_bytes(C.byref(cfg_c), bs, T))
-        ws = self.workspace(ws_bytes)
-        _lib.call("bt_encoder_forward", self._c_layers, cfg.layers, C.byref(cfg_c), lengths_dev.data_ptr(), bs, T,
-                  x_padded_f32.data_ptr(), out_padded_f32.data_ptr(), ws.data_ptr(), ws_bytes,
-                  _lib.stream_ptr(stream))
-        return out_padded_f32
+        with self._lock:
+            cfg = config or self.config
+            cfg_c = self._cfg_c if config is None else layer_cfg_c(cfg)
+            ws_bytes = int(_lib.load().bt_forward_workspace_bytes(C.byref(cfg_c), bs, T))
+            ws = self.workspace(ws_bytes)
+            _lib.call("bt_encoder_forward", self._c_layers, cfg.layers, C.byref(cfg_c), lengths_dev.data_ptr(), bs, T,
+                      x_padded_f32.data_ptr(), out_padded_f32.data_ptr(), ws.data_ptr(), ws_bytes,
+                      _lib.stream_ptr(stream))
+            return out_padded_f32
 
     def forward_ptrs(self, lengths_ptr: int, bs: int, T: int, x_ptr: int, out_ptr: int, stream=None,
                      config: ModelConfig | None = None):
         """Forward on raw pointers: lengths int32[bs], padded fp32 input and
         output [bs*mx, k].  Each may be device memory or pinned host memory
         (zero-copy: only valid input rows cross PCIe; no bulk memcpy)."""
-        cfg = config or self.config
-        cfg_c = self._cfg_c if config is None else layer_cfg_c(cfg)
-        ws_bytes = int(_lib.load().bt_forward_workspace_bytes(C.byref(cfg_c), bs, T))
-        ws = self.workspace(ws_bytes)
-        _lib.call("bt_encoder_forward", self._c_layers, cfg.layers, C.byref(cfg_c), lengths_ptr, bs, T, x_ptr,
-                  out_ptr, ws.data_ptr(), ws_bytes, _lib.stream_ptr(stream))
+        with self._lock:
+            cfg = config or self.config
+            cfg_c = self._cfg_c if config is None else layer_cfg_c(cfg)
+            ws_bytes = int(_lib.load().bt_forward_workspace_bytes(C.byref(cfg_c), bs, T))
+            ws = self.workspace(ws_bytes)
+            _lib.call("bt_encoder_forward", self._c_layers, cfg.layers, C.byref(cfg_c), lengths_ptr, bs, T, x_ptr,
+                      out_ptr, ws.data_ptr(), ws_bytes, _lib.stream_ptr(stream))
 
     GRAPH_CACHE = 4  # batch shapes whose packed forward is kept as a CUDA graph
 
@@ -426,42 +432,44 @@ class BertEncoderB200:
         encoder runs packed -> packed as one CUDA graph (cached per batch
         shape), and the padded output rows are zeroed on the host while the
         GPU computes.  Synchronises."""
-        cfg = config or self.config
-        cfg_c = self._cfg_c if config is None else layer_cfg_c(cfg)
-        bs, mx, k = seqs.batch_size, seqs.max_seq_len, cfg.hidden_dim
-        graph, run, xp, yp, _, _ = self._graph_entry(seqs, cfg, cfg_c)
-        lengths_h = np.ascontiguousarray(np.asarray(seqs.lengths, dtype=np.int32))
-        lp = lengths_h.ctypes.data
-        torch = self.torch
-        if self._io_stream is None:
-            self._io_stream = torch.cuda.Stream()  # not the legacy default stream: batched DMA submission
-        io = self._io_stream
-        io.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(io):
-            s = _lib.stream_ptr()
-            _lib.call("bt_copy_rows", xp.data_ptr(), x_pinned.data_ptr(), lp, bs, mx, k * 4, 1, s)
-            if graph is not None:
-                graph.replay()
-            else:
-                run()
-            _lib.call("bt_copy_rows", out_pinned.data_ptr(), yp.data_ptr(), lp, bs, mx, k * 4, 0, s)
-        # padded rows of the output are exact zeros (packing.py:158-159)
-        o = out_pinned.numpy().reshape(bs, mx, k)
-        for b, n in enumerate(seqs.lengths):
-            if n < mx:
-                o[b, n:] = 0.0
-        io.synchronize()
-        return out_pinned
+        with self._lock:
+            cfg = config or self.config
+            cfg_c = self._cfg_c if config is None else layer_cfg_c(cfg)
+            bs, mx, k = seqs.batch_size, seqs.max_seq_len, cfg.hidden_dim
+            graph, run, xp, yp, _, _ = self._graph_entry(seqs, cfg, cfg_c)
+            lengths_h = np.ascontiguousarray(np.asarray(seqs.lengths, dtype=np.int32))
+            lp = lengths_h.ctypes.data
+            torch = self.torch
+            if self._io_stream is None:
+                self._io_stream = torch.cuda.Stream()  # not the legacy default stream: batched DMA submission
+            io = self._io_stream
+            io.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(io):
+                s = _lib.stream_ptr()
+                _lib.call("bt_copy_rows", xp.data_ptr(), x_pinned.data_ptr(), lp, bs, mx, k * 4, 1, s)
+                if graph is not None:
+                    graph.replay()
+                else:
+                    run()
+                _lib.call("bt_copy_rows", out_pinned.data_ptr(), yp.data_ptr(), lp, bs, mx, k * 4, 0, s)
+            # padded rows of the output are exact zeros (packing.py:158-159)
+            o = out_pinned.numpy().reshape(bs, mx, k)
+            for b, n in enumerate(seqs.lengths):
+                if n < mx:
+                    o[b, n:] = 0.0
+            io.synchronize()
+            return out_pinned
 
     def layer_device(self, li: int, x_bf16, plan: PackingPlan, stream=None):
         """In-place encoder_layer on a packed bf16 [T, k] device tensor."""
-        T = plan.valid_word_cnt
-        ws_bytes = int(_lib.load().bt_layer_workspace_bytes(C.byref(self._cfg_c), T))
-        ws = self.workspace(ws_bytes)
-        _lib.call("bt_encoder_layer", C.byref(self._layers[li].c), C.byref(self._cfg_c),
-                  plan.seq_starts_dev.data_ptr(), plan.batch_size, T, x_bf16.data_ptr(), ws.data_ptr(), ws_bytes,
-                  _lib.stream_ptr(stream))
-        return x_bf16
+        with self._lock:
+            T = plan.valid_word_cnt
+            ws_bytes = int(_lib.load().bt_layer_workspace_bytes(C.byref(self._cfg_c), T))
+            ws = self.workspace(ws_bytes)
+            _lib.call("bt_encoder_layer", C.byref(self._layers[li].c), C.byref(self._cfg_c),
+                      plan.seq_starts_dev.data_ptr(), plan.batch_size, T, x_bf16.data_ptr(), ws.data_ptr(), ws_bytes,
+                      _lib.stream_ptr(stream))
+            return x_bf16
 
 
 # weights (or layer) object -> (weakref, engine, geometry); one upload per object

@@ -133,3 +133,37 @@ def test_flop_counter_and_albert_sharing(bt):
     ocfg = orc.OracleConfig(3, 16, 64, 32, 3, share_layer_weights=True)
     want = orc.forward(orc.init_weights(ocfg, 0), lens, x, ocfg)
     assert_close_bf16(y, want, max_abs_max=2e-2, what="albert")
+
+
+def test_forward_thread_safe():
+    """The service calls forward() from a thread pool: concurrent calls on one
+    model (shared engine, workspace and cached graphs) return exactly what a
+    single call returns."""
+    import threading
+
+    import paper_2210_03052_b200 as bt
+    from oracle import packbert_np as orc
+
+    lens = [100, 7, 64, 128]
+    cfg = bt.preset_config("bert_base", len(lens), 128, bt.OptFlags.all_on(), layers=2)
+    w = bt.init_weights(cfg, seed=3)
+    x = orc.gen_input(lens, 128, 768, seed=3)
+    seqs = bt.SeqLengths.of(lens, 128)
+    ref = bt.forward(w, seqs, bt.Tensor(x), cfg).array
+    outs, errs = [None] * 6, []
+
+    def run(i):
+        try:
+            for _ in range(3):
+                outs[i] = bt.forward(w, seqs, bt.Tensor(x), cfg).array
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+
+    threads = [threading.Thread(target=run, args=(i,)) for i in range(6)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errs, errs
+    for o in outs:
+        assert np.array_equal(o, ref)
