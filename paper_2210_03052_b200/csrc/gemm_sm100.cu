@@ -159,7 +159,7 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
 // Epilogue math on 32 consecutive columns of one row, packed to 16 bf16x2.
 template <int EPI>
 __device__ __forceinline__ void epi_math32(float (&v)[32], const GemmParams& p, int row, int col, bool row_ok,
-                                           uint32_t* out16) {
+                                           uint32_t* out16, const float4* bias) {
   if constexpr (EPI == BT_EPI_BIAS_RESIDUAL) {
     if (row_ok) {
       const uint4* r = reinterpret_cast<const uint4*>(p.residual + static_cast<size_t>(row) * p.N + col);
@@ -180,7 +180,7 @@ __device__ __forceinline__ void epi_math32(float (&v)[32], const GemmParams& p, 
     const float4* b4 = reinterpret_cast<const float4*>(p.bias + col);
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-      const float4 b = __ldg(b4 + q);
+      const float4 b = bias ? bias[q] : __ldg(b4 + q);
       v[4 * q] += b.x;
       v[4 * q + 1] += b.y;
       v[4 * q + 2] += b.z;
@@ -470,6 +470,17 @@ __global__ void __launch_bounds__(GemmCfg<PAIR, BN, EW>::THREADS, 1)
 #pragma unroll 1
         for (int c = colgrp * 64; c < BN; c += 64 * NGRP) {
           uint32_t r0[32], r1[32];
+          const int col = nb * BN + c;
+          // bias for the 64 columns, loaded before the TMEM wait so its latency
+          // overlaps the accumulator load instead of heading the math chain
+          // (stream-K variants keep the in-chain loads: the hoisted registers
+          // would spill next to the partial-sum fix-up)
+          float4 bias4[16];
+          if constexpr (EPI != BT_EPI_NONE && !STREAMK) {
+            const float4* b4 = reinterpret_cast<const float4*>(p.bias + col);
+#pragma unroll
+            for (int q = 0; q < 16; ++q) bias4[q] = __ldg(b4 + q);
+          }
           if (p.dbg != 7) {
             ptx::tmem_ld32(taddr + c, r0);
             ptx::tmem_ld32(taddr + c + 32, r1);
@@ -494,9 +505,8 @@ __global__ void __launch_bounds__(GemmCfg<PAIR, BN, EW>::THREADS, 1)
             add_partial32(v1, src + 8 * 32);
           }
           uint32_t pk[32];
-          const int col = nb * BN + c;
-          epi_math32<EPI>(v0, p, row, col, row_ok, pk);
-          epi_math32<EPI>(v1, p, row, col + 32, row_ok, pk + 16);
+          epi_math32<EPI>(v0, p, row, col, row_ok, pk, STREAMK ? nullptr : bias4);
+          epi_math32<EPI>(v1, p, row, col + 32, row_ok, pk + 16, STREAMK ? nullptr : bias4 + 8);
           if (p.dbg == 6) {  // debug: everything but the output store
             if (pk[0] == 0x12345678u && pk[31] == 0x9abcdef0u) p.C[row] = __float2bfloat16(0.f);
             continue;
