@@ -90,6 +90,12 @@ class ClockSampler:
                  "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self._t = threading.Thread(target=self._read, daemon=True)
             self._t.start()
+            # let nvidia-smi finish starting up (NVML init) before the timed
+            # region opens: its start-up, not its 100 ms sampling, is what can
+            # stall the GPU for milliseconds
+            t_end = time.monotonic() + 3.0
+            while not self.lines and time.monotonic() < t_end:
+                time.sleep(0.01)
         except (OSError, FileNotFoundError):
             self.proc = None
         return self
@@ -350,6 +356,12 @@ def run_ours(args, wl):
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(dev) as clk:
+        # two untimed steps queued right ahead of the timed ones: the GPU sat
+        # idle while the sampler started, and the first step after an idle
+        # period pays the clock ramp (measured: +0.4..13 ms on step 0 at C3)
+        for _ in range(2):
+            flush_l2()
+            run()
         for i in range(args.steps):
             flush_l2()  # evict L2 between timed steps (outside the events)
             evs[i][0].record(stream)
@@ -358,7 +370,12 @@ def run_ours(args, wl):
         torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
-    ms_local = sum(a.elapsed_time(b) for a, b in evs)
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    ms_local = sum(step_ms)
+    log(f"[bench] step ms min {min(step_ms):.4f} median {sorted(step_ms)[len(step_ms) // 2]:.4f} "
+        f"max {max(step_ms):.4f} (step {step_ms.index(max(step_ms))})")
+    if os.environ.get("BT_BENCH_STEPS_LOG"):
+        log("[bench] steps " + " ".join(f"{v:.3f}" for v in step_ms))
     ms_t = torch.tensor([ms_local], dtype=torch.float64, device="cuda" if backend == "nccl" else "cpu")
     if dist is not None:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
