@@ -196,7 +196,7 @@ def time_kernels(torch, bt, eng, shard_seqs, x_dev, reps: int = 30):
     lf = harness.layer_flops(shard_seqs.lengths, k, cfg.ffn_scale)
 
     fused_ln0 = bool(_lib.load().bt_fused_attn_out_ln(T, k))  # what the forward runs for this shape
-    sched = torch.empty(2 * bs, dtype=torch.int32, device="cuda")
+    sched = torch.empty(_lib.load().bt_plan_sched_bytes(bs, mx) // 4 + 1, dtype=torch.int32, device="cuda")
     _lib.call("bt_plan_sched", plan.seq_starts_dev.data_ptr(), bs, mx, sched.data_ptr(), _lib.stream_ptr())
     from paper_2210_03052_b200.fusion import gemm_ln_device
 

@@ -126,9 +126,13 @@ BT_API int bt_mha_padded(const void* qkv, const int32_t* seq_starts, int bs, int
 BT_API int bt_ln_bias_residual(const void* x, const void* residual, const float* bias, const float* gamma,
                         const float* beta, float eps, void* out, int T, int k, bt_stream_t stream);
 
-/* MHA work schedule for a plan: sched[bs] int2 (start row, length) of the sequences ordered by
- * descending 128-key block count, so the fused MHA dispatches the longest problems first. */
+/* MHA work schedule for a plan, in a device buffer of bt_plan_sched_bytes(bs, mx) bytes:
+ * sched[bs] int2 (start row, length) of the sequences ordered by descending 128-key block count,
+ * so the fused MHA dispatches the longest problems first, followed by the same order's list of
+ * 128-row query-tile units (and a claim queue) that the MHA's tile-list mode walks for launches of
+ * many waves. */
 BT_API int bt_plan_sched(const int32_t* seq_starts, int bs, int mx, void* sched, bt_stream_t stream);
+BT_API size_t bt_plan_sched_bytes(int bs, int mx);
 /* bt_mha_varlen with the CTA order of a bt_plan_sched schedule (what bt_encoder_forward runs). */
 BT_API int bt_mha_varlen_sched(const void* qkv, const int32_t* seq_starts, const void* sched, int bs, int mx, int H,
                                int d, int cutoff, void* out, int T, bt_stream_t stream);
@@ -231,6 +235,13 @@ BT_API int bt_debug_gemm_mode(int mode);
 BT_API int bt_debug_forward_events(void** events, int n);
 /* Test hook: query tiles per fused-MHA CTA (0 = automatic: 4 for launches of many waves, else 1). */
 BT_API int bt_debug_mha_qg(int qg);
+/* Test hook: the MHA's tile-list mode (bt_mha_varlen_sched / the forward): 0 off,
+ * 1 automatic (launches of many waves), 2 always, -1 the
+ * BT_MHA_LIST environment policy; grid > 0 pins the number of CTAs walking the list. */
+BT_API int bt_debug_mha_list(int mode, int grid);
+/* Debug hook: resident CTAs per SM of an MHA variant (0 short/2 blocks, 1 short/3 blocks, 2 long,
+ * 3 multi-tile long); info[3] (optional) receives registers, static and max dynamic smem. */
+BT_API int bt_debug_mha_occupancy(int which, int* info);
 /* Debug hook: per-CTA globaltimer event trace of the MHA kernels (32 u64 slots per CTA). */
 BT_API int bt_debug_mha_trace(unsigned long long* buf);
 

@@ -62,6 +62,7 @@ SIGNATURES = {
     "bt_gemm_bias_residual_ln": (_I, [_P, _P, _P, _P, _P, _P, _F, _P, _I, _I, _I, _S]),
     "bt_fused_attn_out_ln": (_I, [_I, _I]),
     "bt_plan_sched": (_I, [_P, _I, _I, _P, _S]),
+    "bt_plan_sched_bytes": (_SZ, [_I, _I]),
     "bt_mha_varlen_sched": (_I, [_P, _P, _P, _I, _I, _I, _I, _I, _P, _I, _S]),
     "bt_layer_workspace_bytes": (_SZ, [C.POINTER(LayerCfgC), _I]),
     "bt_encoder_layer": (_I, [C.POINTER(LayerWeightsC), C.POINTER(LayerCfgC), _P, _I, _I, _P, _P, _SZ, _S]),
@@ -78,6 +79,8 @@ SIGNATURES = {
     "bt_debug_gemm_mode": (_I, [_I]),
     "bt_debug_mha_trace": (_I, [_P]),
     "bt_debug_mha_qg": (_I, [_I]),
+    "bt_debug_mha_list": (_I, [_I, _I]),
+    "bt_debug_mha_occupancy": (_I, [_I, _P]),
     "bt_debug_forward_events": (_I, [_P, _I]),
     "bt_mha_varlen_path": (_I, [_P, _P, _I, _I, _I, _I, _P, _I, _I, _S]),
 }

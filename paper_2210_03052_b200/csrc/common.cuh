@@ -62,6 +62,14 @@ inline cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t 
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
+// bt_plan_sched buffer: int2 sched[bs] (sequences, longest first), then at
+// sched_units_offset(bs) int nunits, int queue[2] (the MHA tile-list
+// claim counter and finished-CTA count, zeroed here, reset by the MHA), pad; then int2 units[bs * ceil(mx/128)]
+// (query-tile units {start row, qt << 20 | length}, longest sequences first).
+inline size_t sched_units_offset(int bs) { return (static_cast<size_t>(bs) * 8 + 15) / 16 * 16; }
+inline size_t sched_bytes(int bs, int mx) {
+  return sched_units_offset(bs) + 16 + static_cast<size_t>(bs) * ((mx + 127) / 128) * 8;
+}
 }  // namespace bt
 
 // Validate a condition on the host before any launch; returns `code`.

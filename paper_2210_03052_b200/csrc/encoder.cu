@@ -163,7 +163,8 @@ extern "C" size_t bt_forward_workspace_bytes(const bt_layer_cfg* cfg, int bs, in
   if (!cfg) return 0;
   const int k = cfg->head_num * cfg->head_size;
   const size_t t = static_cast<size_t>(T < 1 ? 1 : T);
-  return bt::align_up((bs + 1) * sizeof(int32_t)) + bt::align_up(bs * 8) + bt::align_up(t * sizeof(int32_t)) +
+  return bt::align_up((bs + 1) * sizeof(int32_t)) + bt::align_up(bt::sched_bytes(bs, cfg->max_seq_len)) +
+         bt::align_up(t * sizeof(int32_t)) +
          bt::align_up(t * k * 2) + bt_layer_workspace_bytes(cfg, T);
 }
 
@@ -181,7 +182,7 @@ extern "C" int bt_encoder_forward(const bt_layer_weights* layers, int n_layers, 
   auto* seq_starts = reinterpret_cast<int32_t*>(p);
   p += bt::align_up((bs + 1) * sizeof(int32_t));
   void* sched = p;
-  p += bt::align_up(bs * 8);
+  p += bt::align_up(bt::sched_bytes(bs, mx));
   auto* offsets = reinterpret_cast<int32_t*>(p);
   p += bt::align_up(static_cast<size_t>(T) * sizeof(int32_t));
   void* x = p;
@@ -227,7 +228,7 @@ extern "C" int bt_encoder_forward_packed(const bt_layer_weights* layers, int n_l
   auto* seq_starts = reinterpret_cast<int32_t*>(p);
   p += bt::align_up((bs + 1) * sizeof(int32_t));
   void* sched = p;
-  p += bt::align_up(bs * 8);
+  p += bt::align_up(bt::sched_bytes(bs, mx));
   p += bt::align_up(static_cast<size_t>(T) * sizeof(int32_t));  // offsets (unused: input already packed)
   void* x = p;
   p += bt::align_up(static_cast<size_t>(T) * k * 2);

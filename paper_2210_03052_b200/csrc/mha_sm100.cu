@@ -11,6 +11,7 @@
 //
 // Q/K/V biases are already applied by the QKV GEMM epilogue.  d = 64.
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -49,7 +50,26 @@ struct MhaParams {
   int mx;          // max_seq_len (row stride of a sequence in the padded layout)
   int qg;          // query tiles per CTA (kernels with a separate output staging tile)
   const int2* sched;  // optional (packed layout): CTA z -> (start row, length), longest first
+  // optional (LOOP kernels, packed layout): the tile list of bt_plan_sched --
+  // *nunits query-tile units {start row, qt << 20 | length}, longest
+  // sequences first; item i = (unit i / H, head i % H).  CTA c of the 1-D grid
+  // starts on item c and then claims items G, G+1, ... from queue[0] as it
+  // nears the end of each tile (greedy longest-first list scheduling);
+  // queue[1] counts finished CTAs, the last one resets both to 0.
+  const int2* units;
+  const int* nunits;
+  int* queue;
+  int heads;
 };
+
+// One query tile of work: rows [s0 + q0, s0 + min(q0 + 128, len)) of head h,
+// keys [s0, s0 + len).
+struct MhaTile {
+  int s0, len, h, q0;
+};
+
+// Tile-list ring entry: (tile ordinal & 0xFF) << 24 | item (0xFFFFFF: none left).
+constexpr uint32_t MHA_RING_NONE = 0xFFFFFFu;
 
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
@@ -124,29 +144,45 @@ template <bool RESIDENT, int NST, bool MULTI>
 __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_constant__ CUtensorMap tm,
                                                                  const MhaParams p) {
   using Cfg = MhaCfg<RESIDENT, NST, MULTI>;
-  const int h = blockIdx.y, b = blockIdx.z;
-  int sb, len;
-  if (p.sched) {  // longest problems first (plan_sched_kernel)
-    const int2 e = __ldg(p.sched + b);
-    sb = e.x;
-    len = e.y;
+  const bool list = Cfg::LOOP && p.units != nullptr;  // tile list with a claim queue (grid-uniform)
+  int h = blockIdx.y, b = blockIdx.z;
+  int sb = 0, len = 0, qt0 = 0, nqt = 0, nitems = 0;
+  if (list) {
+    nitems = __ldg(p.nunits) * p.heads;
+    if (static_cast<int>(blockIdx.x) >= nitems) return;  // CTA-uniform: fewer items than CTAs
+    nqt = 0x7FFFFFFF;  // tiles come from the queue until it runs dry
   } else {
-    sb = __ldg(p.seq_starts + b);
-    len = __ldg(p.seq_starts + b + 1) - sb;
+    if (p.sched) {  // longest problems first (plan_sched_kernel)
+      const int2 e = __ldg(p.sched + b);
+      sb = e.x;
+      len = e.y;
+    } else {
+      sb = __ldg(p.seq_starts + b);
+      len = __ldg(p.seq_starts + b + 1) - sb;
+    }
   }
   // Packed layout: the sequence's rows start at seq_starts[b] and only its
   // len rows / keys are touched.  Padded layout (the reference's unfused
   // baseline): rows start at b*mx and the whole mx x mx rectangle is
   // computed, keys >= len masked out of the softmax (exp -> 0, the -1e9 mask
   // of attention.py:162-163) and query rows >= len written as zeros.
-  const int s0 = p.padded ? b * p.mx : sb;
-  const int work = p.padded ? p.mx : len;
-  // this CTA's query tiles: qt0, qt0 + 1, ... (p.qg per CTA when Cfg::LOOP)
-  const int qg = Cfg::LOOP ? p.qg : 1;
-  const int qt0 = blockIdx.x * qg;
-  if (qt0 * MHA_QT >= work) return;  // CTA-uniform: past the sequence
-  const int nqt = Cfg::LOOP ? min(qg, (work + MHA_QT - 1) / MHA_QT - qt0) : 1;
-  const int nkb = (work + MHA_KB - 1) / MHA_KB;
+  const int cta_s0 = p.padded ? b * p.mx : sb;
+  const int cta_work = p.padded ? p.mx : len;
+  if (!list) {
+    // this CTA's query tiles: qt0, qt0 + 1, ... (p.qg per CTA when Cfg::LOOP)
+    const int qg = Cfg::LOOP ? p.qg : 1;
+    qt0 = blockIdx.x * qg;
+    if (qt0 * MHA_QT >= cta_work) return;  // CTA-uniform: past the sequence
+    nqt = Cfg::LOOP ? min(qg, (cta_work + MHA_QT - 1) / MHA_QT - qt0) : 1;
+  }
+  // tile-list item -> query tile (len 0: none left)
+  auto tile_of = [&](uint32_t item) -> MhaTile {
+    if (item == MHA_RING_NONE) return MhaTile{0, 0, 0, 0};
+    const int i = static_cast<int>(item);
+    const int u = i / p.heads;
+    const int2 e = __ldg(p.units + u);
+    return MhaTile{e.x, e.y & 0xFFFFF, i - u * p.heads, (e.y >> 20) * MHA_QT};
+  };
 
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sQ = smem + Cfg::Q_OFF;
@@ -165,6 +201,17 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
   uint64_t* q_empty = v_full + NST;       // the tile's last S MMA has read Q
   uint64_t* o_free = q_empty + 1;         // the softmax warps have read O (next tile may overwrite it)
   uint32_t* holder = reinterpret_cast<uint32_t*>(o_free + 1);
+  volatile uint32_t* ring = holder + 1;  // [4] tile-list items of tiles t (slot t & 3), tagged with t
+  // the t-th query tile of this CTA (tile list: wait for the producer's entry)
+  auto tile_at = [&](int t) -> MhaTile {
+    if (list) {
+      uint32_t v;
+      while (((v = ring[t & 3]) >> 24) != (static_cast<uint32_t>(t) & 0xFFu)) {
+      }
+      return tile_of(v & 0xFFFFFFu);
+    }
+    return MhaTile{cta_s0, cta_work, h, (qt0 + t) * MHA_QT};
+  };
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -181,6 +228,7 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
     ptx::mbar_init(pv_done, 1);
     ptx::mbar_init(q_empty, 1);
     ptx::mbar_init(o_free, 256);
+    for (int i = 0; i < 4; ++i) ring[i] = 0xFFFFFFFFu;  // tag 0xFF: no tile yet
     ptx::fence_mbar_init();
   }
   if (warp == 0) {
@@ -205,6 +253,7 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
     ptx::griddep_wait();  // qkv is produced by the previous kernel
     // K blocks on their own barriers ahead of V: S(j) = Q K(j)^T can start
     // before V(j) (needed only by P(j) V(j)) has landed
+    int s0 = 0;
     auto load_k = [&](int j, int slot) {
       if (ptx::elect_one()) {
         ptx::mbar_arrive_expect_tx(&kv_full[slot], MHA_TILE);
@@ -222,10 +271,34 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
     };
     int kvg = 0;  // K/V blocks loaded so far (ring position across query tiles)
     for (int t = 0; t < nqt; ++t) {
-      if (t > 0) ptx::mbar_wait(q_empty, (t - 1) & 1);  // the previous tile's S MMAs are done with sQ
+      MhaTile it;
+      if (list) {
+        // claim the next item once the softmax has finished the previous
+        // tile's exponentials (its P V and store remain, ~the Q load + first
+        // S of the next tile): greedy list scheduling without claiming work
+        // long before this CTA can start it
+        uint32_t item = blockIdx.x;
+        if (t > 0) {
+          ptx::mbar_wait(p_full, (kvg - 1) & 1);  // kvg = blocks of the previous tiles
+          ptx::mbar_wait(q_empty, (t - 1) & 1);
+          if (lane == 0) item = gridDim.x + atomicAdd(p.queue, 1);
+          item = __shfl_sync(0xffffffffu, item, 0);
+          if (item >= static_cast<uint32_t>(nitems)) item = MHA_RING_NONE;
+        }
+        if (lane == 0) ring[t & 3] = (static_cast<uint32_t>(t) & 0xFFu) << 24 | item;
+        __syncwarp();
+        if (item == MHA_RING_NONE) break;
+        it = tile_of(item);
+      } else {
+        if (t > 0) ptx::mbar_wait(q_empty, (t - 1) & 1);  // the previous tile's S MMAs are done with sQ
+        it = tile_at(t);
+      }
+      s0 = it.s0;
+      h = it.h;
+      const int nkb = (it.len + MHA_KB - 1) / MHA_KB;
       if (ptx::elect_one()) {
         ptx::mbar_arrive_expect_tx(q_full, MHA_TILE);
-        ptx::tma_load_2d(sQ, &tm, q_full, h * MHA_D, s0 + (qt0 + t) * MHA_QT);
+        ptx::tma_load_2d(sQ, &tm, q_full, h * MHA_D, s0 + it.q0);
       }
       __syncwarp();
       if (RESIDENT) {
@@ -248,7 +321,7 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
     constexpr uint32_t idesc_o = ptx::idesc_bf16(128, MHA_D, false, true);    // P (TMEM, K-major) x V (MN-major)
     const uint64_t q_desc = ptx::sdesc_sw128(ptx::smem_u32(sQ), 1024, 16);
     const uint32_t kv_base = ptx::smem_u32(sKV);
-    auto issue_pv = [&](int g, int jt, int t, int pslot, uint32_t kvpar) {
+    auto issue_pv = [&](int g, int jt, int t, int pslot, uint32_t kvpar, int work) {
       // O (+)= P(g) V(g): item g is block jt of query tile t; only the
       // k-steps that hold keys of the problem
       ptx::mbar_wait(&v_full[pslot], kvpar);
@@ -267,9 +340,12 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
       __syncwarp();
     };
     int g = 0, kvg = 0;  // items issued (S), K/V ring position
-    int prev_jt = 0, prev_t = 0, prev_slot = 0;
+    int prev_jt = 0, prev_t = 0, prev_slot = 0, prev_work = 0;
     uint32_t prev_par = 0;
     for (int t = 0; t < nqt; ++t) {
+      const int work = tile_at(t).len;
+      if (work == 0) break;  // tile list ran dry
+      const int nkb = (work + MHA_KB - 1) / MHA_KB;
       ptx::mbar_wait(q_full, t & 1);
       if (lane == 0 && t == 0) MHA_TRACE(1);
       for (int j = 0; j < nkb; ++j, ++g, ++kvg) {
@@ -287,14 +363,15 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
           if (j == nkb - 1) ptx::mma_commit(q_empty);  // this tile's Q is no longer read
         }
         __syncwarp();
-        if (g > 0) issue_pv(g - 1, prev_jt, prev_t, prev_slot, prev_par);
+        if (g > 0) issue_pv(g - 1, prev_jt, prev_t, prev_slot, prev_par, prev_work);
         prev_jt = j;
         prev_t = t;
         prev_slot = slot;
         prev_par = par;
+        prev_work = work;
       }
     }
-    issue_pv(g - 1, prev_jt, prev_t, prev_slot, prev_par);
+    issue_pv(g - 1, prev_jt, prev_t, prev_slot, prev_par, prev_work);
   }
   } else {
     ptx::setmaxnreg_inc<MHA_REGS_SOFTMAX>();  // warpgroups 0-1: softmax
@@ -314,7 +391,11 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
     const float sl2 = p.sl2;
     int g = 0;  // items consumed, across query tiles
     for (int t = 0; t < nqt; ++t) {
-    const int q0 = (qt0 + t) * MHA_QT;
+    const MhaTile it = tile_at(t);
+    if (it.len == 0) break;  // tile list ran dry
+    const int q0 = it.q0, s0 = it.s0, work = it.len, hh = it.h;
+    if (list) len = it.len;
+    const int nkb = (work + MHA_KB - 1) / MHA_KB;
     const bool warp_live = q0 + quarter * 32 < work;
     float mref = -INFINITY, lsum = 0.f;
     for (int j = 0; j < nkb; ++j, ++g) {
@@ -468,12 +549,13 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
         const int jj = lane & 7;
         if (q0 + rr < work) {
           const uint4 v = *reinterpret_cast<const uint4*>(sOut + rr * 128 + ((jj ^ (rr & 7)) << 4));
-          *reinterpret_cast<uint4*>(p.out + static_cast<size_t>(s0 + q0 + rr) * p.hidden + h * MHA_D + jj * 8) = v;
+          *reinterpret_cast<uint4*>(p.out + static_cast<size_t>(s0 + q0 + rr) * p.hidden + hh * MHA_D + jj * 8) = v;
         }
       }
-      if (t + 1 < nqt) named_bar_sync(pair_bar, 64);  // the pair's rows are stored: sOut free for the next tile
+      if (list || t + 1 < nqt) named_bar_sync(pair_bar, 64);  // the pair's rows are stored: sOut free for the next tile
     }
-    if (t + 1 < nqt) {
+    if (threadIdx.x == 0 && (t == 1 || t == 2)) MHA_TRACE(27 + t);  // tiles 1, 2 stored (slots 28, 29)
+    if (list || t + 1 < nqt) {
       ptx::tc_fence_before();
       ptx::mbar_arrive(o_free);  // O of this tile has been read: the next tile's first P V may overwrite it
     }
@@ -487,11 +569,25 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, 256);
   }
+  if (list && threadIdx.x == 0) {
+    // every claim of this CTA precedes this point; the last CTA resets the
+    // queue for the next launch
+    const int participants = min(static_cast<int>(gridDim.x), nitems);
+    __threadfence();
+    if (atomicAdd(p.queue + 1, 1) == participants - 1) {
+      p.queue[0] = 0;
+      p.queue[1] = 0;
+      __threadfence();
+    }
+  }
 }
 
 template <typename K>
 static int set_smem(K kern, size_t bytes) {
   BT_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
+  // two CTAs per SM: the multi-tile kernels need 2 x 99 KB, more than the
+  // default carveout leaves for shared memory
+  BT_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   return BT_OK;
 }
 
@@ -506,6 +602,20 @@ static int mha_qtiles_per_cta(int nqt, bool many_waves) {
   }
   const int qg = g_mha_qg_override ? g_mha_qg_override : forced ? forced : (many_waves ? 4 : 1);
   return qg < nqt ? qg : nqt;
+}
+
+// Tile-list policy: BT_MHA_LIST=0 disables it (A/B measurement);
+// bt_debug_mha_list overrides (0 off, 1 automatic, 2 always) and can pin the
+// grid size (tests: many claims per CTA on a small batch).
+static int g_mha_list_mode = -1, g_mha_list_grid = 0;
+static int mha_list_mode() {
+  if (g_mha_list_mode >= 0) return g_mha_list_mode;
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("BT_MHA_LIST");
+    env = (e && e[0] == '0') ? 0 : 1;
+  }
+  return env;
 }
 
 int mha_launch(const void* qkv, const int32_t* seq_starts, int bs, int mx, int H, int d, int cutoff, int T,
@@ -524,6 +634,10 @@ int mha_launch(const void* qkv, const int32_t* seq_starts, int bs, int mx, int H
   p.mx = mx;
   p.sched = padded ? nullptr : static_cast<const int2*>(sched);
   p.qg = 1;
+  p.units = nullptr;
+  p.nunits = nullptr;
+  p.queue = nullptr;
+  p.heads = H;
   BT_REQUIRE(!padded || T == bs * mx, BT_ESHAPE, "padded mha: qkv must have bs*mx = %d rows, got %d", bs * mx, T);
   const int nqt = (mx + MHA_QT - 1) / MHA_QT;
   // dispatch_mha rule (attention.py:309-314); the resident (short) kernel
@@ -538,6 +652,46 @@ int mha_launch(const void* qkv, const int32_t* seq_starts, int bs, int mx, int H
   // longer per-CTA chain would cost more than that saves, so one tile per CTA.
   const int sms = num_sms() > 0 ? num_sms() : 148;
   const long long ctas1 = static_cast<long long>(nqt) * H * bs;
+  // Tile list (bt_plan_sched's units): for launches of many waves a fixed
+  // grid of slot-many CTAs (2 per SM) claims query tiles longest-first from a
+  // queue; each CTA's next Q load overlaps its previous tile's output store
+  // and the per-CTA set-up is paid once.  Measured at C5 (BERT-large, 2048 x
+  // 512): 2806 vs 2917 us per launch against 4 consecutive tiles per CTA.
+  // Few waves (C2, C3) keep one tile per CTA: there the multi-tile kernel's
+  // longer per-tile chain (its issuer warps spill at 32 registers) costs more
+  // than the balance gains (C2 13.9 vs 10.7 us, C3 26.6 vs 26.1 us).
+  const int list_mode = mha_list_mode();
+  if (p.sched && list_mode > 0) {
+    static int slots = 0;
+    if (slots == 0) {
+      // resident CTAs per SM from the resources themselves: the occupancy
+      // API reports 1 for these kernels (measured), while two run per SM
+      // (per-CTA traces: 296 CTAs start within 1.2 us)
+      BT_TRY(set_smem(mha_fwd_kernel<false, 2, true>, MhaCfg<false, 2, true>::SMEM));
+      cudaFuncAttributes fa;
+      BT_CUDA_CHECK(cudaFuncGetAttributes(&fa, mha_fwd_kernel<false, 2, true>));
+      int dev = 0, sm_smem = 0, rsv = 0, sm_regs = 0;
+      BT_CUDA_CHECK(cudaGetDevice(&dev));
+      BT_CUDA_CHECK(cudaDeviceGetAttribute(&sm_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
+      BT_CUDA_CHECK(cudaDeviceGetAttribute(&rsv, cudaDevAttrReservedSharedMemoryPerBlock, dev));
+      BT_CUDA_CHECK(cudaDeviceGetAttribute(&sm_regs, cudaDevAttrMaxRegistersPerMultiprocessor, dev));
+      const int by_smem = sm_smem / static_cast<int>(MhaCfg<false, 2, true>::SMEM + rsv);
+      const int by_regs = sm_regs / (MHA_THREADS * (fa.numRegs > 0 ? fa.numRegs : 80));
+      const int by_tmem = 512 / 256;
+      const int per_sm = std::min(std::min(by_smem, by_regs), by_tmem);
+      BT_REQUIRE(per_sm >= 1, BT_ECUDA, "mha: the tile-list kernel does not fit on an SM");
+      slots = per_sm * sms;
+    }
+    const int grid = g_mha_list_grid > 0 ? g_mha_list_grid : slots;
+    if (ctas1 > 16LL * slots || list_mode == 2) {
+      p.nunits = reinterpret_cast<const int*>(static_cast<const uint8_t*>(sched) + sched_units_offset(bs));
+      p.units = reinterpret_cast<const int2*>(p.nunits + 4);
+      p.queue = const_cast<int*>(p.nunits + 1);
+      BT_LAUNCH((mha_fwd_kernel<false, 2, true>), dim3(grid), dim3(MHA_THREADS), MhaCfg<false, 2, true>::SMEM, s, 1,
+                tm, p);
+      return BT_OK;
+    }
+  }
   const int qg = mha_qtiles_per_cta(nqt, ctas1 > 16LL * 2 * sms);
   p.qg = qg;
   const dim3 grid_multi((nqt + qg - 1) / qg, H, bs), grid_one(nqt, H, bs);
@@ -576,6 +730,15 @@ extern "C" int bt_debug_mha_qg(int qg) {
   return BT_OK;
 }
 
+// Test hook: tile-list mode (0 off, 1 automatic, 2 always, -1 back
+// to the BT_MHA_LIST policy) and its grid size (0 = the resident CTA slots).
+extern "C" int bt_debug_mha_list(int mode, int grid) {
+  BT_REQUIRE(mode >= -1 && mode <= 2 && grid >= 0, BT_ECONFIG, "bt_debug_mha_list: mode -1..2, grid >= 0");
+  bt::g_mha_list_mode = mode;
+  bt::g_mha_list_grid = grid;
+  return BT_OK;
+}
+
 extern "C" int bt_debug_mha_trace(unsigned long long* buf) {
   BT_CUDA_CHECK(cudaMemcpyToSymbol(bt::g_mha_trace, &buf, sizeof(buf)));
   return BT_OK;
@@ -601,4 +764,30 @@ extern "C" int bt_mha_padded(const void* qkv, const int32_t* seq_starts, int bs,
 extern "C" int bt_mha_varlen_path(const void* qkv, const int32_t* seq_starts, int bs, int mx, int H, int d,
                                   void* out, int T, int path, bt_stream_t stream) {
   return bt::mha_launch(qkv, seq_starts, bs, mx, H, d, 384, T, out, path, bt::as_stream(stream), 0, nullptr);
+}
+
+// Debug hook: resident CTAs per SM of the MHA variants (0: short NST 2,
+// 1: short NST 3, 2: long, 3: multi-tile long); -1 on error.  Also writes
+// regs / static smem / max dynamic smem of the variant into info[3].
+extern "C" int bt_debug_mha_occupancy(int which, int* info) {
+  auto probe = [&](auto kern, size_t smem) -> int {
+    if (bt::set_smem(kern, smem) != BT_OK) return -1;
+    cudaFuncAttributes a;
+    if (cudaFuncGetAttributes(&a, kern) != cudaSuccess) return -1;
+    if (info) {
+      info[0] = a.numRegs;
+      info[1] = static_cast<int>(a.sharedSizeBytes);
+      info[2] = a.maxDynamicSharedSizeBytes;
+    }
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, bt::MHA_THREADS, smem) != cudaSuccess) return -1;
+    return n;
+  };
+  switch (which) {
+    case 0: return probe(bt::mha_fwd_kernel<true, 2, false>, bt::MhaCfg<true, 2, false>::SMEM);
+    case 1: return probe(bt::mha_fwd_kernel<true, 3, false>, bt::MhaCfg<true, 3, false>::SMEM);
+    case 2: return probe(bt::mha_fwd_kernel<false, 2, false>, bt::MhaCfg<false, 2, false>::SMEM);
+    case 3: return probe(bt::mha_fwd_kernel<false, 2, true>, bt::MhaCfg<false, 2, true>::SMEM);
+    default: return -1;
+  }
 }

@@ -327,8 +327,14 @@ namespace bt {
 // at no extra load latency per CTA.  One CTA.
 constexpr int SCHED_MAX_BUCKETS = 1024;
 __global__ void __launch_bounds__(1024) plan_sched_kernel(const int32_t* __restrict__ seq_starts, int bs, int nbk,
-                                                           int2* __restrict__ sched) {
+                                                           int2* __restrict__ sched, int* __restrict__ nunits,
+                                                           int2* __restrict__ units) {
+  // counting sort by key-block count (bucket 0 = the most blocks); a
+  // sequence of nb blocks has nb query tiles, so a bucket's tile units are
+  // contiguous: unit_base[bucket] + rank * nb
   __shared__ int cnt[SCHED_MAX_BUCKETS];
+  __shared__ int ubase[SCHED_MAX_BUCKETS];
+  __shared__ int bstart[SCHED_MAX_BUCKETS];
   ptx::griddep_launch_dependents();
   ptx::griddep_wait();
   for (int i = threadIdx.x; i < nbk; i += blockDim.x) cnt[i] = 0;
@@ -339,17 +345,28 @@ __global__ void __launch_bounds__(1024) plan_sched_kernel(const int32_t* __restr
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    int run = 0;
+    int run = 0, urun = 0;
     for (int i = 0; i < nbk; ++i) {
       const int c = cnt[i];
       cnt[i] = run;
+      bstart[i] = run;
+      ubase[i] = urun;
       run += c;
+      urun += c * (nbk - i);
     }
+    nunits[0] = urun;
+    nunits[1] = 0;  // the MHA tile-list queue: next item, finished CTAs
+    nunits[2] = 0;
   }
   __syncthreads();
   for (int i = threadIdx.x; i < bs; i += blockDim.x) {
     const int st = seq_starts[i], len = seq_starts[i + 1] - st;
-    sched[atomicAdd(&cnt[min(nbk - 1, max(0, nbk - (len + 127) / 128))], 1)] = make_int2(st, len);
+    const int bk = min(nbk - 1, max(0, nbk - (len + 127) / 128));
+    const int pos = atomicAdd(&cnt[bk], 1);
+    sched[pos] = make_int2(st, len);
+    const int nb = nbk - bk;
+    int2* u = units + ubase[bk] + (pos - bstart[bk]) * nb;
+    for (int q = 0; q < nb; ++q) u[q] = make_int2(st, (q << 20) | len);
   }
 }
 }  // namespace bt
@@ -397,10 +414,15 @@ int bt_plan_sched(const int32_t* seq_starts, int bs, int mx, void* sched, bt_str
   BT_REQUIRE(bs >= 1 && mx >= 1 && seq_starts && sched, BT_ESHAPE, "plan_sched: bad arguments");
   const int nbk = (mx + 127) / 128;
   BT_REQUIRE(nbk <= SCHED_MAX_BUCKETS, BT_ESHAPE, "plan_sched: max_seq_len %d too large", mx);
+  BT_REQUIRE((mx + 127) / 128 < 2048 && mx < (1 << 20), BT_ESHAPE, "plan_sched: max_seq_len %d too large", mx);
+  uint8_t* base = static_cast<uint8_t*>(sched);
+  int* nunits = reinterpret_cast<int*>(base + sched_units_offset(bs));
   BT_LAUNCH(plan_sched_kernel, dim3(1), dim3(1024), 0, as_stream(stream), 1, seq_starts, bs, nbk,
-            static_cast<int2*>(sched));
+            static_cast<int2*>(sched), nunits, reinterpret_cast<int2*>(nunits + 4));
   return BT_OK;
 }
+
+size_t bt_plan_sched_bytes(int bs, int mx) { return bs >= 1 && mx >= 1 ? sched_bytes(bs, mx) : 0; }
 
 int bt_pack(const void* padded, int in_dtype, const int32_t* offsets, int T, int k, void* packed, int out_dtype,
             bt_stream_t stream) {

@@ -26,6 +26,8 @@ def main():
         mha_device(qkv, plan, H, 64)
     nq = (mx + 127) // 128
     n = nq * H * bs
+    if len(sys.argv) > 2 and sys.argv[2] == "list":
+        return trace_list(torch, np, _lib, plan, qkv, seqs, bs, mx, H, n)
     buf = torch.zeros(n * 32, dtype=torch.int64, device="cuda")
     _lib.call("bt_debug_mha_trace", buf.data_ptr())
     mha_device(qkv, plan, H, 64)
@@ -71,6 +73,45 @@ def main():
     fin = [(t[c, 31] - t[c, 30]) / 1e3 for c in np.nonzero(used)[0]]
     print(f"O ready -> stored median {np.median(fin):.2f} us")
 
+
+def trace_list(torch, np, _lib, plan, qkv, seqs, bs, mx, H, n):
+    """Balanced tile-list mode (bt_mha_varlen_sched, forced): per-CTA start,
+    per-tile store times (slots 24..29), end."""
+    T = plan.valid_word_cnt
+    sched = torch.zeros(_lib.load().bt_plan_sched_bytes(bs, mx) // 4 + 1, dtype=torch.int32, device="cuda")
+    _lib.call("bt_plan_sched", plan.seq_starts_dev.data_ptr(), bs, mx, sched.data_ptr(), _lib.stream_ptr())
+    out = torch.empty(T, H * 64, device="cuda", dtype=torch.bfloat16)
+    mode = int(sys.argv[3]) if len(sys.argv) > 3 else 2
+
+    def go():
+        _lib.call("bt_mha_varlen_sched", qkv.data_ptr(), plan.seq_starts_dev.data_ptr(), sched.data_ptr(), bs, mx, H,
+                  64, 384, out.data_ptr(), T, _lib.stream_ptr())
+
+    _lib.call("bt_debug_mha_list", mode, 0)
+    for _ in range(2000):
+        go()
+    buf = torch.zeros(n * 32, dtype=torch.int64, device="cuda")
+    _lib.call("bt_debug_mha_trace", buf.data_ptr())
+    go()
+    torch.cuda.synchronize()
+    _lib.call("bt_debug_mha_trace", 0)
+    _lib.call("bt_debug_mha_list", -1, 0)
+    t = buf.view(n, 32).cpu().numpy()
+    used = np.nonzero(t[:, 0] > 0)[0]
+    t0 = t[used, 0].min()
+    r = lambda x: (x - t0) / 1e3  # noqa: E731
+    ends = r(t[used, 31])
+    print(f"list mode {mode}: CTAs {len(used)}; start {r(t[used, 0]).min():.2f}..{r(t[used, 0]).max():.2f} us; "
+          f"end {ends.min():.2f}..{ends.max():.2f} us (median {np.median(ends):.2f})")
+    # slots 28, 29: tiles 1 and 2 stored
+    k = 1 + (t[used, 28] > 0) + (t[used, 29] > 0)
+    for nt in sorted(set(k.tolist())):
+        cs = used[k == nt]
+        print(f"  {len(cs)} CTAs with {nt}{'+' if nt == 3 else ''} tiles: end median {np.median(r(t[cs, 31])):.2f} us, "
+              f"tile 1 {np.median((t[cs, 28] - t[cs, 0]) / 1e3) if nt > 1 else 0:.2f} us after start")
+    for c in list(used[:3]) + list(used[-3:]):
+        print(f"  cta {c}: start {r(t[c, 0]):.2f} Q {r(t[c, 1]):.2f} S0 {r(t[c, 2]):.2f} tiles 1,2 stored "
+              + " ".join(f"{r(x):.2f}" for x in t[c, 28:30] if x > 0) + f" end {r(t[c, 31]):.2f}")
 
 if __name__ == "__main__":
     main()

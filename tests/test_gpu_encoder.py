@@ -167,3 +167,31 @@ def test_forward_thread_safe():
     assert not errs, errs
     for o in outs:
         assert np.array_equal(o, ref)
+
+
+@pytest.mark.gpu
+def test_forward_mha_tile_list_bitwise():
+    """The forward with the MHA's tile-list mode forced (every layer's MHA a
+    small fixed grid claiming tiles from the queue, which each launch must
+    leave reset for the next) equals the default forward bit for bit."""
+    import paper_2210_03052_b200 as bt
+    from oracle import packbert_np as orc
+    from paper_2210_03052_b200 import _lib
+
+    lens = [300, 7, 512, 129, 1, 256]
+    cfg = bt.preset_config("bert_base", len(lens), 512, bt.OptFlags.all_on(), layers=3)
+    x = orc.gen_input(lens, 512, 768, seed=5)
+    seqs = bt.SeqLengths.of(lens, 512)
+    _lib.call("bt_debug_mha_list", 0, 0)
+    try:
+        # a fresh weights object per mode: each gets its own engine, so the
+        # forward's cached CUDA graph is captured under that mode
+        ref = bt.forward(bt.init_weights(cfg, seed=5), seqs, bt.Tensor(x), cfg).array
+        for grid in (5, 0):
+            _lib.call("bt_debug_mha_list", 2, grid)
+            w = bt.init_weights(cfg, seed=5)
+            for _ in range(3):
+                out = bt.forward(w, seqs, bt.Tensor(x), cfg).array
+                assert np.array_equal(out, ref), f"grid {grid}"
+    finally:
+        _lib.call("bt_debug_mha_list", -1, 0)

@@ -308,17 +308,61 @@ def test_mha_sched_order_is_result_neutral(env):
     plan = bt.plan_for_lengths(bt.SeqLengths.of(lens, mx))
     T = plan.valid_word_cnt
     qkv = _rand_qkv(torch, T, H * 64, seed=5)
-    sched = torch.empty(2 * len(lens), dtype=torch.int32, device="cuda")
+    nbytes = _lib.load().bt_plan_sched_bytes(len(lens), mx)
+    sched = torch.zeros(nbytes // 4, dtype=torch.int32, device="cuda")
     _lib.call("bt_plan_sched", plan.seq_starts_dev.data_ptr(), len(lens), mx, sched.data_ptr(), _lib.stream_ptr())
     out = torch.empty(T, H * 64, device="cuda", dtype=torch.bfloat16)
     _lib.call("bt_mha_varlen_sched", qkv.data_ptr(), plan.seq_starts_dev.data_ptr(), sched.data_ptr(), len(lens), mx,
               H, 64, 384, out.data_ptr(), T, _lib.stream_ptr())
     ref = mha_device(qkv, plan, H, 64)
     assert torch.equal(out, ref)
-    pairs = sched.view(-1, 2).cpu().numpy()
+    pairs = sched[:2 * len(lens)].view(-1, 2).cpu().numpy()
     starts = plan.seq_starts
     assert sorted(map(tuple, pairs)) == sorted((int(starts[b]), lens[b]) for b in range(len(lens)))
     blocks = [(l + 127) // 128 for _, l in pairs]
+    assert blocks == sorted(blocks, reverse=True)
+
+
+@pytest.mark.parametrize("grid", [0, 1, 3, 7, 64])
+@pytest.mark.parametrize("lens,mx", [([5, 300, 129, 1, 512, 128, 257, 77], 512), ([256, 140, 9, 255, 1, 2], 256),
+                                     ([1000, 3, 700, 129], 1024)])
+def test_mha_tile_list(env, lens, mx, grid):
+    """The tile-list MHA (a fixed grid claims bt_plan_sched's query tiles x
+    heads longest-first from a queue; what the forward runs for launches of
+    many waves) is bitwise the one-tile-per-CTA kernel,
+    for any grid size -- one CTA walking everything, fewer CTAs than heads,
+    more CTAs than items -- and the unit list covers every query tile once,
+    longest sequences first."""
+    bt, torch = env
+    from paper_2210_03052_b200 import _lib
+    from paper_2210_03052_b200.attention import mha_device
+
+    H = 3
+    plan = bt.plan_for_lengths(bt.SeqLengths.of(lens, mx))
+    T = plan.valid_word_cnt
+    qkv = _rand_qkv(torch, T, H * 64, seed=11)
+    nbytes = _lib.load().bt_plan_sched_bytes(len(lens), mx)
+    sched = torch.full((nbytes // 4,), -1, dtype=torch.int32, device="cuda")
+    _lib.call("bt_plan_sched", plan.seq_starts_dev.data_ptr(), len(lens), mx, sched.data_ptr(), _lib.stream_ptr())
+    out = torch.full((T, H * 64), float("nan"), device="cuda", dtype=torch.bfloat16)
+    _lib.call("bt_debug_mha_list", 2, grid)
+    try:
+        _lib.call("bt_mha_varlen_sched", qkv.data_ptr(), plan.seq_starts_dev.data_ptr(), sched.data_ptr(), len(lens),
+                  mx, H, 64, 384, out.data_ptr(), T, _lib.stream_ptr())
+    finally:
+        _lib.call("bt_debug_mha_list", -1, 0)
+    torch.cuda.synchronize()
+    ref = mha_device(qkv, plan, H, 64)
+    assert torch.equal(out, ref)
+    # unit list: every (sequence, query tile) once, descending key blocks
+    off = (2 * len(lens) * 4 + 15) // 16 * 4
+    n = int(sched[off].item())
+    units = sched[off + 4: off + 4 + 2 * n].view(-1, 2).cpu().numpy()
+    starts = plan.seq_starts
+    want = sorted((int(starts[b]), q, lens[b]) for b in range(len(lens)) for q in range((lens[b] + 127) // 128))
+    got = sorted((int(s0), int(w) >> 20, int(w) & 0xFFFFF) for s0, w in units)
+    assert got == want
+    blocks = [((int(w) & 0xFFFFF) + 127) // 128 for _, w in units]
     assert blocks == sorted(blocks, reverse=True)
 
 
