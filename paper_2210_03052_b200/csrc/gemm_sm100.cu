@@ -724,9 +724,9 @@ static int gemm_run(const void* A, const void* Bt, const float* bias, const void
   }
   switch (ch.bn) {
     case 64: return dispatch_sk<1, 64, 4>(ch.streamk, epi, ta, tb, tc, p, units, s);
-    case 128: return dispatch_sk<1, 128, 4>(ch.streamk, epi, ta, tb, tc, p, units, s);
-    case 192: return dispatch_sk<1, 192, 4>(ch.streamk, epi, ta, tb, tc, p, units, s);
-    case 256: return dispatch_sk<1, 256, 4>(ch.streamk, epi, ta, tb, tc, p, units, s);
+    case 128: return dispatch_sk<1, 128, 8>(ch.streamk, epi, ta, tb, tc, p, units, s);
+    case 192: return dispatch_sk<1, 192, 8>(ch.streamk, epi, ta, tb, tc, p, units, s);
+    case 256: return dispatch_sk<1, 256, 8>(ch.streamk, epi, ta, tb, tc, p, units, s);
     default: BT_REQUIRE(false, BT_ECONFIG, "gemm: tile width %d unsupported", ch.bn);
   }
   return BT_OK;
