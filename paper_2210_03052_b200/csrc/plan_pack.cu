@@ -328,7 +328,8 @@ namespace bt {
 constexpr int SCHED_MAX_BUCKETS = 1024;
 __global__ void __launch_bounds__(1024) plan_sched_kernel(const int32_t* __restrict__ seq_starts, int bs, int nbk,
                                                            int2* __restrict__ sched, int* __restrict__ nunits,
-                                                           int2* __restrict__ units) {
+                                                           int2* __restrict__ units, int* __restrict__ nsegs,
+                                                           int4* __restrict__ segs) {
   // counting sort by key-block count (bucket 0 = the most blocks); a
   // sequence of nb blocks has nb query tiles, so a bucket's tile units are
   // contiguous: unit_base[bucket] + rank * nb
@@ -367,6 +368,39 @@ __global__ void __launch_bounds__(1024) plan_sched_kernel(const int32_t* __restr
     const int nb = nbk - bk;
     int2* u = units + ubase[bk] + (pos - bstart[bk]) * nb;
     for (int q = 0; q < nb; ++q) u[q] = make_int2(st, (q << 20) | len);
+  }
+  // MHA segments (short batches): the query tiles of sequences longer than
+  // 128 rows, then groups of adjacent sequences of <= 128 rows whose rows
+  // fit one 128-row tile together (one key block; each row masked to its own
+  // sequence).  One thread, over seq_starts staged in shared memory.
+  if (segs != nullptr) {
+    __shared__ int ss[SEG_MAX_BS + 1];
+    for (int i = threadIdx.x; i <= bs; i += blockDim.x) ss[i] = seq_starts[i];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int n = 0;
+      for (int i = 0; i < bs; ++i) {
+        const int st = ss[i], en = ss[i + 1];
+        if (en - st <= 128) continue;
+        for (int q = st; q < en; q += 128) {
+          segs[2 * n] = make_int4(st, en, q, min(en, q + 128));
+          segs[2 * n + 1] = make_int4(i, i, 0, 0);
+          ++n;
+        }
+      }
+      int g0 = -1;
+      for (int i = 0; i <= bs; ++i) {
+        const bool shortseq = i < bs && ss[i + 1] - ss[i] <= 128;
+        if (g0 >= 0 && (!shortseq || ss[i + 1] - ss[g0] > 128)) {  // close the open group [g0, i)
+          segs[2 * n] = make_int4(ss[g0], ss[i], ss[g0], ss[i]);
+          segs[2 * n + 1] = make_int4(g0, i - 1, 0, 0);
+          ++n;
+          g0 = -1;
+        }
+        if (shortseq && g0 < 0) g0 = i;
+      }
+      *nsegs = n;
+    }
   }
 }
 }  // namespace bt
@@ -418,7 +452,10 @@ int bt_plan_sched(const int32_t* seq_starts, int bs, int mx, void* sched, bt_str
   uint8_t* base = static_cast<uint8_t*>(sched);
   int* nunits = reinterpret_cast<int*>(base + sched_units_offset(bs));
   BT_LAUNCH(plan_sched_kernel, dim3(1), dim3(1024), 0, as_stream(stream), 1, seq_starts, bs, nbk,
-            static_cast<int2*>(sched), nunits, reinterpret_cast<int2*>(nunits + 4));
+            static_cast<int2*>(sched), nunits, reinterpret_cast<int2*>(nunits + 4),
+            reinterpret_cast<int*>(base + sched_wins_offset(bs, mx)),
+            bs <= SEG_MAX_BS && mx <= SEG_MAX_MX ? reinterpret_cast<int4*>(base + sched_wins_offset(bs, mx) + 16)
+                                                 : nullptr);
   return BT_OK;
 }
 

@@ -28,6 +28,8 @@ def main():
     n = nq * H * bs
     if len(sys.argv) > 2 and sys.argv[2] == "list":
         return trace_list(torch, np, _lib, plan, qkv, seqs, bs, mx, H, n)
+    if len(sys.argv) > 2 and sys.argv[2] == "win":
+        return trace_win(torch, np, _lib, plan, qkv, bs, mx, H)
     buf = torch.zeros(n * 32, dtype=torch.int64, device="cuda")
     _lib.call("bt_debug_mha_trace", buf.data_ptr())
     mha_device(qkv, plan, H, 64)
@@ -112,6 +114,50 @@ def trace_list(torch, np, _lib, plan, qkv, seqs, bs, mx, H, n):
     for c in list(used[:3]) + list(used[-3:]):
         print(f"  cta {c}: start {r(t[c, 0]):.2f} Q {r(t[c, 1]):.2f} S0 {r(t[c, 2]):.2f} tiles 1,2 stored "
               + " ".join(f"{r(x):.2f}" for x in t[c, 28:30] if x > 0) + f" end {r(t[c, 31]):.2f}")
+
+def trace_win(torch, np, _lib, plan, qkv, bs, mx, H):
+    """Segment kernel (forced): per-CTA start, S-ready / softmax-done per key
+    block, output stored."""
+    T = plan.valid_word_cnt
+    sched = torch.zeros(_lib.load().bt_plan_sched_bytes(bs, mx) // 4 + 1, dtype=torch.int32, device="cuda")
+    _lib.call("bt_plan_sched", plan.seq_starts_dev.data_ptr(), bs, mx, sched.data_ptr(), _lib.stream_ptr())
+    out = torch.empty(T, H * 64, device="cuda", dtype=torch.bfloat16)
+
+    def go():
+        _lib.call("bt_mha_varlen_sched", qkv.data_ptr(), plan.seq_starts_dev.data_ptr(), sched.data_ptr(), bs, mx, H,
+                  64, 384, out.data_ptr(), T, _lib.stream_ptr())
+
+    _lib.call("bt_debug_mha_win", 2)
+    for _ in range(2000):
+        go()
+    n = bs * ((mx + 127) // 128) * H  # grid (H, bs * ceil(mx / 128)); CTAs past the item list exit
+    buf = torch.zeros(n * 32, dtype=torch.int64, device="cuda")
+    _lib.call("bt_debug_mha_trace", buf.data_ptr())
+    go()
+    torch.cuda.synchronize()
+    _lib.call("bt_debug_mha_trace", 0)
+    _lib.call("bt_debug_mha_win", -1)
+    t = buf.view(n, 32).cpu().numpy()
+    used = np.nonzero(t[:, 0] > 0)[0]
+    t0 = t[used, 0].min()
+    r = lambda x: (x - t0) / 1e3  # noqa: E731
+    ends = r(t[used, 31])
+    nblk = np.array([sum(1 for i in range(7) if t[c, 2 + 2 * i] > 0) for c in used])
+    print(f"segment kernel: CTAs {len(used)} of {n}; start {r(t[used, 0]).min():.2f}..{r(t[used, 0]).max():.2f} us; "
+          f"end {ends.min():.2f}..{ends.max():.2f} (median {np.median(ends):.2f}); key blocks per CTA "
+          f"{dict(zip(*np.unique(nblk, return_counts=True)))}")
+    for k in sorted(set(nblk.tolist())):
+        cs = used[nblk == k]
+        print(f"  {len(cs)} CTAs with {k} blocks: duration median {np.median((t[cs, 31] - t[cs, 0]) / 1e3):.2f} us")
+    for c in list(used[:2]) + list(used[-2:]):
+        row = t[c]
+        s = f"  cta {c}: start {r(row[0]):.2f} Q {r(row[1]):.2f} |"
+        for i in range(7):
+            if row[2 + 2 * i] == 0:
+                break
+            s += f" S{i} {r(row[2 + 2 * i]):.2f}-{r(row[3 + 2 * i]):.2f}"
+        print(s + f" | O {r(row[30]):.2f} st {r(row[31]):.2f}")
+
 
 if __name__ == "__main__":
     main()

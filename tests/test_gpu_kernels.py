@@ -346,11 +346,13 @@ def test_mha_tile_list(env, lens, mx, grid):
     _lib.call("bt_plan_sched", plan.seq_starts_dev.data_ptr(), len(lens), mx, sched.data_ptr(), _lib.stream_ptr())
     out = torch.full((T, H * 64), float("nan"), device="cuda", dtype=torch.bfloat16)
     _lib.call("bt_debug_mha_list", 2, grid)
+    _lib.call("bt_debug_mha_win", 0)
     try:
         _lib.call("bt_mha_varlen_sched", qkv.data_ptr(), plan.seq_starts_dev.data_ptr(), sched.data_ptr(), len(lens),
                   mx, H, 64, 384, out.data_ptr(), T, _lib.stream_ptr())
     finally:
         _lib.call("bt_debug_mha_list", -1, 0)
+        _lib.call("bt_debug_mha_win", -1)
     torch.cuda.synchronize()
     ref = mha_device(qkv, plan, H, 64)
     assert torch.equal(out, ref)
@@ -386,3 +388,75 @@ def test_mha_query_tiles_per_cta(env, lens, mx):
             assert torch.equal(mha_device(qkv, plan, 2, 64), one), f"qg={qg}"
     finally:
         _lib.call("bt_debug_mha_qg", 0)
+
+
+def _mha_sched_call(bt, torch, qkv, plan, heads, mx, cutoff=384):
+    from paper_2210_03052_b200 import _lib
+
+    bs = plan.batch_size
+    T = plan.valid_word_cnt
+    sched = torch.full((_lib.load().bt_plan_sched_bytes(bs, mx) // 4,), -1, dtype=torch.int32, device="cuda")
+    _lib.call("bt_plan_sched", plan.seq_starts_dev.data_ptr(), bs, mx, sched.data_ptr(), _lib.stream_ptr())
+    out = torch.full((T, heads * 64), float("nan"), device="cuda", dtype=torch.bfloat16)
+    _lib.call("bt_mha_varlen_sched", qkv.data_ptr(), plan.seq_starts_dev.data_ptr(), sched.data_ptr(), bs, mx, heads,
+              64, cutoff, out.data_ptr(), T, _lib.stream_ptr())
+    torch.cuda.synchronize()
+    return out
+
+
+@pytest.mark.parametrize("lens,mx", [([1, 2, 3, 127, 128, 129, 200, 256], 256), ([5] * 40, 8),
+                                     ([1] * 250 + [64, 250], 256), ([100, 28, 128, 1, 127, 129, 60], 256),
+                                     ([244, 190, 157, 96, 105, 36, 45, 30, 70, 234, 192, 256, 154, 181, 256, 212], 256),
+                                     ([64] * 200, 64)])
+def test_mha_segment_kernel(env, lens, mx):
+    """The segment kernel (query tiles of sequences > 128 rows, and groups of
+    adjacent short sequences sharing one 128-row tile with each row masked
+    to its own sequence -- what the forward runs for bs, max_seq_len <= 256)
+    vs the fp32 oracle: groups of hundreds of 1-token sequences, exact
+    128-row groups, the C2 batch."""
+    bt, torch = env
+    from paper_2210_03052_b200 import _lib
+
+    heads = 3
+    plan = bt.plan_for_lengths(bt.SeqLengths.of(lens, mx))
+    qkv = _rand_qkv(torch, plan.valid_word_cnt, heads * 64, seed=len(lens) + 3)
+    _lib.call("bt_debug_mha_win", 2)
+    try:
+        out = _mha_sched_call(bt, torch, qkv, plan, heads, mx)
+    finally:
+        _lib.call("bt_debug_mha_win", -1)
+    assert torch.isfinite(out.float()).all()
+    ref = _oracle_mha(qkv, plan, heads, mx)
+    assert_close_bf16(out, ref, what=f"segments {lens[:4]}")
+
+
+def test_mha_segment_kernel_isolation_and_rescale(env):
+    """Segment kernel: a sequence's output does not depend on its window
+    neighbours (perturbing every other sequence's q/k/v leaves it bitwise
+    unchanged), and a late jump of the row max (keys 128.. scaled 4x) is
+    rescaled correctly."""
+    bt, torch = env
+    from paper_2210_03052_b200 import _lib
+
+    lens, mx, heads = [37, 200, 5, 256, 90, 1, 140], 256, 2
+    hid = heads * 64
+    plan = bt.plan_for_lengths(bt.SeqLengths.of(lens, mx))
+    qkv = _rand_qkv(torch, plan.valid_word_cnt, hid, seed=21)
+    s = plan.seq_starts
+    for b in range(len(lens)):
+        lo, hi = s[b] + 128, min(s[b] + 256, s[b + 1])
+        if hi > lo:
+            qkv[lo:hi, hid:2 * hid] *= 4
+    _lib.call("bt_debug_mha_win", 2)
+    try:
+        out = _mha_sched_call(bt, torch, qkv, plan, heads, mx)
+        ref = _oracle_mha(qkv, plan, heads, mx)
+        assert_close_bf16(out, ref, what="segments rescale")
+        pert = qkv.clone()
+        for b in range(len(lens)):
+            if b != 1:
+                pert[s[b]:s[b + 1]] = (torch.randn_like(pert[s[b]:s[b + 1]].float()) * 3).to(torch.bfloat16)
+        out2 = _mha_sched_call(bt, torch, pert, plan, heads, mx)
+    finally:
+        _lib.call("bt_debug_mha_win", -1)
+    assert torch.equal(out[s[1]:s[2]], out2[s[1]:s[2]])
