@@ -191,21 +191,24 @@ def time_kernels(torch, bt, eng, shard_seqs, x_dev, reps: int = 30):
     out = torch.empty_like(x)
     lengths_dev = torch.tensor(shard_seqs.lengths, dtype=torch.int32, device="cuda")
     starts = torch.empty(bs + 1, dtype=torch.int32, device="cuda")
-    offs = torch.empty(T, dtype=torch.int32, device="cuda")
     upad = torch.empty((bs * mx, k), dtype=torch.float32, device="cuda")
     lf = harness.layer_flops(shard_seqs.lengths, k, cfg.ffn_scale)
 
     fused_ln0 = bool(_lib.load().bt_fused_attn_out_ln(T, k))  # what the forward runs for this shape
     sched = torch.empty(_lib.load().bt_plan_sched_bytes(bs, mx) // 4 + 1, dtype=torch.int32, device="cuda")
     _lib.call("bt_plan_sched", plan.seq_starts_dev.data_ptr(), bs, mx, sched.data_ptr(), _lib.stream_ptr())
+    sched2 = torch.empty_like(sched)  # scratch schedule for timing bt_plan_forward
     from paper_2210_03052_b200.fusion import gemm_ln_device
 
     ops = {
-        "plan": (lambda: _lib.call("bt_plan_lengths", lengths_dev.data_ptr(), bs, mx, starts.data_ptr(),
-                                   offs.data_ptr(), _lib.stream_ptr()), 1, "hbm",
-                 harness.kernel_bytes("plan", T, k, bs, mx), 2),
-        "pack": (lambda: pack_device(x_dev, plan, out_dtype=torch.bfloat16), 1, "hbm",
-                 harness.kernel_bytes("pack", T, k), 1),
+        # the forward's plan: seq_starts + MHA schedule in one launch (bt_plan_forward)
+        "plan": (lambda: _lib.call("bt_plan_forward", lengths_dev.data_ptr(), bs, mx, starts.data_ptr(),
+                                   sched2.data_ptr(), _lib.stream_ptr()), 1, "hbm",
+                 harness.kernel_bytes("plan", T, k, bs, mx), 1),
+        # the forward's pack: fp32 padded -> bf16 packed rows addressed by seq_starts
+        "pack": (lambda: _lib.call("bt_pack_starts", x_dev.data_ptr(), plan.seq_starts_dev.data_ptr(), bs, mx, k,
+                                   x.data_ptr(), _lib.stream_ptr()), 1, "hbm",
+                 harness.kernel_bytes("pack", T, k, bs, mx), 1),
         "gemm_qkv": (lambda: gemm_device(x, L0.qkv_w, L0.qkv_b, None, _lib.EPI_BIAS, out=qkv), cfg.layers, "tensor",
                      lf["gemm0"], 1),
         # the forward's MHA launch: CTAs in the longest-first schedule of bt_plan_sched
@@ -482,7 +485,8 @@ def run_ours(args, wl):
             "clocks": clk.summary(),
         }
         # whole-step roofline floor: FLOPs at the tensor peak + memory-bound bytes at HBM peak
-        mem_bytes = (harness.kernel_bytes("pack", T, hidden) + harness.kernel_bytes("unpack", T, hidden, len(lens), mx)
+        mem_bytes = (harness.kernel_bytes("pack", T, hidden, len(lens), mx)
+                     + harness.kernel_bytes("unpack", T, hidden, len(lens), mx)
                      + 2 * layers * harness.kernel_bytes("ln", T, hidden))
         floor_s = step_flops / (peaks["bf16_tflops"] * 1e12) + mem_bytes / (peaks["hbm_gbs"] * 1e9)
         result["step_roofline_frac"] = round(floor_s / (ms_per_step / 1e3), 4)

@@ -133,6 +133,14 @@ BT_API int bt_ln_bias_residual(const void* x, const void* residual, const float*
  * many waves. */
 BT_API int bt_plan_sched(const int32_t* seq_starts, int bs, int mx, void* sched, bt_stream_t stream);
 BT_API size_t bt_plan_sched_bytes(int bs, int mx);
+/* What bt_encoder_forward runs: plan_for_lengths' seq_starts (packing.py:122) and the
+ * bt_plan_sched schedule in ONE single-CTA launch; sched holds bt_plan_sched_bytes(bs, mx). */
+BT_API int bt_plan_forward(const int32_t* lengths, int bs, int mx, int32_t* seq_starts, void* sched,
+                           bt_stream_t stream);
+/* pack (packing.py:141) of an fp32 padded batch [bs*mx, k] into bf16 packed rows [T, k], addressed
+ * by seq_starts instead of an offsets array (k % 8 == 0). */
+BT_API int bt_pack_starts(const float* padded, const int32_t* seq_starts, int bs, int mx, int k, void* packed_bf16,
+                          bt_stream_t stream);
 /* bt_mha_varlen with the CTA order of a bt_plan_sched schedule (what bt_encoder_forward runs). */
 BT_API int bt_mha_varlen_sched(const void* qkv, const int32_t* seq_starts, const void* sched, int bs, int mx, int H,
                                int d, int cutoff, void* out, int T, bt_stream_t stream);

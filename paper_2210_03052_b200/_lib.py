@@ -63,6 +63,8 @@ SIGNATURES = {
     "bt_fused_attn_out_ln": (_I, [_I, _I]),
     "bt_plan_sched": (_I, [_P, _I, _I, _P, _S]),
     "bt_plan_sched_bytes": (_SZ, [_I, _I]),
+    "bt_plan_forward": (_I, [_P, _I, _I, _P, _P, _S]),
+    "bt_pack_starts": (_I, [_P, _P, _I, _I, _I, _P, _S]),
     "bt_mha_varlen_sched": (_I, [_P, _P, _P, _I, _I, _I, _I, _I, _P, _I, _S]),
     "bt_layer_workspace_bytes": (_SZ, [C.POINTER(LayerCfgC), _I]),
     "bt_encoder_layer": (_I, [C.POINTER(LayerWeightsC), C.POINTER(LayerCfgC), _P, _I, _I, _P, _P, _SZ, _S]),

@@ -192,9 +192,15 @@ extern "C" int bt_encoder_forward(const bt_layer_weights* layers, int n_layers, 
 
   bt::g_fwd_event_idx = 0;
   BT_TRY(bt::mark(bt::as_stream(stream)));
-  BT_TRY(bt_plan_lengths(lengths, bs, mx, seq_starts, offsets, stream));
-  BT_TRY(bt_plan_sched(seq_starts, bs, mx, sched, stream));
-  BT_TRY(bt_pack(x_padded, BT_F32, offsets, T, k, x, BT_BF16, stream));
+  (void)offsets;  // the forward packs from seq_starts
+  if (k % 8 == 0) {
+    BT_TRY(bt_plan_forward(lengths, bs, mx, seq_starts, sched, stream));
+    BT_TRY(bt_pack_starts(x_padded, seq_starts, bs, mx, k, x, stream));
+  } else {
+    BT_TRY(bt_plan_lengths(lengths, bs, mx, seq_starts, offsets, stream));
+    BT_TRY(bt_plan_sched(seq_starts, bs, mx, sched, stream));
+    BT_TRY(bt_pack(x_padded, BT_F32, offsets, T, k, x, BT_BF16, stream));
+  }
   BT_TRY(bt::mark(bt::as_stream(stream)));
   for (int li = 0; li < n_layers; ++li)
     BT_TRY(bt::encoder_layer_impl(&layers[li], cfg, seq_starts, bs, T, x, lws, lws_bytes, stream, sched));
@@ -234,8 +240,7 @@ extern "C" int bt_encoder_forward_packed(const bt_layer_weights* layers, int n_l
   p += bt::align_up(static_cast<size_t>(T) * k * 2);
   void* lws = p;
   const size_t lws_bytes = bt_layer_workspace_bytes(cfg, T);
-  BT_TRY(bt_plan_lengths(lengths, bs, mx, seq_starts, nullptr, stream));
-  BT_TRY(bt_plan_sched(seq_starts, bs, mx, sched, stream));
+  BT_TRY(bt_plan_forward(lengths, bs, mx, seq_starts, sched, stream));
   BT_TRY(bt_bias_act(x_packed, BT_F32, k, nullptr, x, BT_BF16, k, T, k, 0, stream));  // fp32 -> bf16
   for (int li = 0; li < n_layers; ++li)
     BT_TRY(bt::encoder_layer_impl(&layers[li], cfg, seq_starts, bs, T, x, lws, lws_bytes, stream, sched));

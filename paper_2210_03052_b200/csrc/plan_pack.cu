@@ -87,13 +87,11 @@ __global__ void plan_rows_kernel(const uint8_t* __restrict__ mask, int bs, int m
 
 // Single-CTA exclusive scan of lengths -> seq_starts[bs+1] (+ total T).
 // 1024 threads, chunked over bs with a running carry.
-__global__ void __launch_bounds__(1024) plan_scan_kernel(const int32_t* __restrict__ lengths, int bs,
-                                                          int32_t* __restrict__ seq_starts,
-                                                          int32_t* __restrict__ valid_cnt) {
+__device__ __forceinline__ void plan_scan_body(const int32_t* __restrict__ lengths, int bs,
+                                               int32_t* __restrict__ seq_starts, int32_t* __restrict__ valid_cnt,
+                                               int32_t* sm_starts = nullptr) {
   __shared__ int32_t warp_sums[32];
   __shared__ int32_t carry_s;
-  ptx::griddep_launch_dependents();
-  ptx::griddep_wait();
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   if (tid == 0) carry_s = 0;
   __syncthreads();
@@ -118,15 +116,27 @@ __global__ void __launch_bounds__(1024) plan_scan_kernel(const int32_t* __restri
     __syncthreads();
     const int carry = carry_s;
     const int incl = x + (wid ? warp_sums[wid - 1] : 0) + carry;
-    if (i < bs) seq_starts[i] = incl - v;
+    if (i < bs) {
+      seq_starts[i] = incl - v;
+      if (sm_starts) sm_starts[i] = incl - v;
+    }
     __syncthreads();
     if (tid == 1023) carry_s = incl;
     __syncthreads();
   }
   if (tid == 0) {
     seq_starts[bs] = carry_s;
+    if (sm_starts) sm_starts[bs] = carry_s;
     if (valid_cnt) *valid_cnt = carry_s;
   }
+}
+
+__global__ void __launch_bounds__(1024) plan_scan_kernel(const int32_t* __restrict__ lengths, int bs,
+                                                          int32_t* __restrict__ seq_starts,
+                                                          int32_t* __restrict__ valid_cnt) {
+  ptx::griddep_launch_dependents();
+  ptx::griddep_wait();
+  plan_scan_body(lengths, bs, seq_starts, valid_cnt);
 }
 
 // offsets[seq_starts[b] + j] = b*mx + j for j < len[b]  (the flat indices of
@@ -326,18 +336,16 @@ namespace bt {
 // problems start in the first wave and the short ones fill the tail (LPT),
 // at no extra load latency per CTA.  One CTA.
 constexpr int SCHED_MAX_BUCKETS = 1024;
-__global__ void __launch_bounds__(1024) plan_sched_kernel(const int32_t* __restrict__ seq_starts, int bs, int nbk,
-                                                           int2* __restrict__ sched, int* __restrict__ nunits,
-                                                           int2* __restrict__ units, int* __restrict__ nsegs,
-                                                           int4* __restrict__ segs) {
+__device__ __forceinline__ void plan_sched_body(const int32_t* __restrict__ seq_starts, int bs, int nbk,
+                                                int2* __restrict__ sched, int* __restrict__ nunits,
+                                                int2* __restrict__ units, int* __restrict__ nsegs,
+                                                int4* __restrict__ segs) {
   // counting sort by key-block count (bucket 0 = the most blocks); a
   // sequence of nb blocks has nb query tiles, so a bucket's tile units are
   // contiguous: unit_base[bucket] + rank * nb
   __shared__ int cnt[SCHED_MAX_BUCKETS];
   __shared__ int ubase[SCHED_MAX_BUCKETS];
   __shared__ int bstart[SCHED_MAX_BUCKETS];
-  ptx::griddep_launch_dependents();
-  ptx::griddep_wait();
   for (int i = threadIdx.x; i < nbk; i += blockDim.x) cnt[i] = 0;
   __syncthreads();
   for (int i = threadIdx.x; i < bs; i += blockDim.x) {
@@ -403,6 +411,54 @@ __global__ void __launch_bounds__(1024) plan_sched_kernel(const int32_t* __restr
     }
   }
 }
+
+__global__ void __launch_bounds__(1024) plan_sched_kernel(const int32_t* __restrict__ seq_starts, int bs, int nbk,
+                                                           int2* __restrict__ sched, int* __restrict__ nunits,
+                                                           int2* __restrict__ units, int* __restrict__ nsegs,
+                                                           int4* __restrict__ segs) {
+  ptx::griddep_launch_dependents();
+  ptx::griddep_wait();
+  plan_sched_body(seq_starts, bs, nbk, sched, nunits, units, nsegs, segs);
+}
+
+constexpr int PLAN_SMEM_BS = 4096;
+// The forward's whole plan in one CTA: lengths -> seq_starts, then the MHA
+// schedule (what plan_scan_kernel + plan_sched_kernel do in two launches).
+__global__ void __launch_bounds__(1024) plan_forward_kernel(const int32_t* __restrict__ lengths, int bs, int nbk,
+                                                             int32_t* __restrict__ seq_starts,
+                                                             int2* __restrict__ sched, int* __restrict__ nunits,
+                                                             int2* __restrict__ units, int* __restrict__ nsegs,
+                                                             int4* __restrict__ segs) {
+  // seq_starts also kept in shared memory (bs <= PLAN_SMEM_BS) so the
+  // schedule reads no global memory
+  __shared__ int32_t sm_starts[PLAN_SMEM_BS + 1];
+  ptx::griddep_launch_dependents();
+  ptx::griddep_wait();
+  const bool in_smem = bs <= PLAN_SMEM_BS;
+  plan_scan_body(lengths, bs, seq_starts, nullptr, in_smem ? sm_starts : nullptr);
+  __syncthreads();  // seq_starts written by this CTA is visible to all its threads
+  plan_sched_body(in_smem ? sm_starts : seq_starts, bs, nbk, sched, nunits, units, nsegs, segs);
+}
+
+// Pack by sequence starts (no offsets array): padded row b*mx + j -> packed
+// row seq_starts[b] + j for j < len[b]; padded rows are skipped.
+template <typename Tin, typename Tout>
+__global__ void pack_starts_kernel(const Tin* __restrict__ padded, const int32_t* __restrict__ seq_starts, int bs,
+                                   int mx, int k, Tout* __restrict__ packed) {
+  ptx::griddep_launch_dependents();
+  ptx::griddep_wait();
+  const int chunks = k / 8;
+  const long long total = static_cast<long long>(bs) * mx * chunks;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long prow = i / chunks;
+    const int c = static_cast<int>(i - prow * chunks) * 8;
+    const int b = static_cast<int>(prow / mx);
+    const int j = static_cast<int>(prow - static_cast<long long>(b) * mx);
+    const int s0 = __ldg(seq_starts + b);
+    if (j < __ldg(seq_starts + b + 1) - s0) move8(padded + prow * k + c, packed + static_cast<long long>(s0 + j) * k + c);
+  }
+}
 }  // namespace bt
 
 extern "C" {
@@ -456,6 +512,33 @@ int bt_plan_sched(const int32_t* seq_starts, int bs, int mx, void* sched, bt_str
             reinterpret_cast<int*>(base + sched_wins_offset(bs, mx)),
             bs <= SEG_MAX_BS && mx <= SEG_MAX_MX ? reinterpret_cast<int4*>(base + sched_wins_offset(bs, mx) + 16)
                                                  : nullptr);
+  return BT_OK;
+}
+
+// The forward's plan (bt_encoder_forward): seq_starts + MHA schedule in one
+// launch, and the pack from seq_starts (no offsets array).
+int bt_plan_forward(const int32_t* lengths, int bs, int mx, int32_t* seq_starts, void* sched,
+                             bt_stream_t stream) {
+  BT_REQUIRE(bs >= 1 && mx >= 1 && lengths && seq_starts && sched, BT_ESHAPE, "plan_forward: bad arguments");
+  const int nbk = (mx + 127) / 128;
+  BT_REQUIRE(nbk <= SCHED_MAX_BUCKETS && mx < (1 << 20), BT_ESHAPE, "plan_forward: max_seq_len %d too large", mx);
+  uint8_t* base = static_cast<uint8_t*>(sched);
+  int* nunits = reinterpret_cast<int*>(base + sched_units_offset(bs));
+  BT_LAUNCH(plan_forward_kernel, dim3(1), dim3(1024), 0, as_stream(stream), 1, lengths, bs, nbk, seq_starts,
+            static_cast<int2*>(sched), nunits, reinterpret_cast<int2*>(nunits + 4),
+            reinterpret_cast<int*>(base + sched_wins_offset(bs, mx)),
+            bs <= SEG_MAX_BS && mx <= SEG_MAX_MX ? reinterpret_cast<int4*>(base + sched_wins_offset(bs, mx) + 16)
+                                                 : nullptr);
+  return BT_OK;
+}
+
+int bt_pack_starts(const float* padded, const int32_t* seq_starts, int bs, int mx, int k, void* packed_bf16,
+                            bt_stream_t stream) {
+  BT_REQUIRE(bs >= 1 && mx >= 1 && k >= 8 && k % 8 == 0, BT_ESHAPE, "pack_starts: bad shape");
+  const int threads = 256;
+  BT_LAUNCH((pack_starts_kernel<float, __nv_bfloat16>), dim3(grid_for(static_cast<long long>(bs) * mx * (k / 8), threads)),
+            dim3(threads), 0, as_stream(stream), 1, padded, seq_starts, bs, mx, k,
+            static_cast<__nv_bfloat16*>(packed_bf16));
   return BT_OK;
 }
 

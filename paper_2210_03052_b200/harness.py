@@ -75,10 +75,10 @@ def kernel_bytes(kind: str, T: int, k: int, bs: int = 0, mx: int = 0) -> int:
     (SURVEY.md section 8d): bf16 activations, fp32 padded I/O."""
     if kind == "ln":        # read x, read residual, write y (bf16)
         return 3 * T * k * 2
-    if kind == "pack":      # fp32 valid rows in, bf16 packed out, int32 offsets
-        return T * k * 4 + T * k * 2 + 4 * T
+    if kind == "pack":      # fp32 valid rows in, bf16 packed out, int32 seq_starts
+        return T * k * 4 + T * k * 2 + 4 * (bs + 1)
     if kind == "unpack":    # bf16 packed in, fp32 padded out (zeros included)
         return T * k * 2 + bs * mx * k * 4
-    if kind == "plan":
-        return bs * mx + 4 * T + 4 * (bs + 1)
+    if kind == "plan":      # int32 lengths in, seq_starts + (start, length) schedule out
+        return 4 * bs + 4 * (bs + 1) + 8 * bs
     raise ValueError(kind)

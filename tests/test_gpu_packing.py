@@ -106,3 +106,41 @@ def test_pack_bf16_and_round_trip_large(bt):
     assert torch.equal(up, ref)
     pk32 = pack_device(x, plan)
     assert torch.equal(unpack_device(pk32, plan)[idx], x[idx])
+
+
+@pytest.mark.parametrize("bs,mx", [(16, 256), (1, 1), (300, 64), (2048, 512), (7, 1000)])
+def test_forward_plan_and_pack_starts(bt, bs, mx):
+    """The forward's one-launch plan (bt_plan_forward) gives plan_for_lengths'
+    seq_starts bit for bit and the same MHA schedule as bt_plan_sched; the
+    seq_starts-addressed pack (bt_pack_starts) equals the offsets pack."""
+    import torch
+
+    from paper_2210_03052_b200 import _lib
+    from paper_2210_03052_b200.packing import pack_device
+
+    lens = orc.gen_lengths(bs, mx, "fixed", seed=bs, alpha=0.6)
+    seqs = bt.SeqLengths.of(lens, mx)
+    plan = bt.plan_for_lengths(seqs)
+    L = _lib.load()
+    nb = L.bt_plan_sched_bytes(bs, mx) // 4
+    sched_ref = torch.zeros(nb, dtype=torch.int32, device="cuda")
+    sched = torch.full((nb,), -7, dtype=torch.int32, device="cuda")
+    _lib.call("bt_plan_sched", plan.seq_starts_dev.data_ptr(), bs, mx, sched_ref.data_ptr(), _lib.stream_ptr())
+    lengths_dev = torch.tensor(list(lens), dtype=torch.int32, device="cuda")
+    starts = torch.full((bs + 1,), -1, dtype=torch.int32, device="cuda")
+    _lib.call("bt_plan_forward", lengths_dev.data_ptr(), bs, mx, starts.data_ptr(), sched.data_ptr(),
+              _lib.stream_ptr())
+    torch.cuda.synchronize()
+    assert np.array_equal(starts.cpu().numpy(), plan.seq_starts)
+    # sequence order within a key-block bucket is unspecified: compare as multisets
+    pairs = lambda t: sorted(map(tuple, t[:2 * bs].view(-1, 2).cpu().numpy().tolist()))  # noqa: E731
+    assert pairs(sched) == pairs(sched_ref)
+    off = (2 * bs * 4 + 15) // 16 * 4
+    assert sched[off].item() == sched_ref[off].item()  # unit count
+    k = 64
+    x = torch.randn(bs * mx, k, device="cuda")
+    out = torch.empty(plan.valid_word_cnt, k, dtype=torch.bfloat16, device="cuda")
+    _lib.call("bt_pack_starts", x.data_ptr(), plan.seq_starts_dev.data_ptr(), bs, mx, k, out.data_ptr(),
+              _lib.stream_ptr())
+    torch.cuda.synchronize()
+    assert torch.equal(out, pack_device(x, plan, out_dtype=torch.bfloat16))
