@@ -339,14 +339,25 @@ static int max_active_clusters() {
 
 // Whether the fused kernel applies (N = 128 * CL, CL in {4, 6, 8}) and its
 // row blocks fit one wave of clusters.
+// Row blocks allowed per resident cluster slot (BT_GEMM_LN_WAVES, default 1).
+static int gemm_ln_waves() {
+  static int w = -1;
+  if (w < 0) {
+    const char* e = getenv("BT_GEMM_LN_WAVES");
+    w = (e && e[0] >= '1' && e[0] <= '9') ? e[0] - '0' : 1;
+  }
+  return w;
+}
+
 bool gemm_ln_fits(int M, int N, int K) {
   if (N % GLN_BN || K % GLN_BK || K < GLN_BK) return false;
   const int cl = N / GLN_BN;
   const int rbs = (M + 127) / 128;
+  const int waves = gemm_ln_waves();
   switch (cl) {
-    case 4: return rbs <= max_active_clusters<4>();
-    case 6: return rbs <= max_active_clusters<6>();
-    case 8: return rbs <= max_active_clusters<8>();
+    case 4: return rbs <= waves * max_active_clusters<4>();
+    case 6: return rbs <= waves * max_active_clusters<6>();
+    case 8: return rbs <= waves * max_active_clusters<8>();
     default: return false;
   }
 }
