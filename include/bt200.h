@@ -249,8 +249,8 @@ BT_API int bt_debug_mha_qg(int qg);
 BT_API int bt_debug_mha_list(int mode, int grid);
 /* Test hook: the MHA's segment kernel (bt_mha_varlen_sched / the forward, batches of bs <= 256 and
  * max_seq_len <= 256: adjacent sequences of <= 128 rows share one CTA per head, rows masked to their
- * own sequence): 0 off, 1 or 2 on, -1 the BT_MHA_WIN environment policy (default on). */
-BT_API int bt_debug_mha_win(int mode);
+ * own sequence): 0 off, 1 or 2 on, -1 the BT_MHA_SEG environment policy (default on). */
+BT_API int bt_debug_mha_seg(int mode);
 /* Debug hook: resident CTAs per SM of an MHA variant (0 short/2 blocks, 1 short/3 blocks, 2 long,
  * 3 multi-tile long); info[3] (optional) receives registers, static and max dynamic smem. */
 BT_API int bt_debug_mha_occupancy(int which, int* info);

@@ -82,7 +82,7 @@ SIGNATURES = {
     "bt_debug_mha_trace": (_I, [_P]),
     "bt_debug_mha_qg": (_I, [_I]),
     "bt_debug_mha_list": (_I, [_I, _I]),
-    "bt_debug_mha_win": (_I, [_I]),
+    "bt_debug_mha_seg": (_I, [_I]),
     "bt_debug_mha_occupancy": (_I, [_I, _P]),
     "bt_debug_forward_events": (_I, [_P, _I]),
     "bt_mha_varlen_path": (_I, [_P, _P, _I, _I, _I, _I, _P, _I, _I, _S]),

@@ -66,17 +66,17 @@ inline cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t 
 // sched_units_offset(bs) int nunits, int queue[2] (the MHA tile-list
 // claim counter and finished-CTA count, zeroed here, reset by the MHA), pad; then int2 units[bs * ceil(mx/128)]
 // (query-tile units {start row, qt << 20 | length}, longest sequences first).
-// Then at sched_wins_offset(bs, mx) int nsegs (16 B) and int4 segs[2 *
+// Then at sched_segs_offset(bs, mx) int nsegs (16 B) and int4 segs[2 *
 // bs * ceil(mx/128)]: the MHA segment kernel's work items, two int4 each:
 // {first key row, key end row, first query row, query end row}, {first
 // sequence, last sequence, -, -} (written for bs <= 256, mx <= 256).
 constexpr int SEG_MAX_BS = 256, SEG_MAX_MX = 256;
 inline size_t sched_units_offset(int bs) { return (static_cast<size_t>(bs) * 8 + 15) / 16 * 16; }
-inline size_t sched_wins_offset(int bs, int mx) {
+inline size_t sched_segs_offset(int bs, int mx) {
   return sched_units_offset(bs) + 16 + (static_cast<size_t>(bs) * ((mx + 127) / 128) * 8 + 15) / 16 * 16;
 }
 inline size_t sched_bytes(int bs, int mx) {
-  return sched_wins_offset(bs, mx) + 16 + static_cast<size_t>(bs) * ((mx + 127) / 128) * 32;
+  return sched_segs_offset(bs, mx) + 16 + static_cast<size_t>(bs) * ((mx + 127) / 128) * 32;
 }
 }  // namespace bt
 

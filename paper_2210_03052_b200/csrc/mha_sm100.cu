@@ -120,7 +120,7 @@ __device__ __forceinline__ void reg_tie(uint32_t (&r)[32]) {
 // (they complete warpgroup 2 for setmaxnreg); both issuer warps walk their loops warp-uniformly and
 // issue through elect.sync.  TMEM: S [0,128), O [128,192) -> 256 columns;
 // ~112 KB smem -> two CTAs per SM, whose latency chains interleave.
-template <bool RESIDENT, int NST, bool MULTI, bool WIN = false>
+template <bool RESIDENT, int NST, bool MULTI, bool SEG = false>
 struct MhaCfg {
   // MULTI (NST == 2 only: no room next to 2 CTAs per SM otherwise): a
   // separate output staging tile, so a CTA can loop over several query tiles
@@ -146,21 +146,21 @@ constexpr int MHA_THREADS = 384;
 constexpr int MHA_REGS_ISSUE = 32;
 constexpr int MHA_REGS_SOFTMAX = 104;
 
-// WIN = true: the segment kernel.  A CTA (grid: head x item) takes one
+// SEG = true: the segment kernel.  A CTA (grid: head x item) takes one
 // bt_plan_sched segment: a query tile of a sequence longer than 128 rows,
 // or a group of adjacent short sequences whose rows fit one 128-row tile --
 // their keys are one block, each row masked to its own sequence.  Short
 // sequences then share CTAs instead of taking one each.
-template <bool RESIDENT, int NST, bool MULTI, bool WIN = false>
+template <bool RESIDENT, int NST, bool MULTI, bool SEG = false>
 __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_constant__ CUtensorMap tm,
                                                                  const MhaParams p) {
   using Cfg = MhaCfg<RESIDENT, NST, MULTI>;
   const bool list = Cfg::LOOP && p.units != nullptr;  // tile list with a claim queue (grid-uniform)
   int h = blockIdx.y, b = blockIdx.z;
   int sb = 0, len = 0, qt0 = 0, nqt = 0, nitems = 0;
-  int win_a = 0, win_b = 0;  // WIN: first / last sequence of the window
-  int seg_q = 0, seg_rows = 0;  // WIN: first query row, query rows
-  if (WIN) {
+  int seg_a = 0, seg_b = 0;  // SEG: first / last sequence of the segment
+  int seg_q = 0, seg_rows = 0;  // SEG: first query row, query rows
+  if (SEG) {
     if (static_cast<int>(blockIdx.y) >= __ldg(p.nsegs)) return;  // CTA-uniform: past the item list
     h = blockIdx.x;
     const int4 e = __ldg(p.segs + 2 * blockIdx.y), f = __ldg(p.segs + 2 * blockIdx.y + 1);
@@ -168,8 +168,8 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
     len = e.y - e.x;
     seg_q = e.z;
     seg_rows = e.w - e.z;
-    win_a = f.x;
-    win_b = f.y;
+    seg_a = f.x;
+    seg_b = f.y;
   } else if (list) {
     nitems = __ldg(p.nunits) * p.heads;
     if (static_cast<int>(blockIdx.x) >= nitems) return;  // CTA-uniform: fewer items than CTAs
@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
   // of attention.py:162-163) and query rows >= len written as zeros.
   const int cta_s0 = p.padded ? b * p.mx : sb;
   const int cta_work = p.padded ? p.mx : len;
-  if (WIN) {
+  if (SEG) {
     nqt = 1;
   } else if (!list) {
     // this CTA's query tiles: qt0, qt0 + 1, ... (p.qg per CTA when Cfg::LOOP)
@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
       }
       return tile_of(v & 0xFFFFFFu);
     }
-    if (WIN) return MhaTile{cta_s0, cta_work, h, seg_q - cta_s0};
+    if (SEG) return MhaTile{cta_s0, cta_work, h, seg_q - cta_s0};
     return MhaTile{cta_s0, cta_work, h, (qt0 + t) * MHA_QT};
   };
 
@@ -423,15 +423,15 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
     if (list) len = it.len;
     const int nkb = (work + MHA_KB - 1) / MHA_KB;
     // query rows of this tile that exist (sequence tiles: inside the
-    // sequence; windows: inside the packed batch)
-    const int rows_here = WIN ? seg_rows : work - q0;
+    // sequence; segments: the segment's rows)
+    const int rows_here = SEG ? seg_rows : work - q0;
     const bool warp_live = quarter * 32 < rows_here;
-    // WIN: my row's keys [ks, ke) relative to s0 (its own sequence)
+    // SEG: my row's keys [ks, ke) relative to s0 (its own sequence)
     int ks = 0, ke = len;
-    if (WIN && win_a < win_b) {  // a group of short sequences
+    if (SEG && seg_a < seg_b) {  // a group of short sequences
       const int r = s0 + q0 + row;
       if (row < rows_here) {
-        int lo = win_a, hi = win_b;
+        int lo = seg_a, hi = seg_b;
         while (lo < hi) {
           const int mid = (lo + hi + 1) >> 1;
           if (__ldg(p.seq_starts + mid) <= r) lo = mid; else hi = mid - 1;
@@ -445,9 +445,9 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
     float mref = -INFINITY, lsum = 0.f;
     for (int j = 0; j < nkb; ++j, ++g) {
       const int kvalid = min(MHA_KB, len - j * MHA_KB) - half * 64;  // valid keys among my 64 (may be <= 0)
-      // WIN: valid keys of my row among my 64 are [klo, khi)
-      const int klo = WIN ? ks - j * MHA_KB - half * 64 : 0;
-      const int khi = WIN ? min(ke - j * MHA_KB - half * 64, 64) : kvalid;
+      // SEG: valid keys of my row among my 64 are [klo, khi)
+      const int klo = SEG ? ks - j * MHA_KB - half * 64 : 0;
+      const int khi = SEG ? min(ke - j * MHA_KB - half * 64, 64) : kvalid;
       ptx::mbar_wait(s_full, g & 1);
       ptx::tc_fence_after();
       if (threadIdx.x == 0 && t == 0) MHA_TRACE(2 + 2 * j);
@@ -465,7 +465,7 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
       bool need = false;
       float mnew = mref, alpha = 1.f;
       if (warp_live) {
-        if (WIN) {
+        if (SEG) {
           if (klo > 0 || khi < 64) {
             // keys outside my row's sequence: s = -inf (out of the max; exp -> 0)
 #pragma unroll
@@ -510,9 +510,9 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
       }
       if (threadIdx.x == 0 && t == 0 && j < 3) MHA_TRACE(18 + 4 * j);
       if (warp_live) {
-        // (WIN: a row whose sequence has no key in the blocks so far keeps
+        // (SEG: a row whose sequence has no key in the blocks so far keeps
         // m_ref = -inf; its S are all -inf, so any finite offset gives P = 0)
-        const float msc = (WIN && mref == -INFINITY) ? 0.f : mref * sl2;
+        const float msc = (SEG && mref == -INFINITY) ? 0.f : mref * sl2;
         const unsigned long long sl2x2 = ptx::f2(sl2, sl2), nm2 = ptx::f2(-msc, -msc);
         unsigned long long sum4[4] = {0ull, 0ull, 0ull, 0ull};  // 4 independent add chains
         // P = 2^((s - m_ref) * scale * log2 e): BT_MHA_POLY of every 16 on the
@@ -583,7 +583,7 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
       named_bar_sync(pair_bar, 64);
       const float l = x[row] + x[128 + row];
       ptx::tmem_wait_ld(o);
-      const float inv = (WIN ? row < rows_here : q0 + row < len) ? 1.0f / l : 0.f;
+      const float inv = (SEG ? row < rows_here : q0 + row < len) ? 1.0f / l : 0.f;
       const unsigned long long inv2 = ptx::f2(inv, inv);
       uint8_t* mine = sOut + row * 128;
 #pragma unroll
@@ -666,14 +666,14 @@ static int mha_qtiles_per_cta(int nqt, bool many_waves) {
 // Tile-list policy: BT_MHA_LIST=0 disables it (A/B measurement);
 // bt_debug_mha_list overrides (0 off, 1 automatic, 2 always) and can pin the
 // grid size (tests: many claims per CTA on a small batch).
-static int g_mha_list_mode = -1, g_mha_list_grid = 0, g_mha_win_mode = -1;
+static int g_mha_list_mode = -1, g_mha_list_grid = 0, g_mha_seg_mode = -1;
 // Segment-kernel policy (batches of bs <= 256, max_seq_len <= 256):
-// BT_MHA_WIN=0 disables it; bt_debug_mha_win overrides (0 off, 1 / 2 on).
-static int mha_win_mode() {
-  if (g_mha_win_mode >= 0) return g_mha_win_mode;
+// BT_MHA_SEG=0 disables it; bt_debug_mha_seg overrides (0 off, 1 / 2 on).
+static int mha_seg_mode() {
+  if (g_mha_seg_mode >= 0) return g_mha_seg_mode;
   static int env = -1;
   if (env < 0) {
-    const char* e = getenv("BT_MHA_WIN");
+    const char* e = getenv("BT_MHA_SEG");
     env = (e && (e[0] == '0' || e[0] == '2')) ? e[0] - '0' : 1;
   }
   return env;
@@ -734,9 +734,9 @@ int mha_launch(const void* qkv, const int32_t* seq_starts, int bs, int mx, int H
   // longer per-tile chain (its issuer warps spill at 32 registers) costs more
   // than the balance gains (C2 13.9 vs 10.7 us, C3 26.6 vs 26.1 us).
   // Segment kernel (short batches): adjacent short sequences share a CTA
-  const int win_mode = mha_win_mode();
-  if (p.sched && win_mode > 0 && bs <= SEG_MAX_BS && mx <= SEG_MAX_MX) {
-    p.nsegs = reinterpret_cast<const int*>(static_cast<const uint8_t*>(sched) + sched_wins_offset(bs, mx));
+  const int seg_mode = mha_seg_mode();
+  if (p.sched && seg_mode > 0 && bs <= SEG_MAX_BS && mx <= SEG_MAX_MX) {
+    p.nsegs = reinterpret_cast<const int*>(static_cast<const uint8_t*>(sched) + sched_segs_offset(bs, mx));
     p.segs = reinterpret_cast<const int4*>(p.nsegs + 4);
     static bool set = false;
     if (!set) {
@@ -827,10 +827,10 @@ extern "C" int bt_debug_mha_list(int mode, int grid) {
 }
 
 // Test hook: the segment kernel (0 off, 1 / 2 on where it applies, -1 back to
-// the BT_MHA_WIN policy).
-extern "C" int bt_debug_mha_win(int mode) {
-  BT_REQUIRE(mode >= -1 && mode <= 2, BT_ECONFIG, "bt_debug_mha_win: mode -1..2");
-  bt::g_mha_win_mode = mode;
+// the BT_MHA_SEG policy).
+extern "C" int bt_debug_mha_seg(int mode) {
+  BT_REQUIRE(mode >= -1 && mode <= 2, BT_ECONFIG, "bt_debug_mha_seg: mode -1..2");
+  bt::g_mha_seg_mode = mode;
   return BT_OK;
 }
 

@@ -509,8 +509,8 @@ int bt_plan_sched(const int32_t* seq_starts, int bs, int mx, void* sched, bt_str
   int* nunits = reinterpret_cast<int*>(base + sched_units_offset(bs));
   BT_LAUNCH(plan_sched_kernel, dim3(1), dim3(1024), 0, as_stream(stream), 1, seq_starts, bs, nbk,
             static_cast<int2*>(sched), nunits, reinterpret_cast<int2*>(nunits + 4),
-            reinterpret_cast<int*>(base + sched_wins_offset(bs, mx)),
-            bs <= SEG_MAX_BS && mx <= SEG_MAX_MX ? reinterpret_cast<int4*>(base + sched_wins_offset(bs, mx) + 16)
+            reinterpret_cast<int*>(base + sched_segs_offset(bs, mx)),
+            bs <= SEG_MAX_BS && mx <= SEG_MAX_MX ? reinterpret_cast<int4*>(base + sched_segs_offset(bs, mx) + 16)
                                                  : nullptr);
   return BT_OK;
 }
@@ -526,8 +526,8 @@ int bt_plan_forward(const int32_t* lengths, int bs, int mx, int32_t* seq_starts,
   int* nunits = reinterpret_cast<int*>(base + sched_units_offset(bs));
   BT_LAUNCH(plan_forward_kernel, dim3(1), dim3(1024), 0, as_stream(stream), 1, lengths, bs, nbk, seq_starts,
             static_cast<int2*>(sched), nunits, reinterpret_cast<int2*>(nunits + 4),
-            reinterpret_cast<int*>(base + sched_wins_offset(bs, mx)),
-            bs <= SEG_MAX_BS && mx <= SEG_MAX_MX ? reinterpret_cast<int4*>(base + sched_wins_offset(bs, mx) + 16)
+            reinterpret_cast<int*>(base + sched_segs_offset(bs, mx)),
+            bs <= SEG_MAX_BS && mx <= SEG_MAX_MX ? reinterpret_cast<int4*>(base + sched_segs_offset(bs, mx) + 16)
                                                  : nullptr);
   return BT_OK;
 }

@@ -28,8 +28,8 @@ def main():
     n = nq * H * bs
     if len(sys.argv) > 2 and sys.argv[2] == "list":
         return trace_list(torch, np, _lib, plan, qkv, seqs, bs, mx, H, n)
-    if len(sys.argv) > 2 and sys.argv[2] == "win":
-        return trace_win(torch, np, _lib, plan, qkv, bs, mx, H)
+    if len(sys.argv) > 2 and sys.argv[2] == "seg":
+        return trace_seg(torch, np, _lib, plan, qkv, bs, mx, H)
     buf = torch.zeros(n * 32, dtype=torch.int64, device="cuda")
     _lib.call("bt_debug_mha_trace", buf.data_ptr())
     mha_device(qkv, plan, H, 64)
@@ -115,7 +115,7 @@ def trace_list(torch, np, _lib, plan, qkv, seqs, bs, mx, H, n):
         print(f"  cta {c}: start {r(t[c, 0]):.2f} Q {r(t[c, 1]):.2f} S0 {r(t[c, 2]):.2f} tiles 1,2 stored "
               + " ".join(f"{r(x):.2f}" for x in t[c, 28:30] if x > 0) + f" end {r(t[c, 31]):.2f}")
 
-def trace_win(torch, np, _lib, plan, qkv, bs, mx, H):
+def trace_seg(torch, np, _lib, plan, qkv, bs, mx, H):
     """Segment kernel (forced): per-CTA start, S-ready / softmax-done per key
     block, output stored."""
     T = plan.valid_word_cnt
@@ -127,7 +127,7 @@ def trace_win(torch, np, _lib, plan, qkv, bs, mx, H):
         _lib.call("bt_mha_varlen_sched", qkv.data_ptr(), plan.seq_starts_dev.data_ptr(), sched.data_ptr(), bs, mx, H,
                   64, 384, out.data_ptr(), T, _lib.stream_ptr())
 
-    _lib.call("bt_debug_mha_win", 2)
+    _lib.call("bt_debug_mha_seg", 2)
     for _ in range(2000):
         go()
     n = bs * ((mx + 127) // 128) * H  # grid (H, bs * ceil(mx / 128)); CTAs past the item list exit
@@ -136,7 +136,7 @@ def trace_win(torch, np, _lib, plan, qkv, bs, mx, H):
     go()
     torch.cuda.synchronize()
     _lib.call("bt_debug_mha_trace", 0)
-    _lib.call("bt_debug_mha_win", -1)
+    _lib.call("bt_debug_mha_seg", -1)
     t = buf.view(n, 32).cpu().numpy()
     used = np.nonzero(t[:, 0] > 0)[0]
     t0 = t[used, 0].min()

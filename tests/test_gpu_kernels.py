@@ -346,13 +346,13 @@ def test_mha_tile_list(env, lens, mx, grid):
     _lib.call("bt_plan_sched", plan.seq_starts_dev.data_ptr(), len(lens), mx, sched.data_ptr(), _lib.stream_ptr())
     out = torch.full((T, H * 64), float("nan"), device="cuda", dtype=torch.bfloat16)
     _lib.call("bt_debug_mha_list", 2, grid)
-    _lib.call("bt_debug_mha_win", 0)
+    _lib.call("bt_debug_mha_seg", 0)
     try:
         _lib.call("bt_mha_varlen_sched", qkv.data_ptr(), plan.seq_starts_dev.data_ptr(), sched.data_ptr(), len(lens),
                   mx, H, 64, 384, out.data_ptr(), T, _lib.stream_ptr())
     finally:
         _lib.call("bt_debug_mha_list", -1, 0)
-        _lib.call("bt_debug_mha_win", -1)
+        _lib.call("bt_debug_mha_seg", -1)
     torch.cuda.synchronize()
     ref = mha_device(qkv, plan, H, 64)
     assert torch.equal(out, ref)
@@ -420,11 +420,11 @@ def test_mha_segment_kernel(env, lens, mx):
     heads = 3
     plan = bt.plan_for_lengths(bt.SeqLengths.of(lens, mx))
     qkv = _rand_qkv(torch, plan.valid_word_cnt, heads * 64, seed=len(lens) + 3)
-    _lib.call("bt_debug_mha_win", 2)
+    _lib.call("bt_debug_mha_seg", 2)
     try:
         out = _mha_sched_call(bt, torch, qkv, plan, heads, mx)
     finally:
-        _lib.call("bt_debug_mha_win", -1)
+        _lib.call("bt_debug_mha_seg", -1)
     assert torch.isfinite(out.float()).all()
     ref = _oracle_mha(qkv, plan, heads, mx)
     assert_close_bf16(out, ref, what=f"segments {lens[:4]}")
@@ -447,7 +447,7 @@ def test_mha_segment_kernel_isolation_and_rescale(env):
         lo, hi = s[b] + 128, min(s[b] + 256, s[b + 1])
         if hi > lo:
             qkv[lo:hi, hid:2 * hid] *= 4
-    _lib.call("bt_debug_mha_win", 2)
+    _lib.call("bt_debug_mha_seg", 2)
     try:
         out = _mha_sched_call(bt, torch, qkv, plan, heads, mx)
         ref = _oracle_mha(qkv, plan, heads, mx)
@@ -458,5 +458,5 @@ def test_mha_segment_kernel_isolation_and_rescale(env):
                 pert[s[b]:s[b + 1]] = (torch.randn_like(pert[s[b]:s[b + 1]].float()) * 3).to(torch.bfloat16)
         out2 = _mha_sched_call(bt, torch, pert, plan, heads, mx)
     finally:
-        _lib.call("bt_debug_mha_win", -1)
+        _lib.call("bt_debug_mha_seg", -1)
     assert torch.equal(out[s[1]:s[2]], out2[s[1]:s[2]])
