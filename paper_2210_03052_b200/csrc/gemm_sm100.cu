@@ -796,10 +796,11 @@ static int autotune(const void* A, const void* Bt, const float* bias, const void
       if (sk && !(tiles % units != 0 && tiles <= 4 * units)) continue;
       const GemmChoice ch{c.pair, c.bn, sk != 0};
       BT_TRY(gemm_run(A, Bt, bias, residual, C, M, N, K, epi, ch, s));  // warm (module load, L2)
-      // two rounds of 5 back-to-back launches, each queued behind a ~40 us spin
-      // so host launch gaps stay out of the timing; the faster round counts
+      // three rounds of 5 back-to-back launches, each queued behind a ~40 us
+      // spin so host launch gaps stay out of the timing; the fastest round
+      // counts (two rounds let process-to-process noise flip close calls)
       float ms = 1e30f;
-      for (int round = 0; round < 2; ++round) {
+      for (int round = 0; round < 3; ++round) {
         spin_kernel<<<1, 32, 0, s>>>(80000);
         BT_CUDA_CHECK(cudaEventRecord(e0, s));
         for (int r = 0; r < 5; ++r) BT_TRY(gemm_run(A, Bt, bias, residual, C, M, N, K, epi, ch, s));
