@@ -195,3 +195,30 @@ def test_forward_mha_tile_list_bitwise():
                 assert np.array_equal(out, ref), f"grid {grid}"
     finally:
         _lib.call("bt_debug_mha_list", -1, 0)
+
+
+@pytest.mark.parametrize("bs,mx,lens_kind", [(256, 256, "short"), (257, 64, "uniform"), (3, 257, "uniform"),
+                                              (200, 8, "ones"), (40, 256, "mixed")])
+def test_forward_schedule_boundaries_vs_oracle(bt, bs, mx, lens_kind):
+    """Forward vs the fp32 oracle at the MHA scheduling boundaries: the
+    segment kernel's limits (bs 256 / 257, max_seq_len 256 / 257), hundreds of
+    one-token sequences in one segment, and runs of short sequences between
+    long ones (1 layer, 2 heads, so the oracle stays fast)."""
+    rng = np.random.default_rng(bs * 1000 + mx)
+    if lens_kind == "ones":
+        lens = [1] * bs
+    elif lens_kind == "short":
+        lens = [int(v) for v in rng.integers(1, 40, size=bs)]
+    elif lens_kind == "mixed":
+        lens = [int(v) if i % 5 else mx for i, v in enumerate(rng.integers(1, 60, size=bs))]
+    else:
+        lens = [int(v) for v in rng.integers(1, mx + 1, size=bs)]
+    cfg = bt.ModelConfig(layers=1, head_num=2, head_size=64, max_seq_len=mx, batch_size=bs,
+                         flags=bt.OptFlags.all_on())
+    ocfg = orc.OracleConfig(1, 2, 64, mx, bs)
+    x = orc.gen_input(lens, mx, 128, 3)
+    want = orc.forward(orc.init_weights(ocfg, 3), lens, x, ocfg)
+    y = bt.forward(bt.init_weights(cfg, 3), bt.SeqLengths.of(lens, mx), bt.Tensor(x), cfg)
+    assert_close_bf16(y, want, max_abs_max=2e-2, what=f"bs{bs} mx{mx} {lens_kind}")
+    valid = orc.build_mask(lens, mx).reshape(-1).astype(bool)
+    assert not np.asarray(y.array)[~valid].any()
