@@ -226,12 +226,15 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
   uint64_t* q_empty = v_full + NST;       // the tile's last S MMA has read Q
   uint64_t* o_free = q_empty + 1;         // the softmax warps have read O (next tile may overwrite it)
   uint32_t* holder = reinterpret_cast<uint32_t*>(o_free + 1);
-  volatile uint32_t* ring = holder + 1;  // [4] tile-list items of tiles t (slot t & 3), tagged with t
+  // [4] tile-list items of tiles t (slot t & 3), tagged with t; one word per
+  // entry, written / polled with shared-memory atomics (a self-contained
+  // handoff: readers use nothing else the writer stored)
+  uint32_t* ring = holder + 1;
   // the t-th query tile of this CTA (tile list: wait for the producer's entry)
   auto tile_at = [&](int t) -> MhaTile {
     if (list) {
       uint32_t v;
-      while (((v = ring[t & 3]) >> 24) != (static_cast<uint32_t>(t) & 0xFFu)) {
+      while (((v = atomicAdd(ring + (t & 3), 0u)) >> 24) != (static_cast<uint32_t>(t) & 0xFFu)) {
       }
       return tile_of(v & 0xFFFFFFu);
     }
@@ -311,7 +314,7 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
           item = __shfl_sync(0xffffffffu, item, 0);
           if (item >= static_cast<uint32_t>(nitems)) item = MHA_RING_NONE;
         }
-        if (lane == 0) ring[t & 3] = (static_cast<uint32_t>(t) & 0xFFu) << 24 | item;
+        if (lane == 0) atomicExch(ring + (t & 3), (static_cast<uint32_t>(t) & 0xFFu) << 24 | item);
         __syncwarp();
         if (item == MHA_RING_NONE) break;
         it = tile_of(item);
