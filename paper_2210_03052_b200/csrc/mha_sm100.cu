@@ -111,7 +111,7 @@ __device__ __forceinline__ void reg_tie(uint32_t (&r)[32]) {
 // reference's long-path algorithm -- per-128-column tile partial (max, sum)
 // combined by a full reduction, then exp on load (tensor.py:166-173,
 // attention.py:104-122, grouped.py:202-206) -- with P never reaching HBM.
-// 3 of every 8 exponentials run as a polynomial on the FMA pipe (ex2_poly2)
+// BT_MHA_POLY of every 16 exponentials run as a polynomial on the FMA pipe (ex2_poly2)
 // so the SFU (16 ex2 / clk / SM) is not the softmax's bound.  Keys past the
 // sequence end are masked (p = 0).
 //
@@ -136,7 +136,7 @@ struct MhaCfg {
 };
 
 #ifndef BT_MHA_POLY
-#define BT_MHA_POLY 6  // of every 16 exponentials, this many run as ex2_poly2 on the FMA pipe
+#define BT_MHA_POLY 2  // of every 16 exponentials, this many run as ex2_poly2 on the FMA pipe (measured 0..8: 2 best)
 #endif
 constexpr float MHA_RESCALE_LOG2 = 8.0f;  // move m_ref once P would exceed 2^8
 // 384 threads x 2 CTAs/SM -> 80 registers each at launch (30720 per CTA).
