@@ -38,7 +38,7 @@ namespace bt {
 
 constexpr int GLN_BN = 128;
 constexpr int GLN_BK = 64;
-constexpr int GLN_STAGES = 4;
+constexpr int GLN_STAGES = 5;
 constexpr int GLN_THREADS = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue
 constexpr uint32_t GLN_TILE = 128 * GLN_BK * 2;  // 16 KB: one 128 x 64 bf16 operand tile
 
