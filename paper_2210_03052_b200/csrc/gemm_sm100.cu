@@ -82,6 +82,9 @@ constexpr int MAX_UNITS = 148;              // stream-K workspace slots (one per
 
 constexpr uint32_t pow2_cols(uint32_t c) { return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512; }
 
+#ifndef GEMM_STAGING_BUFS
+#define GEMM_STAGING_BUFS 1
+#endif
 template <int PAIR, int BN, int EW>
 struct GemmCfg {
   static constexpr int BM = 128 * PAIR;     // rows per tile (per pair)
@@ -90,7 +93,8 @@ struct GemmCfg {
   static constexpr uint32_t A_BYTES = 128 * GEMM_BK * 2;
   static constexpr uint32_t B_BYTES = BN_CTA * GEMM_BK * 2;
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr uint32_t STAGING_BYTES = EW * 2 * 32 * 128;  // per epilogue warp: 2 buffers x 32 rows x 128 B
+  static constexpr int NBUF = GEMM_STAGING_BUFS;                  // staging buffers per epilogue warp
+  static constexpr uint32_t STAGING_BYTES = EW * NBUF * 32 * 128;  // per epilogue warp: NBUF x 32 rows x 128 B
   static constexpr int STAGES_FIT = static_cast<int>((GEMM_SMEM_LIMIT - 1024 - 256 - STAGING_BYTES) / STAGE_BYTES);
   static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
   static constexpr uint32_t TMEM_COLS = pow2_cols(2 * BN);
@@ -399,7 +403,7 @@ __global__ void __launch_bounds__(GemmCfg<PAIR, BN, EW>::THREADS, 1)
     const int quarter = warp & 3;
     const int colgrp = ew >> 2;
     constexpr int NGRP = EW / 4;
-    uint8_t* stage_buf = sC + ew * 8192;
+    uint8_t* stage_buf = sC + ew * (Cfg::NBUF * 4096);
     const uint32_t tempty_leader = (PAIR == 2) ? ptx::mapa_shared(ptx::smem_u32(tempty), 0) : 0;
     uint32_t buf_ctr = 0;
     int it = 0;
@@ -515,8 +519,8 @@ __global__ void __launch_bounds__(GemmCfg<PAIR, BN, EW>::THREADS, 1)
           // warp).  Measured alternative: coalesced st.global from the slab is
           // slower (2.99 vs 2.75 us per 128 x 256 tile; 5.8 vs 3.9 with GELU) --
           // the async store lets the warp go on to the next chunk's math.
-          uint8_t* buf = stage_buf + (buf_ctr & 1) * 4096;
-          if (lane == 0) ptx::bulk_wait_group_read<1>();  // the store issued from this buffer 2 chunks ago has read it
+          uint8_t* buf = stage_buf + (buf_ctr % Cfg::NBUF) * 4096;
+          if (lane == 0) ptx::bulk_wait_group_read<Cfg::NBUF - 1>();  // the store issued from this buffer NBUF chunks ago has read it
           __syncwarp();
           uint8_t* myrow = buf + lane * 128;
 #pragma unroll
