@@ -45,6 +45,8 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "BERT fwd sequences/sec (varlen, avg 0.6·max); fused MHA µs; % roofline"
+DATA_DESC = ("synthetic: reference generators gen_lengths(fixed, alpha=0.6, seed 0) + _gen_input(seed 0); "
+             "weights init_weights(seed 0) U(+-0.02)")
 
 WORKLOADS = {
     # name: (description, head_num, layers, batch per GPU (weak) or global (strong), max_seq_len, scaling)
@@ -134,35 +136,117 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ CPU side
-def cpu_oracle_forward_time(desc_cfg, seqs, x, budget_s: float, min_runs: int = 1):
-    """Time the CPU oracle (numpy port of the reference, OpenBLAS on all host
-    cores) on a bounded sample: whole forwards of the first n sequences, n
-    chosen so one run takes <= ~budget_s.  Returns (seq/s, sample description,
-    cores)."""
-    from oracle import packbert_np as orc
+def reference_module():
+    """The UNMODIFIED reference package (packbert 0.1.0) installed into
+    baseline/_ref by the offline pip install DESIGN.md records, or None
+    (then the CPU legs fall back to the numpy port in oracle/)."""
+    p = ROOT / "baseline" / "_ref"
+    if not (p / "packbert" / "encoder.py").exists():
+        return None
+    if str(p) not in sys.path:
+        sys.path.insert(0, str(p))
+    try:
+        import packbert.encoder  # noqa: F401
+        import packbert.packing  # noqa: F401
+        import packbert.tensor  # noqa: F401
 
-    head_num, layers, mx = desc_cfg
-    hidden = head_num * 64
-    lens_all = list(seqs.lengths)
-    w = orc.init_weights(orc.OracleConfig(layers, head_num, 64, mx, len(lens_all)), 0)
-    # probe: one layer on 2 sequences
-    n = min(len(lens_all), 2)
-    probe_cfg = orc.OracleConfig(1, head_num, 64, mx, n)
-    t0 = time.perf_counter()
-    orc.forward(w[:1], lens_all[:n], x[: n * mx], probe_cfg)
-    per_seq_layer = (time.perf_counter() - t0) / n
-    n = max(1, min(len(lens_all), int(budget_s / max(per_seq_layer * layers, 1e-6))))
-    cfg = orc.OracleConfig(layers, head_num, 64, mx, n)
-    times = []
-    for _ in range(max(1, min_runs)):
+        import packbert
+        return packbert
+    except Exception as e:  # noqa: BLE001
+        log(f"[bench] reference package in baseline/_ref not importable ({e}); using the oracle port")
+        return None
+
+
+class CpuForward:
+    """The reference's CPU forward on a bounded sample: the first n sequences
+    of the workload, OptFlags.all_on() (the padding-free path), weights
+    init_weights(seed 0) -- bit-identical draws to the GPU arm's.  Runs the
+    real reference (``packbert.encoder.forward`` from baseline/_ref,
+    kind "reference") when installed, else the numpy port (kind "port")."""
+
+    def __init__(self, heads, layers, mx, lens_all, x_all):
+        self.heads, self.layers, self.mx = heads, layers, mx
+        self.lens_all, self.x_all = list(lens_all), x_all
+        self.ref = reference_module()
+        self.kind = "reference" if self.ref is not None else "port"
+        if self.ref is not None:
+            enc = self.ref.encoder
+            self.flags = enc.OptFlags(True, True, True, True)
+            cfg = enc.ModelConfig(layers=layers, head_num=heads, head_size=64, max_seq_len=mx,
+                                  batch_size=len(self.lens_all), flags=self.flags)
+            self.w = enc.init_weights(cfg, 0)
+        else:
+            from oracle import packbert_np as orc
+
+            self.w = orc.init_weights(orc.OracleConfig(layers, heads, 64, mx, len(self.lens_all)), 0)
+        self.what = ("packbert.encoder.forward (the unmodified reference from baseline/_ref, OptFlags.all_on, "
+                     "workers=1, numpy/OpenBLAS)" if self.kind == "reference" else
+                     "oracle.forward (numpy/OpenBLAS port of packbert forward, OptFlags.all_on)")
+
+    def run(self, n: int, layers: int | None = None):
+        """One forward over the first n sequences; returns the padded fp32 output."""
+        layers = layers or self.layers
+        lens, x = self.lens_all[:n], self.x_all[: n * self.mx]
+        if self.ref is not None:
+            enc = self.ref.encoder
+            cfg = enc.ModelConfig(layers=layers, head_num=self.heads, head_size=64, max_seq_len=self.mx, batch_size=n,
+                                  flags=self.flags)
+            w = self.w if layers == self.layers else enc.EncoderWeights(layers=self.w.layers[:layers], shared=False)
+            y = enc.forward(w, self.ref.packing.SeqLengths.of(lens, self.mx), self.ref.tensor.Tensor(x), cfg)
+            return y.array
+        from oracle import packbert_np as orc
+
+        return orc.forward(self.w[:layers], lens, x, orc.OracleConfig(layers, self.heads, 64, self.mx, n))
+
+    def size_for(self, budget_s: float) -> int:
+        """Sequences per run so that one full-depth run takes about budget_s."""
+        n = min(len(self.lens_all), 2)
         t0 = time.perf_counter()
-        orc.forward(w, lens_all[:n], x[: n * mx], cfg)
+        self.run(n, layers=1)
+        per_seq = (time.perf_counter() - t0) / n * self.layers
+        return max(1, min(len(self.lens_all), int(budget_s / max(per_seq, 1e-6))))
+
+
+def blas_threads() -> int:
+    try:
+        from threadpoolctl import threadpool_info
+
+        return max((i.get("num_threads") or 1 for i in threadpool_info() if i.get("user_api") == "blas"), default=1)
+    except Exception:  # noqa: BLE001
+        return int(os.environ.get("OPENBLAS_NUM_THREADS", os.cpu_count() or 1))
+
+
+def cpu_baseline_leg(cf: CpuForward, budget_s: float, runs: int = 3):
+    """cpu_baseline: median of `runs` timed forwards on all host BLAS threads
+    plus one run on a single thread (threadpoolctl), each on a bounded
+    sample.  Returns (baseline dict, output of the first n sequences, n)."""
+    n = cf.size_for(budget_s / (runs + 1))
+    y = cf.run(n)  # warm-up, and the parity reference for the GPU rows
+    times = []
+    for _ in range(runs):
+        t0 = time.perf_counter()
+        cf.run(n)
         times.append(time.perf_counter() - t0)
     dt = statistics.median(times)
-    cores = int(os.environ.get("OPENBLAS_NUM_THREADS", os.cpu_count() or 1))
-    sample = (f"oracle.forward (numpy/OpenBLAS port of packbert forward, OptFlags.all_on) on the first {n} of "
-              f"{len(lens_all)} sequences ({sum(lens_all[:n])} tokens), {layers} layers, median of {len(times)}")
-    return n / dt, sample, cores
+    cores = blas_threads()
+    one = None
+    try:
+        from threadpoolctl import threadpool_limits
+
+        n1 = max(1, n // max(1, cores // 2))
+        with threadpool_limits(limits=1):
+            t0 = time.perf_counter()
+            cf.run(n1)
+            one = {"value": round(n1 / (time.perf_counter() - t0), 4), "unit": "seq/s", "cores": 1,
+                   "sample": f"first {n1} sequences, 1 run"}
+    except Exception as e:  # noqa: BLE001
+        log(f"[bench] 1-thread CPU row skipped ({e})")
+    toks = sum(cf.lens_all[:n])
+    base = {"value": round(n / dt, 4), "unit": "seq/s", "cores": cores, "kind": cf.kind,
+            "sample": f"{cf.what} on the first {n} of {len(cf.lens_all)} sequences ({toks} tokens), "
+                      f"{cf.layers} layers, median of {runs} runs ({', '.join(f'{t:.2f}' for t in times)} s)",
+            "single_thread": one}
+    return base, y, n
 
 
 # ------------------------------------------------------------------ GPU side
@@ -452,22 +536,19 @@ def run_ours(args, wl):
                     "peak_source": f"{peaks['source']} (MEASURED_PEAKS.json burst figure; kernel timed alone)",
                     "work_per_launch": dom["work_per_launch"]}
         step_flops = harness.forward_flops(seqs.lengths, hidden, layers)
-        cpu = None
+        cpu, parity = None, None
         if world == 1 and not args.no_cpu_baseline:
-            v, sample, cores = cpu_oracle_forward_time((heads, layers, mx), seqs, x_host, args.cpu_budget)
-            cpu = {"value": round(v, 4), "unit": "seq/s", "cores": cores, "kind": "port", "sample": sample}
+            cf = CpuForward(heads, layers, mx, lens, x_host)
+            cpu, y_ref, n_ref = cpu_baseline_leg(cf, args.cpu_budget)
+            # parity of the TIMED output (the last graph replay's out_dev) against
+            # the CPU reference's output for the same sequences
+            parity = parity_check(out_dev[: n_ref * mx].float().cpu().numpy(), y_ref, lens[:n_ref], mx, cf)
         result = {
             "metric": METRIC, "value": round(seq_per_s, 2), "unit": "seq/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
             "scaling": scaling, "vs_baseline": None, "dtype": "bf16",
-            "data": "synthetic: reference generators gen_lengths(fixed, alpha=0.6, seed 0) + _gen_input(seed 0); "
-                    "weights init_weights(seed 0) U(+-0.02)",
-            "config": {"workload": desc, "model": "bert_base" if heads == 12 else "bert_large", "layers": layers,
-                       "hidden": hidden, "global_batch": bs_global, "max_seq_len": mx, "tokens": seqs_g.total,
-                       "alpha": round(seqs_g.alpha, 4),
-                       "parallelism": f"token-balanced contiguous sequence partition x{world} (no collective)",
-                       "partition_imbalance": round(imbalance(shards), 4), "l2": "flushed (256 MB read) between "
-                       "timed steps", "cuda_graph": bool(use_graph), "timing": "CUDA events per step, max over ranks"},
+            "data": DATA_DESC,
+            "config": workload_config(wl, world),
             "tokens_per_s": round(tok_per_s, 1),
             "tflops": round(step_flops * world / (ms_per_step / 1e3) / 1e12, 2) if scaling == "weak" else
             round(harness.forward_flops(seqs_g.lengths, hidden, layers) / (ms_per_step / 1e3) / 1e12, 2),
@@ -480,7 +561,9 @@ def run_ours(args, wl):
                         for n, v in kernels.items()},
             "kernel_sum_ms": round(step_est / 1e3, 4),
             "cpu_baseline": cpu,
+            "parity": parity,
             "e2e": e2e,
+            "run": {"partition_imbalance": round(imbalance(shards), 4), "cuda_graph": bool(use_graph)},
             "gpu_launches": int(launches_per_step * args.steps),
             "gpu_launches_per_step": int(launches_per_step),
             "clocks": clk.summary(),
@@ -498,13 +581,14 @@ def run_ours(args, wl):
 
 
 def run_reference(args, wl):
-    """--impl reference: the reference's CPU implementation of the path (the
-    numpy port in oracle/, OpenBLAS on every host core), rank 0 only."""
+    """--impl reference: the reference's own CPU implementation of the path
+    (the unmodified packbert from baseline/_ref when installed, else the
+    numpy port in oracle/) on the host's cores, rank 0 only; each step a
+    bounded sample of the same workload (the first n sequences)."""
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return None
-    from oracle import packbert_np as orc
     from paper_2210_03052_b200 import harness
 
     desc, heads, layers, bs_cfg, mx, scaling = wl
@@ -512,36 +596,61 @@ def run_reference(args, wl):
     seqs = harness.gen_lengths(bs_global, mx, "fixed", seed=0, alpha=0.6)
     hidden = heads * 64
     x = harness.gen_input(seqs, hidden, 0)
-    lens = list(seqs.lengths)
-    w = orc.init_weights(orc.OracleConfig(layers, heads, 64, mx, len(lens)), 0)
-    # bound each step: the first n sequences of the batch so that W + K steps fit ~150 s
-    probe_cfg = orc.OracleConfig(1, heads, 64, mx, 1)
-    t0 = time.perf_counter()
-    orc.forward(w[:1], lens[:1], x[:mx], probe_cfg)
-    per_seq = (time.perf_counter() - t0) * layers
-    budget = args.cpu_budget_total / max(1, args.steps + args.warmup)
-    n = max(1, min(len(lens), int(budget / max(per_seq, 1e-6))))
-    cfg = orc.OracleConfig(layers, heads, 64, mx, n)
+    cf = CpuForward(heads, layers, mx, list(seqs.lengths), x)
+    # bound each step so that W + K steps fit cpu_budget_total
+    n = cf.size_for(args.cpu_budget_total / max(1, args.steps + args.warmup))
     for _ in range(args.warmup):
-        orc.forward(w, lens[:n], x[: n * mx], cfg)
+        cf.run(n)
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        orc.forward(w, lens[:n], x[: n * mx], cfg)
+        cf.run(n)
         times.append(time.perf_counter() - t0)
     ms = sum(times) * 1e3 / len(times)
     v = n / (ms / 1e3)
-    cores = int(os.environ.get("OPENBLAS_NUM_THREADS", os.cpu_count() or 1))
-    sample = (f"oracle.forward (numpy/OpenBLAS port of packbert forward, OptFlags.all_on) on the first {n} of "
-              f"{len(lens)} sequences ({sum(lens[:n])} tokens), {layers} layers per step")
+    cores = blas_threads()
+    sample = (f"{cf.what} on the first {n} of {len(seqs.lengths)} sequences ({sum(seqs.lengths[:n])} tokens), "
+              f"{layers} layers per step")
     return {"impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": "seq/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
             "scaling": scaling, "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic: reference generators (same lengths / input / weights as the GPU arm)",
-            "config": {"workload": desc, "model": "bert_base" if heads == 12 else "bert_large", "layers": layers,
-                       "global_batch": bs_global, "max_seq_len": mx, "tokens": seqs.total},
-            "cpu_baseline": {"value": round(v, 4), "unit": "seq/s", "cores": cores, "kind": "port", "sample": sample},
+            "data": DATA_DESC,
+            "config": workload_config(wl, world),
+            "cpu_baseline": {"value": round(v, 4), "unit": "seq/s", "cores": cores, "kind": cf.kind, "sample": sample},
             "e2e": {"value": round(v, 4), "unit": "seq/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def parity_check(got, want, lens, mx, cf):
+    """cosine / max-abs / relFro of the GPU's timed output rows against the CPU
+    reference's output for the same sequences (valid rows; padded rows must be
+    exactly zero)."""
+    valid = np.zeros(len(lens) * mx, dtype=bool)
+    for b, n in enumerate(lens):
+        valid[b * mx: b * mx + n] = True
+    a = got[valid].astype(np.float64).ravel()
+    b = np.asarray(want)[valid].astype(np.float64).ravel()
+    cos = float(a @ b / (np.linalg.norm(a) * np.linalg.norm(b)))
+    mab = float(np.abs(a - b).max())
+    rel = float(np.linalg.norm(a - b) / np.linalg.norm(b))
+    ok = cos >= 0.9999 and mab <= 2e-2 and not got[~valid].any()
+    return {"cosine": round(cos, 7), "max_abs": mab, "rel_fro": rel, "padded_rows_zero": bool(not got[~valid].any()),
+            "sequences": len(lens), "tokens": int(valid.sum()), "against": cf.kind,
+            "tolerance": "cosine >= 0.9999 and max-abs <= 2e-2 (north star)", "pass": bool(ok)}
+
+
+def workload_config(wl, world):
+    """The config dict both arms print (identical for the same workload)."""
+    from paper_2210_03052_b200 import harness
+
+    desc, heads, layers, bs_cfg, mx, scaling = wl
+    bs_global = bs_cfg * world if scaling == "weak" else bs_cfg
+    seqs = harness.gen_lengths(bs_global, mx, "fixed", seed=0, alpha=0.6)
+    return {"workload": desc, "model": "bert_base" if heads == 12 else "bert_large", "layers": layers,
+            "hidden": heads * 64, "global_batch": bs_global, "max_seq_len": mx, "tokens": seqs.total,
+            "alpha": round(seqs.alpha, 4),
+            "parallelism": f"token-balanced contiguous sequence partition x{world} (no collective)",
+            "l2": "flushed (256 MB read) between timed steps",
+            "timing": "device: CUDA events per step, max over ranks; CPU: wall clock per step"}
 
 
 def main():

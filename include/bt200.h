@@ -257,6 +257,16 @@ BT_API int bt_debug_mha_occupancy(int which, int* info);
 /* Debug hook: per-CTA globaltimer event trace of the MHA kernels (32 u64 slots per CTA). */
 BT_API int bt_debug_mha_trace(unsigned long long* buf);
 
+/* Instrumented FlopCounter (replaces the counter.add calls of reference
+ * tensor.py:198-199 / attention.py:232-236 with launch-level counting).
+ * bt_flops_enable(dev): from now on every GEMM the encoder layer launches adds
+ * 2*M*N*K of its launch shape under its module key (host counters, read with
+ * bt_flops_read: out[0..3] = gemm0 QKV, gemm1 attention output, gemm2 FFN1,
+ * gemm3 FFN2), and every MHA tile adds the FLOPs it computed (4*d per query
+ * row x key of its problem) to the device u64 *dev.  NULL turns it off. */
+BT_API int bt_flops_enable(unsigned long long* dev_mha_counter);
+BT_API int bt_flops_read(long long* out4);
+
 /* forward on the packed layout: x_packed / out_packed fp32 [T, k] (device).
  * Same pipeline as bt_encoder_forward minus the gather / scatter; the
  * end-to-end host path DMAs only valid rows in and out (bt_copy_rows). */

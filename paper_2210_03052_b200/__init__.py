@@ -35,3 +35,4 @@ from .errors import ConfigError, PackbertError, ShapeError, WeightFormatError
 from .fusion import LayernormParams, add, add_bias_residual_layernorm, add_rowvec, bias_gelu_epilogue, gelu, layernorm
 from .packing import PackedBatch, PackingPlan, SeqLengths, build_mask, compute_plan, pack, plan_for_lengths, unpack
 from .tensor import EpilogueHook, EpilogueKind, FlopCounter, Tensor, batched_gemm, gemm
+from .partition import forward_sharded, token_balanced_partition

@@ -86,6 +86,8 @@ SIGNATURES = {
     "bt_debug_mha_occupancy": (_I, [_I, _P]),
     "bt_debug_forward_events": (_I, [_P, _I]),
     "bt_mha_varlen_path": (_I, [_P, _P, _I, _I, _I, _I, _P, _I, _I, _S]),
+    "bt_flops_enable": (_I, [_P]),
+    "bt_flops_read": (_I, [_P]),
 }
 
 _lock = threading.Lock()

@@ -106,17 +106,21 @@ def _qkv_device(inp: AttentionInput):
     return qkv
 
 
-def _flops(inp: AttentionInput, counter: FlopCounter | None) -> None:
-    if counter is not None:
-        counter.add("mha", sum(4 * n * n * inp.head_size for n in inp.plan.seqs.lengths) * inp.head_num)
-
-
 def _run(inp: AttentionInput, op: str, path: int, cutoff: int, split_seq_len: int, counter):
     inp.plan = ensure_plan(inp.plan)
     inp.require_packed(op)
-    out = mha_device(_qkv_device(inp), inp.plan, inp.head_num, inp.head_size, cutoff=cutoff,
-                     split_seq_len=split_seq_len, path=path)
-    _flops(inp, counter)
+    qkv = _qkv_device(inp)
+    if counter is None:
+        out = mha_device(qkv, inp.plan, inp.head_num, inp.head_size, cutoff=cutoff, split_seq_len=split_seq_len,
+                         path=path)
+    else:
+        # instrumented: the kernel's tiles count the work they did (instrument.py)
+        from .instrument import LaunchFlops
+
+        with LaunchFlops() as lf:
+            out = mha_device(qkv, inp.plan, inp.head_num, inp.head_size, cutoff=cutoff,
+                             split_seq_len=split_seq_len, path=path)
+        counter.add("mha", lf.counts["mha"])
     return out.float() if is_device(inp.q) else Tensor(out.float().cpu().numpy())
 
 

@@ -3,12 +3,16 @@
 surface, driving the GPU kernels instead of numpy.
 
 Timing is CUDA-event time of the device-resident forward (plan + pack + L
-layers + unpack for the packed rungs), median over ``repeats``; the
+layers + unpack for the packed rungs), each rung captured into a CUDA graph
+so that rungs compare device work, median over ``repeats``; the
 deviation column is the reference's masked relative Frobenius norm against
 the all-off padded baseline over valid rows (bench.py:171-178), and the FLOP
 columns come from the exact / analytic model (flops.py).  ``check=True``
-additionally verifies that the instrumented FlopCounter matches the exact
-model with zero tolerance (bench.py:256-267).
+additionally runs the instrumented forward (``counter=FlopCounter()``: the
+launches count their own FLOPs, instrument.py) and requires every module key
+to match the exact model with zero tolerance (bench.py:256-267); soft
+alpha-inversion warnings as bench.py:273-288; ``--weights`` loads a PKBW file
+(bench.py:201-202).
 
     python -m paper_2210_03052_b200.bench_ladder --preset bert_base --batch 16 --max-len 256 --alpha 0.6
 """
@@ -27,7 +31,7 @@ import numpy as np
 from . import _lib
 from .encoder import ModelConfig, OptFlags, engine_for, init_weights, preset_config
 from .errors import ConfigError
-from .harness import gen_input, gen_lengths, layer_flops
+from .harness import gen_input, gen_lengths
 from .ladder import LADDER_NAMES, forward_variant_device, ladder_flags
 from .packing import build_mask, plan_for_lengths
 from .tensor import FlopCounter
@@ -48,6 +52,7 @@ class BenchSpec:
     variants: tuple = tuple(LADDER_NAMES)
     workers: int = 1
     layers: int | None = None
+    weights_path: str | None = None
     check: bool = False
 
     def __post_init__(self):
@@ -105,36 +110,48 @@ def _masked_rel_dev(out, ref, valid_rows) -> float:
     return float(np.linalg.norm(a)) if d == 0.0 else float(np.linalg.norm(a - b) / d)
 
 
-def _flops(config, seqs, variant) -> tuple[int, float]:
-    k = config.hidden_dim
-    m = seqs.batch_size * seqs.max_seq_len
-    fused = variant == "fused_mha"
-    packed = variant in ("rm_padding", "fused_mha")
-    me = seqs.total if packed else m
-    ma = seqs.alpha * m if packed else float(m)
-    f = 2 * config.ffn_scale
-    exact = 6 * me * k * k + 2 * me * k * k + 2 * f * me * k * k
-    analytic = (6 + 2 + 2 * f) * ma * k * k
-    if fused:
-        exact += layer_flops(seqs.lengths, k, config.ffn_scale)["mha"]
-        analytic += 4.0 * (seqs.alpha * m) ** 2 * k / seqs.batch_size
-    else:
-        exact += 4 * seqs.batch_size * seqs.max_seq_len ** 2 * k
-        analytic += 4.0 * m * m * k / seqs.batch_size
-    return exact * config.layers, analytic * config.layers
+def _graphed(torch, fn):
+    """fn captured into a CUDA graph (after an eager warm-up that also runs
+    the GEMM autotune) -> replay callable; eager fn when capture fails."""
+    fn()
+    torch.cuda.synchronize()
+    try:
+        g = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            fn()
+        torch.cuda.current_stream().wait_stream(side)
+        with torch.cuda.graph(g):
+            fn()
+        torch.cuda.synchronize()
+        return g.replay
+    except Exception:  # noqa: BLE001
+        return fn
 
 
 def run_ladder(spec: BenchSpec) -> BenchResult:
+    """The ladder (reference bench.py:194-270).  Each rung's device forward is
+    captured into a CUDA graph and timed by CUDA events over its replays, so
+    rungs compare device work, not Python launch overhead.  ``check`` runs
+    the public ``forward(..., counter=FlopCounter())`` -- whose launches count
+    their own FLOPs (instrument.py) -- and compares every module key with the
+    exact model, zero tolerance (bench.py:256-267)."""
+    from . import flops as flops_model
+    from .encoder import forward, load_weights
+    from .packing import SeqLengths
+
     torch = _lib.require_device()
     result = BenchResult(rows=[])
     base = spec.config_for(spec.max_seq_lens[0])
-    weights = init_weights(base, spec.seed)
+    weights = load_weights(spec.weights_path, base) if spec.weights_path else init_weights(base, spec.seed)
     tol = deviation_tolerance(base.layers)
     for max_len in spec.max_seq_lens:
         for alpha in (spec.alphas or (None,)):
             seqs = gen_lengths(spec.batch_size, max_len, spec.mode, spec.seed, alpha)
             cfg_pt = spec.config_for(max_len)
-            x = torch.from_numpy(gen_input(seqs, cfg_pt.hidden_dim, spec.seed)).cuda()
+            x_host = gen_input(seqs, cfg_pt.hidden_dim, spec.seed)
+            x = torch.from_numpy(x_host).cuda()
             valid = build_mask(seqs).reshape(-1).astype(bool)
             plan = plan_for_lengths(seqs)
             eng = engine_for(weights, cfg_pt)
@@ -143,16 +160,17 @@ def run_ladder(spec: BenchSpec) -> BenchResult:
                 if name not in spec.variants:
                     continue
                 cfg = cfg_pt.with_flags(ladder_flags(name))
+                box = {}
                 if name == "fused_mha":
                     lengths = torch.tensor(seqs.lengths, dtype=torch.int32, device="cuda")
-                    y = torch.empty_like(x)
-                    run = lambda: eng.forward_device(lengths, seqs.batch_size, seqs.total, x, y, config=cfg)  # noqa
+                    box["y"] = torch.empty_like(x)
+                    fn = lambda: eng.forward_device(lengths, seqs.batch_size, seqs.total, x, box["y"], config=cfg)  # noqa
                 else:
-                    box = {}
-                    run = lambda: box.__setitem__("y", forward_variant_device(eng, plan, x, cfg))  # noqa: E731
+                    fn = lambda: box.__setitem__("y", forward_variant_device(eng, plan, x, cfg))  # noqa: E731
+                run = _graphed(torch, fn)
                 run()
                 torch.cuda.synchronize()
-                out = (y if name == "fused_mha" else box["y"]).cpu().numpy()
+                out = box["y"].cpu().numpy()
                 times = []
                 for _ in range(spec.repeats):
                     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -162,7 +180,9 @@ def run_ladder(spec: BenchSpec) -> BenchResult:
                     torch.cuda.synchronize()
                     times.append(e0.elapsed_time(e1))
                 dev = _masked_rel_dev(out, base_out, valid)
-                fe, fa = _flops(cfg, seqs, name)
+                report = flops_model.count(cfg, seqs, flops_model.variant_for_flags(cfg.flags))
+                fe = report.exact_total * cfg.layers
+                fa = report.analytic_total * cfg.layers
                 result.rows.append(BenchRow(spec.preset, name, spec.batch_size, max_len, seqs.alpha, spec.workers,
                                             statistics.median(times), fe, fa, dev))
                 if dev > tol:
@@ -170,14 +190,34 @@ def run_ladder(spec: BenchSpec) -> BenchResult:
                     result.diagnostics.append(f"{name} @ max_len={max_len} alpha={seqs.alpha:.3f}: "
                                               f"deviation {dev:.3e} exceeds {tol:.0e}")
                 if spec.check:
-                    from .ladder import _count
-
                     c = FlopCounter()
-                    _count(c, cfg, seqs, cfg.layers)
-                    if c.total() != fe:
-                        result.passed = False
-                        result.diagnostics.append(f"{name}: instrumented {c.total()} != exact {fe}")
+                    forward(weights, SeqLengths.of(seqs.lengths, max_len), x_host, cfg, counter=c)
+                    for key in flops_model.MODULE_KEYS:
+                        want = report.exact[key] * cfg.layers
+                        got = c.get(key)
+                        if got != want:
+                            result.passed = False
+                            result.diagnostics.append(f"{name} @ max_len={max_len}: instrumented {key} counted "
+                                                      f"{got}, exact model predicts {want}")
+    _warn_on_alpha_inversions(result)
     return result
+
+
+def _warn_on_alpha_inversions(result: BenchResult) -> None:
+    """Soft check (reference bench.py:273-288): packed-rung time should not
+    fall as alpha grows."""
+    by_key: dict = {}
+    for row in result.rows:
+        if row.variant == "rm_padding":
+            by_key.setdefault((row.preset, row.max_len), []).append(row)
+    for (preset, max_len), rows in by_key.items():
+        rows = sorted(rows, key=lambda r: r.alpha_actual)
+        for prev, cur in zip(rows, rows[1:]):
+            if cur.median_ms < prev.median_ms * 0.95:
+                result.warnings.append(
+                    f"rm_padding @ {preset} max_len={max_len}: median time fell from {prev.median_ms:.2f} ms "
+                    f"(alpha {prev.alpha_actual:.2f}) to {cur.median_ms:.2f} ms (alpha {cur.alpha_actual:.2f}); "
+                    "expected nondecreasing in alpha (noisy machine?)")
 
 
 def rows_to_csv(rows) -> str:
@@ -203,13 +243,16 @@ def main(argv=None):
     ap.add_argument("--layers", type=int, default=None)
     ap.add_argument("--repeats", type=int, default=10)
     ap.add_argument("--check", action="store_true")
+    ap.add_argument("--weights", default=None, help="PKBW weight file (default: init_weights(seed))")
     ap.add_argument("--json", action="store_true")
     a = ap.parse_args(argv)
     spec = BenchSpec(preset=a.preset, batch_size=a.batch, max_seq_lens=tuple(a.max_len),
                      alphas=tuple(a.alpha) if a.alpha else None, mode="fixed" if a.alpha else "uniform",
-                     repeats=a.repeats, layers=a.layers, check=a.check)
+                     repeats=a.repeats, layers=a.layers, weights_path=a.weights, check=a.check)
     res = run_ladder(spec)
     print(rows_to_json(res.rows) if a.json else rows_to_csv(res.rows), end="")
+    for w in res.warnings:
+        print("WARN:", w)
     for d in res.diagnostics:
         print("FAIL:", d)
     return 0 if res.passed else 1

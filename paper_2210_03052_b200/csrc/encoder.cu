@@ -52,6 +52,18 @@ static bool debug_skip(char c) {
 
 static inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
+// Instrumented FlopCounter (reference tensor.py:198-199, attention.py:232-236):
+// while enabled, every GEMM the layer launches adds 2*M*N*K under its module
+// key (gemm0 QKV, gemm1 attention output, gemm2 FFN1, gemm3 FFN2) from the
+// shapes it was launched with, and the MHA kernel adds the work its tiles did
+// to a device counter.  Off by default (no cost on the hot path).
+extern unsigned long long* g_mha_flops;
+static bool g_flops_on = false;
+static long long g_flops[4] = {0, 0, 0, 0};
+static void count_gemm(int key, int M, int N, int K) {
+  if (g_flops_on) g_flops[key] += 2LL * M * N * K;
+}
+
 struct LayerWs {
   __nv_bfloat16 *qkv, *ctx, *proj, *y0, *h1;
 };
@@ -130,6 +142,7 @@ static int encoder_layer_impl(const bt_layer_weights* w, const bt_layer_cfg* cfg
   auto* x = static_cast<__nv_bfloat16*>(x_inout);
 
   if (!debug_skip('q')) BT_TRY(bt::gemm_launch(x, w->qkv_w, w->qkv_b, nullptr, L.qkv, T, 3 * k, k, BT_EPI_BIAS, 0, s));
+  count_gemm(0, T, 3 * k, k);
   BT_TRY(mark(s));
   if (!debug_skip('m'))
     BT_TRY(bt::mha_launch(L.qkv, seq_starts, bs, cfg->max_seq_len, cfg->head_num, cfg->head_size, cfg->cutoff, T,
@@ -138,20 +151,25 @@ static int encoder_layer_impl(const bt_layer_weights* w, const bt_layer_cfg* cfg
   if (debug_skip('a')) {
   } else if (fused_ln_mode() >= 1 && gemm_ln_fits(T, k, k)) {  // y0 = LN((ctx Wo + x) + bo), one kernel
     BT_TRY(gemm_ln_launch(L.ctx, w->ao_w, w->ao_b, x, w->ln0_g, w->ln0_b, w->ln0_eps, L.y0, T, k, k, s));
+    count_gemm(1, T, k, k);
     BT_TRY(mark(s));
   } else {
     BT_TRY(bt::gemm_launch(L.ctx, w->ao_w, nullptr, nullptr, L.proj, T, k, k, BT_EPI_NONE, 0, s));
+    count_gemm(1, T, k, k);
     BT_TRY(mark(s));
     BT_TRY(bt_ln_bias_residual(L.proj, x, w->ao_b, w->ln0_g, w->ln0_b, w->ln0_eps, L.y0, T, k, stream));
   }
   BT_TRY(mark(s));
   if (!debug_skip('f')) BT_TRY(bt::gemm_launch(L.y0, w->w1, w->b1, nullptr, L.h1, T, f, k, BT_EPI_BIAS_GELU, 0, s));
+  count_gemm(2, T, f, k);
   BT_TRY(mark(s));
   if (fused_ln_mode() >= 2 && gemm_ln_fits(T, k, f)) {  // x = LN((h1 W2 + y0) + b2), one kernel
     BT_TRY(gemm_ln_launch(L.h1, w->w2, w->b2, L.y0, w->ln1_g, w->ln1_b, w->ln1_eps, x, T, k, f, s));
+    count_gemm(3, T, k, f);
     BT_TRY(mark(s));
   } else {
     if (!debug_skip('s')) BT_TRY(bt::gemm_launch(L.h1, w->w2, nullptr, nullptr, L.proj, T, k, f, BT_EPI_NONE, 0, s));
+    count_gemm(3, T, k, f);
     BT_TRY(mark(s));
     if (!debug_skip('l'))
       BT_TRY(bt_ln_bias_residual(L.proj, L.y0, w->b2, w->ln1_g, w->ln1_b, w->ln1_eps, x, T, k, stream));
@@ -305,5 +323,21 @@ extern "C" int bt_copy_rows(void* dst, const void* src, const int32_t* lengths_h
   }
   for (size_t i = 0; i < sizes.size(); ++i)
     BT_CUDA_CHECK(cudaMemcpyAsync(dsts[i], srcs[i], sizes[i], cudaMemcpyDefault, s));
+  return BT_OK;
+}
+
+// Instrumented FLOP counting on (dev_mha_counter: a device u64 the MHA tiles
+// add to; the GEMM counts start from zero) or off (NULL).
+extern "C" int bt_flops_enable(unsigned long long* dev_mha_counter) {
+  bt::g_flops_on = dev_mha_counter != nullptr;
+  bt::g_mha_flops = dev_mha_counter;
+  for (long long& v : bt::g_flops) v = 0;
+  return BT_OK;
+}
+
+// The GEMM FLOPs counted since bt_flops_enable: out[0..3] = gemm0..gemm3.
+extern "C" int bt_flops_read(long long* out4) {
+  BT_REQUIRE(out4 != nullptr, BT_ESHAPE, "bt_flops_read: null output");
+  for (int i = 0; i < 4; ++i) out4[i] = bt::g_flops[i];
   return BT_OK;
 }

@@ -592,9 +592,14 @@ static int streamk_workspace(cudaStream_t s, StreamKWorkspace** out) {
   if (!ws.partials) {
     // one fp32 128 x 256 partial per (unit, rank) + one flag each; flags
     // start at 0 and every finisher resets the flags it consumed
+    // (first use outside a stream capture: cudaMalloc would invalidate it)
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    BT_CUDA_CHECK(cudaStreamIsCapturing(s, &cs));
+    BT_REQUIRE(cs == cudaStreamCaptureStatusNone, BT_ECONFIG,
+               "gemm: stream-K needs one eager launch on this stream before a graph capture");
     BT_CUDA_CHECK(cudaMalloc(&ws.partials, sizeof(float) * MAX_UNITS * 2 * 128 * 256));
     BT_CUDA_CHECK(cudaMalloc(&ws.flags, sizeof(int) * MAX_UNITS * 2));
-    BT_CUDA_CHECK(cudaMemset(ws.flags, 0, sizeof(int) * MAX_UNITS * 2));
+    BT_CUDA_CHECK(cudaMemsetAsync(ws.flags, 0, sizeof(int) * MAX_UNITS * 2, s));
   }
   *out = &ws;
   return BT_OK;
@@ -635,6 +640,7 @@ struct GemmChoice {
 // time at ~55 B/clk/SM).  Round-robin: waves x per-tile time.  Stream-K:
 // ceil(work / units) k-blocks per unit plus a fix-up cost for split tiles.
 // Plus a fixed fill / drain cost.
+static bool g_auto_streamk = false;  // stream-K among the automatic candidates (off: see choose_tile)
 static GemmChoice choose_tile(int M, int N, int K, int sms) {
   struct Cand { int pair, bn; };
   const Cand cands[] = {{2, 256}, {2, 192}, {2, 128}, {1, 256}, {1, 192}, {1, 128}, {1, 64}};
@@ -659,8 +665,12 @@ static GemmChoice choose_tile(int M, int N, int K, int sms) {
     }
     // stream-K (only when it changes the balance, and only for small
     // problems: contiguous per-unit ranges spread the units over the whole
-    // M range, which costs L2 locality once A no longer fits in L2)
-    if (tiles % units != 0 && tiles <= 4 * units && units <= MAX_UNITS) {
+    // M range, which costs L2 locality once A no longer fits in L2).  Never
+    // chosen automatically (g_auto_streamk): its fix-up changes the fp32
+    // summation order with the unit count, and the forward guarantees
+    // results that do not depend on M (a shard equals its rows of the full
+    // batch, bit for bit).
+    if (g_auto_streamk && tiles % units != 0 && tiles <= 4 * units && units <= MAX_UNITS) {
       const long long work = tiles * nk;
       const double per_unit = static_cast<double>((work + units - 1) / units);
       const double fixup = 8000.0;  // measured: partial write + fence/flag + read costs ~4 us per split tile
@@ -797,7 +807,7 @@ static int autotune(const void* A, const void* Bt, const float* bias, const void
     const long long tiles = static_cast<long long>((M + bm - 1) / bm) * (N / c.bn);
     const long long units = sms / c.pair;
     for (int sk = 0; sk < 2; ++sk) {
-      if (sk && !(tiles % units != 0 && tiles <= 4 * units)) continue;
+      if (sk && !(g_auto_streamk && tiles % units != 0 && tiles <= 4 * units)) continue;
       const GemmChoice ch{c.pair, c.bn, sk != 0};
       BT_TRY(gemm_run(A, Bt, bias, residual, C, M, N, K, epi, ch, s));  // warm (module load, L2)
       // three rounds of 5 back-to-back launches, each queued behind a ~40 us

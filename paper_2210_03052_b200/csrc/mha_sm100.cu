@@ -66,6 +66,10 @@ struct MhaParams {
   const int4* segs;
   const int* nsegs;
   int T;
+  // optional: the instrumented FlopCounter's "mha" slot (reference
+  // attention.py:232-236) -- every tile adds the work it did, 4 * d FLOPs
+  // per (query row, key of its own problem)
+  unsigned long long* flops;
 };
 
 // One query tile of work: rows [s0 + q0, s0 + min(q0 + 128, len)) of head h,
@@ -118,7 +122,7 @@ __device__ __forceinline__ void reg_tie(uint32_t (&r)[32]) {
 // Warp roles (384 threads): warps 0-7 softmax / epilogue (two threads per query
 // row, 64 keys each), warp 8 TMA producer, warp 9 MMA issuer, warps 10-11 idle
 // (they complete warpgroup 2 for setmaxnreg); both issuer warps walk their loops warp-uniformly and
-// issue through elect.sync.  TMEM: S [0,128), O [128,192) -> 256 columns;
+// issue through elect.sync.  TMEM: S [0,128), P [128,192), O [192,256) -> 256 columns;
 // ~112 KB smem -> two CTAs per SM, whose latency chains interleave.
 template <bool RESIDENT, int NST, bool MULTI, bool SEG = false>
 struct MhaCfg {
@@ -160,55 +164,6 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
   int sb = 0, len = 0, qt0 = 0, nqt = 0, nitems = 0;
   int seg_a = 0, seg_b = 0;  // SEG: first / last sequence of the segment
   int seg_q = 0, seg_rows = 0;  // SEG: first query row, query rows
-  if (SEG) {
-    if (static_cast<int>(blockIdx.y) >= __ldg(p.nsegs)) return;  // CTA-uniform: past the item list
-    h = blockIdx.x;
-    const int4 e = __ldg(p.segs + 2 * blockIdx.y), f = __ldg(p.segs + 2 * blockIdx.y + 1);
-    sb = e.x;
-    len = e.y - e.x;
-    seg_q = e.z;
-    seg_rows = e.w - e.z;
-    seg_a = f.x;
-    seg_b = f.y;
-  } else if (list) {
-    nitems = __ldg(p.nunits) * p.heads;
-    if (static_cast<int>(blockIdx.x) >= nitems) return;  // CTA-uniform: fewer items than CTAs
-    nqt = 0x7FFFFFFF;  // tiles come from the queue until it runs dry
-  } else {
-    if (p.sched) {  // longest problems first (plan_sched_kernel)
-      const int2 e = __ldg(p.sched + b);
-      sb = e.x;
-      len = e.y;
-    } else {
-      sb = __ldg(p.seq_starts + b);
-      len = __ldg(p.seq_starts + b + 1) - sb;
-    }
-  }
-  // Packed layout: the sequence's rows start at seq_starts[b] and only its
-  // len rows / keys are touched.  Padded layout (the reference's unfused
-  // baseline): rows start at b*mx and the whole mx x mx rectangle is
-  // computed, keys >= len masked out of the softmax (exp -> 0, the -1e9 mask
-  // of attention.py:162-163) and query rows >= len written as zeros.
-  const int cta_s0 = p.padded ? b * p.mx : sb;
-  const int cta_work = p.padded ? p.mx : len;
-  if (SEG) {
-    nqt = 1;
-  } else if (!list) {
-    // this CTA's query tiles: qt0, qt0 + 1, ... (p.qg per CTA when Cfg::LOOP)
-    const int qg = Cfg::LOOP ? p.qg : 1;
-    qt0 = blockIdx.x * qg;
-    if (qt0 * MHA_QT >= cta_work) return;  // CTA-uniform: past the sequence
-    nqt = Cfg::LOOP ? min(qg, (cta_work + MHA_QT - 1) / MHA_QT - qt0) : 1;
-  }
-  // tile-list item -> query tile (len 0: none left)
-  auto tile_of = [&](uint32_t item) -> MhaTile {
-    if (item == MHA_RING_NONE) return MhaTile{0, 0, 0, 0};
-    const int i = static_cast<int>(item);
-    const int u = i / p.heads;
-    const int2 e = __ldg(p.units + u);
-    return MhaTile{e.x, e.y & 0xFFFFF, i - u * p.heads, (e.y >> 20) * MHA_QT};
-  };
-
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sQ = smem + Cfg::Q_OFF;
   uint8_t* sKV = smem + Cfg::KV_OFF;
@@ -230,18 +185,8 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
   // entry, written / polled with shared-memory atomics (a self-contained
   // handoff: readers use nothing else the writer stored)
   uint32_t* ring = holder + 1;
-  // the t-th query tile of this CTA (tile list: wait for the producer's entry)
-  auto tile_at = [&](int t) -> MhaTile {
-    if (list) {
-      uint32_t v;
-      while (((v = atomicAdd(ring + (t & 3), 0u)) >> 24) != (static_cast<uint32_t>(t) & 0xFFu)) {
-      }
-      return tile_of(v & 0xFFFFFFu);
-    }
-    if (SEG) return MhaTile{cta_s0, cta_work, h, seg_q - cta_s0};
-    return MhaTile{cta_s0, cta_work, h, (qt0 + t) * MHA_QT};
-  };
 
+  // ---- prologue (touches no data of the previous kernels): barriers, TMEM
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     ptx::prefetch_tmap(&tm);
@@ -274,8 +219,81 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
   constexpr uint32_t S_COL = 0, P_COL = 128, O_COL = 192;
   ptx::griddep_launch_dependents();
   if (threadIdx.x == 0) MHA_TRACE(0);
+  // The work description (seq_starts, the bt_plan_sched schedule / segments /
+  // tile list) may come from an earlier kernel of the same stream (the
+  // forward's plan launch): PDL only orders this kernel after its immediate
+  // predecessor, so every read of it comes after griddepcontrol.wait (which
+  // returns once the predecessor -- and transitively, everything it waited
+  // for -- has completed and flushed).
+  ptx::griddep_wait();
+  bool active = true;
+  if (SEG) {
+    if (static_cast<int>(blockIdx.y) >= __ldg(p.nsegs)) {
+      active = false;  // CTA-uniform: past the item list
+    } else {
+      h = blockIdx.x;
+      const int4 e = __ldg(p.segs + 2 * blockIdx.y), f = __ldg(p.segs + 2 * blockIdx.y + 1);
+      sb = e.x;
+      len = e.y - e.x;
+      seg_q = e.z;
+      seg_rows = e.w - e.z;
+      seg_a = f.x;
+      seg_b = f.y;
+    }
+  } else if (list) {
+    nitems = __ldg(p.nunits) * p.heads;
+    if (static_cast<int>(blockIdx.x) >= nitems) active = false;  // CTA-uniform: fewer items than CTAs
+    nqt = 0x7FFFFFFF;  // tiles come from the queue until it runs dry
+  } else {
+    if (p.sched) {  // longest problems first (plan_sched_kernel)
+      const int2 e = __ldg(p.sched + b);
+      sb = e.x;
+      len = e.y;
+    } else {
+      sb = __ldg(p.seq_starts + b);
+      len = __ldg(p.seq_starts + b + 1) - sb;
+    }
+  }
+  // Packed layout: the sequence's rows start at seq_starts[b] and only its
+  // len rows / keys are touched.  Padded layout (the reference's unfused
+  // baseline): rows start at b*mx and the whole mx x mx rectangle is
+  // computed, keys >= len masked out of the softmax (exp -> 0, the -1e9 mask
+  // of attention.py:162-163) and query rows >= len written as zeros.
+  const int cta_s0 = p.padded ? b * p.mx : sb;
+  const int cta_work = p.padded ? p.mx : len;
+  if (SEG) {
+    nqt = 1;
+  } else if (!list) {
+    // this CTA's query tiles: qt0, qt0 + 1, ... (p.qg per CTA when Cfg::LOOP)
+    const int qg = Cfg::LOOP ? p.qg : 1;
+    qt0 = blockIdx.x * qg;
+    if (qt0 * MHA_QT >= cta_work) active = false;  // CTA-uniform: past the sequence
+    nqt = Cfg::LOOP ? min(qg, (cta_work + MHA_QT - 1) / MHA_QT - qt0) : 1;
+  }
+  // tile-list item -> query tile (len 0: none left)
+  auto tile_of = [&](uint32_t item) -> MhaTile {
+    if (item == MHA_RING_NONE) return MhaTile{0, 0, 0, 0};
+    const int i = static_cast<int>(item);
+    const int u = i / p.heads;
+    const int2 e = __ldg(p.units + u);
+    return MhaTile{e.x, e.y & 0xFFFFF, i - u * p.heads, (e.y >> 20) * MHA_QT};
+  };
 
-  if (warp >= 8) {
+  // the t-th query tile of this CTA (tile list: wait for the producer's entry)
+  auto tile_at = [&](int t) -> MhaTile {
+    if (list) {
+      uint32_t v;
+      while (((v = atomicAdd(ring + (t & 3), 0u)) >> 24) != (static_cast<uint32_t>(t) & 0xFFu)) {
+      }
+      return tile_of(v & 0xFFFFFFu);
+    }
+    if (SEG) return MhaTile{cta_s0, cta_work, h, seg_q - cta_s0};
+    return MhaTile{cta_s0, cta_work, h, (qt0 + t) * MHA_QT};
+  };
+
+  if (!active) {
+    // nothing to do: straight to the teardown
+  } else if (warp >= 8) {
     ptx::setmaxnreg_dec<MHA_REGS_ISSUE>();  // warpgroup 2: TMA (warp 8), MMA (warp 9), 2 idle warps
   if (warp == 8) {
     // ------------------------------------------------ TMA producer
@@ -616,6 +634,12 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
       }
       if (list || t + 1 < nqt) named_bar_sync(pair_bar, 64);  // the pair's rows are stored: sOut free for the next tile
     }
+    if (p.flops != nullptr && warp_live) {
+      // instrumentation: half 0 of each row pair counts the row's keys
+      const unsigned keys = (half == 0 && row < rows_here) ? static_cast<unsigned>(ke - ks) : 0u;
+      const unsigned w = __reduce_add_sync(0xffffffffu, keys);
+      if (lane == 0 && w) atomicAdd(p.flops, 4ull * MHA_D * w);
+    }
     if (threadIdx.x == 0 && (t == 1 || t == 2)) MHA_TRACE(27 + t);  // tiles 1, 2 stored (slots 28, 29)
     if (list || t + 1 < nqt) {
       ptx::tc_fence_before();
@@ -631,7 +655,7 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, 256);
   }
-  if (list && threadIdx.x == 0) {
+  if (list && active && threadIdx.x == 0) {
     // every claim of this CTA precedes this point; the last CTA resets the
     // queue for the next launch
     const int participants = min(static_cast<int>(gridDim.x), nitems);
@@ -691,6 +715,10 @@ static int mha_list_mode() {
   return env;
 }
 
+// Instrumented FLOP counting (bt_flops_enable): device counter the MHA
+// tiles add their work to, null when off.
+unsigned long long* g_mha_flops = nullptr;
+
 int mha_launch(const void* qkv, const int32_t* seq_starts, int bs, int mx, int H, int d, int cutoff, int T,
                void* out, int force_path, cudaStream_t s, int padded, const void* sched) {
   BT_REQUIRE(d == MHA_D, BT_ECONFIG, "fused MHA supports head_size 64, got %d", d);
@@ -714,6 +742,7 @@ int mha_launch(const void* qkv, const int32_t* seq_starts, int bs, int mx, int H
   p.nsegs = nullptr;
   p.T = T;
   p.heads = H;
+  p.flops = g_mha_flops;
   BT_REQUIRE(!padded || T == bs * mx, BT_ESHAPE, "padded mha: qkv must have bs*mx = %d rows, got %d", bs * mx, T);
   const int nqt = (mx + MHA_QT - 1) / MHA_QT;
   // dispatch_mha rule (attention.py:309-314); the resident (short) kernel

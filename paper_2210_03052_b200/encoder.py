@@ -340,6 +340,7 @@ class BertEncoderB200:
         self._c_layers = (_lib.LayerWeightsC * n)(*[dl.c for dl in self._layers])
         self._cfg_c = layer_cfg_c(self.config)
         self._ws = None
+        self._ws_event = None
         self._graphs = {}
         # one forward at a time per engine: the workspace, the cached graphs
         # and their I/O buffers are shared state (the service runs requests on
@@ -350,10 +351,27 @@ class BertEncoderB200:
     def layer(self, i: int) -> DeviceLayer:
         return self._layers[i]
 
-    def workspace(self, nbytes: int):
+    def workspace(self, nbytes: int, stream=None):
+        """The shared activation workspace, ordered after its previous use:
+        a caller on another stream waits (on the device) for the last
+        launch that used it, so two threads on different streams never
+        overlap on it.  Call ``_ws_used(stream)`` after queueing the launch."""
+        torch = self.torch
+        s = stream if stream is not None else torch.cuda.current_stream()
+        if self._ws_event is not None and not torch.cuda.is_current_stream_capturing():
+            s.wait_event(self._ws_event)
         if self._ws is None or self._ws.numel() < nbytes:
-            self._ws = self.torch.empty(max(nbytes, 1), dtype=self.torch.uint8, device="cuda")
+            self._ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device="cuda")
         return self._ws
+
+    def _ws_used(self, stream=None):
+        torch = self.torch
+        if torch.cuda.is_current_stream_capturing():
+            return  # (graph replays are ordered by the stream they replay on)
+        s = stream if stream is not None else torch.cuda.current_stream()
+        if self._ws_event is None:
+            self._ws_event = torch.cuda.Event()
+        self._ws_event.record(s)
 
     def forward_device(self, lengths_dev, bs: int, T: int, x_padded_f32, out_padded_f32, stream=None,
                        config: ModelConfig | None = None):
@@ -363,10 +381,11 @@ class BertEncoderB200:
             cfg = config or self.config
             cfg_c = self._cfg_c if config is None else layer_cfg_c(cfg)
             ws_bytes = int(_lib.load().bt_forward_workspace_bytes(C.byref(cfg_c), bs, T))
-            ws = self.workspace(ws_bytes)
+            ws = self.workspace(ws_bytes, stream)
             _lib.call("bt_encoder_forward", self._c_layers, cfg.layers, C.byref(cfg_c), lengths_dev.data_ptr(), bs, T,
                       x_padded_f32.data_ptr(), out_padded_f32.data_ptr(), ws.data_ptr(), ws_bytes,
                       _lib.stream_ptr(stream))
+            self._ws_used(stream)
             return out_padded_f32
 
     def forward_ptrs(self, lengths_ptr: int, bs: int, T: int, x_ptr: int, out_ptr: int, stream=None,
@@ -378,9 +397,10 @@ class BertEncoderB200:
             cfg = config or self.config
             cfg_c = self._cfg_c if config is None else layer_cfg_c(cfg)
             ws_bytes = int(_lib.load().bt_forward_workspace_bytes(C.byref(cfg_c), bs, T))
-            ws = self.workspace(ws_bytes)
+            ws = self.workspace(ws_bytes, stream)
             _lib.call("bt_encoder_forward", self._c_layers, cfg.layers, C.byref(cfg_c), lengths_ptr, bs, T, x_ptr,
                       out_ptr, ws.data_ptr(), ws_bytes, _lib.stream_ptr(stream))
+            self._ws_used(stream)
 
     GRAPH_CACHE = 4  # batch shapes whose packed forward is kept as a CUDA graph
 
@@ -460,15 +480,23 @@ class BertEncoderB200:
             io.synchronize()
             return out_pinned
 
-    def layer_device(self, li: int, x_bf16, plan: PackingPlan, stream=None):
-        """In-place encoder_layer on a packed bf16 [T, k] device tensor."""
+    def layer_device(self, li: int, x_bf16, plan: PackingPlan, stream=None, config: ModelConfig | None = None):
+        """In-place encoder_layer on a packed bf16 [T, k] device tensor.
+
+        The MHA geometry comes from THIS call: max_seq_len from the plan (the
+        reference dispatches on plan.max_seq_len, attention.py:309-314),
+        cutoff / split_seq_len from ``config`` (default: the engine's), so a
+        cached engine never runs a later call with an earlier call's shape."""
         with self._lock:
+            cfg = as_model_config(config) if config is not None else self.config
+            cfg_c = layer_cfg_c(replace(cfg, max_seq_len=plan.max_seq_len))
             T = plan.valid_word_cnt
-            ws_bytes = int(_lib.load().bt_layer_workspace_bytes(C.byref(self._cfg_c), T))
-            ws = self.workspace(ws_bytes)
-            _lib.call("bt_encoder_layer", C.byref(self._layers[li].c), C.byref(self._cfg_c),
+            ws_bytes = int(_lib.load().bt_layer_workspace_bytes(C.byref(cfg_c), T))
+            ws = self.workspace(ws_bytes, stream)
+            _lib.call("bt_encoder_layer", C.byref(self._layers[li].c), C.byref(cfg_c),
                       plan.seq_starts_dev.data_ptr(), plan.batch_size, T, x_bf16.data_ptr(), ws.data_ptr(), ws_bytes,
                       _lib.stream_ptr(stream))
+            self._ws_used(stream)
             return x_bf16
 
 
@@ -506,20 +534,6 @@ def engine_for_layer(layer, config) -> BertEncoderB200:
     return _cached_engine(layer, geom, lambda: BertEncoderB200(EncoderWeights(layers=[layer], shared=False), config))
 
 
-def _count_flops(counter: FlopCounter | None, config: ModelConfig, seqs: SeqLengths, layers: int) -> None:
-    """Exact per-module counts the reference's instrumented kernels add
-    (tensor.py:198-199, attention.py:232-236): zero tolerance in bench --check."""
-    if counter is None:
-        return
-    k, T = config.hidden_dim, seqs.total
-    for _ in range(layers):
-        counter.add("gemm0", 3 * 2 * T * k * k)
-        counter.add("mha", sum(4 * n * n * config.head_size for n in seqs.lengths) * config.head_num)
-        counter.add("gemm1", 2 * T * k * k)
-        counter.add("gemm2", 2 * T * k * config.ffn_scale * k)
-        counter.add("gemm3", 2 * T * config.ffn_scale * k * k)
-
-
 def _is_all_on(flags) -> bool:
     return bool(flags.fuse_layernorm and flags.fuse_bias_gelu and flags.zero_padding and flags.fused_mha)
 
@@ -545,8 +559,14 @@ def encoder_layer(x, layer, config, plan, *, workers: int = 1, counter: FlopCoun
     device_mode = is_device(x)
     xb = x.to(torch.bfloat16).contiguous().clone() if device_mode else \
         torch.from_numpy(host_array(x)).to("cuda").to(torch.bfloat16)
-    eng.layer_device(0, xb, plan)
-    _count_flops(counter, config, plan.seqs, 1)
+    if counter is None:
+        eng.layer_device(0, xb, plan, config=config)
+    else:
+        from .instrument import LaunchFlops
+
+        with LaunchFlops() as lf:  # counts come from the launches themselves
+            eng.layer_device(0, xb, plan, config=config)
+        lf.add_to(counter)
     return xb.float() if device_mode else Tensor(xb.float().cpu().numpy())
 
 
@@ -574,20 +594,28 @@ def forward(weights, seqs, input_padded, config, *, workers: int = 1, counter: F
         return ladder.forward_variant(weights, seqs, input_padded, config, counter=counter)
     torch = _lib.require_device()
     eng = engine_for(weights, config)
-    if is_device(input_padded):
-        x = input_padded.to(torch.float32).contiguous()
+    if is_device(input_padded) or counter is not None:
+        x = input_padded.to(torch.float32).contiguous() if is_device(input_padded) else \
+            torch.from_numpy(np.ascontiguousarray(host_array(input_padded), dtype=np.float32)).to("cuda")
         lengths = torch.tensor(seqs.lengths, dtype=torch.int32).to(x.device)
         out = torch.empty((padded_rows, cols), dtype=torch.float32, device=x.device)
-        eng.forward_device(lengths, seqs.batch_size, seqs.total, x, out, config=config)
-        _count_flops(counter, config, seqs, config.layers)
-        return out
+        if counter is None:
+            eng.forward_device(lengths, seqs.batch_size, seqs.total, x, out, config=config)
+        else:
+            # instrumented FlopCounter: an eager forward whose launches count
+            # their own work (instrument.py), not the cached graph
+            from .instrument import LaunchFlops
+
+            with LaunchFlops() as lf:
+                eng.forward_device(lengths, seqs.batch_size, seqs.total, x, out, config=config)
+            lf.add_to(counter)
+        return out if is_device(input_padded) else Tensor(out.cpu().numpy())
     # Host I/O: DMA only each sequence's valid rows into a packed device
     # buffer, run packed -> packed, DMA the valid output rows back into their
     # padded positions, and zero the padded rows on the host while the GPU works.
     x_host = _pinned_f32(input_padded, torch)
     out = torch.empty((padded_rows, cols), dtype=torch.float32, pin_memory=True)
     eng.forward_host_packed(seqs, x_host, out, config=config)
-    _count_flops(counter, config, seqs, config.layers)
     return Tensor(out.numpy())
 
 

@@ -75,8 +75,13 @@ def layer_variant_device(dl, x, plan: PackingPlan, config, flags):
     from .fusion import bias_act_device, ln_device
     from .tensor import gemm_device
 
+    from .instrument import count_gemm
+
     k = config.hidden_dim
+    f = config.ffn_scale * k
+    m = int(x.shape[0])
     qkv = gemm_device(x, dl.qkv_w, dl.qkv_b, None, _lib.EPI_BIAS)  # Q/K/V biases (added on load in the reference)
+    count_gemm("gemm0", m, 3 * k, k)
     if not flags.zero_padding:
         attn = mha_padded_device(qkv, plan, config.head_num, config.head_size)
     elif not flags.fused_mha:
@@ -86,6 +91,7 @@ def layer_variant_device(dl, x, plan: PackingPlan, config, flags):
         attn = mha_device(qkv, plan, config.head_num, config.head_size, cutoff=config.cutoff,
                           split_seq_len=config.split_seq_len)
     proj = gemm_device(attn, dl.ao_w)
+    count_gemm("gemm1", m, k, k)
     if flags.fuse_layernorm:
         y0 = ln_device(proj, x, dl.ao_b, dl.ln0_g, dl.ln0_b, dl.ln0_eps)
     else:
@@ -94,7 +100,9 @@ def layer_variant_device(dl, x, plan: PackingPlan, config, flags):
         h1 = gemm_device(y0, dl.w1, dl.b1, None, _lib.EPI_BIAS_GELU)
     else:
         h1 = bias_act_device(gemm_device(y0, dl.w1), dl.b1, 1)
+    count_gemm("gemm2", m, f, k)
     h2 = gemm_device(h1, dl.w2)
+    count_gemm("gemm3", m, k, f)
     if flags.fuse_layernorm:
         return ln_device(h2, y0, dl.b2, dl.ln1_g, dl.ln1_b, dl.ln1_eps)
     return _ln_unfused(h2, y0, dl.b2, dl.ln1_g, dl.ln1_b, dl.ln1_eps)
@@ -116,24 +124,6 @@ def forward_variant_device(eng, plan: PackingPlan, x_padded_f32, config):
     return x.float()
 
 
-def _count(counter: FlopCounter | None, config, seqs, layers: int) -> None:
-    if counter is None:
-        return
-    from .encoder import _count_flops
-
-    if config.flags.zero_padding and config.flags.fused_mha:
-        _count_flops(counter, config, seqs, layers)
-        return
-    k = config.hidden_dim
-    m = seqs.total if config.flags.zero_padding else seqs.batch_size * seqs.max_seq_len
-    for _ in range(layers):
-        counter.add("gemm0", 6 * m * k * k)
-        counter.add("mha", 4 * seqs.batch_size * seqs.max_seq_len * seqs.max_seq_len * k)
-        counter.add("gemm1", 2 * m * k * k)
-        counter.add("gemm2", 2 * config.ffn_scale * m * k * k)
-        counter.add("gemm3", 2 * config.ffn_scale * m * k * k)
-
-
 def forward_variant(weights, seqs, input_padded, config, *, counter=None):
     """forward() for OptFlags other than all_on() (reference encoder.py:411-437)."""
     from .encoder import engine_for
@@ -144,8 +134,14 @@ def forward_variant(weights, seqs, input_padded, config, *, counter=None):
     device_mode = is_device(input_padded)
     x = input_padded.to(torch.float32).contiguous() if device_mode else torch.from_numpy(
         host_array(input_padded)).to("cuda")
-    out = forward_variant_device(eng, plan, x, config)
-    _count(counter, config, seqs, config.layers)
+    if counter is None:
+        out = forward_variant_device(eng, plan, x, config)
+    else:
+        from .instrument import LaunchFlops
+
+        with LaunchFlops() as lf:
+            out = forward_variant_device(eng, plan, x, config)
+        lf.add_to(counter)
     return out if device_mode else Tensor(out.cpu().numpy())
 
 
@@ -159,6 +155,12 @@ def encoder_layer_variant(x, layer, config, plan, *, counter=None):
     device_mode = is_device(x)
     xb = x.to(torch.bfloat16).contiguous() if device_mode else torch.from_numpy(host_array(x)).to("cuda").to(
         torch.bfloat16)
-    y = layer_variant_device(eng.layer(0), xb, plan, config, config.flags)
-    _count(counter, config, plan.seqs, 1)
+    if counter is None:
+        y = layer_variant_device(eng.layer(0), xb, plan, config, config.flags)
+    else:
+        from .instrument import LaunchFlops
+
+        with LaunchFlops() as lf:
+            y = layer_variant_device(eng.layer(0), xb, plan, config, config.flags)
+        lf.add_to(counter)
     return y.float() if device_mode else Tensor(y.float().cpu().numpy())

@@ -107,3 +107,55 @@ def gather_packed(local_packed, shards: list[Shard], group=None):
     parts = [torch.empty_like(buf) for _ in range(world)]
     dist.all_gather(parts, buf, group=group)
     return torch.cat([parts[s.rank][: s.tokens] for s in shards], dim=0)
+
+
+def forward_sharded(weights, seqs, input_padded, config, *, group=None, gather: bool = True):
+    """Multi-GPU encoder forward (reference
+    ``forward``, encoder.py:411-437, split over ranks).
+
+    Every rank holds the whole batch description and input; it runs the
+    padding-free GPU engine on its contiguous token-balanced shard of
+    sequences only (no collective on the hot path).  With ``gather`` the
+    valid output rows of every shard are all-gathered (``gather_packed``:
+    NCCL over NVLink, or gloo through host memory) and unpacked on the device
+    into the one padded ``[bs*mx, k]`` result the reference returns, on every
+    rank.  Without ``gather`` the rank's own padded shard output is returned.
+
+    Output type follows the input, as ``forward``: a CUDA tensor for a CUDA
+    input, a host ``Tensor`` otherwise.  Per-sequence results do not depend
+    on the partition when the forward runs the one-problem-per-tile MHA
+    (max_seq_len > 256 or batch > 256; the segment kernel that groups short
+    sequences for small batches shifts their keys inside a block, which
+    changes bf16 rounding only): tests/test_gpu_determinism.py."""
+    from dataclasses import replace
+
+    import torch
+    import torch.distributed as dist
+
+    from .encoder import as_model_config, forward
+    from .packing import as_seq_lengths, pack_device, plan_for_lengths, unpack_device
+    from .tensor import Tensor, host_array, is_device
+
+    config = as_model_config(config)
+    seqs = as_seq_lengths(seqs)
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    shards = token_balanced_partition(seqs.lengths, world, config.hidden_dim)
+    sh = shards[rank]
+    mx = seqs.max_seq_len
+    local_seqs = type(seqs).of(list(seqs.lengths[sh.start:sh.stop]), mx)
+    local_cfg = replace(config, batch_size=sh.batch_size)
+    device_io = is_device(input_padded)
+    if device_io:
+        x_local = input_padded[sh.start * mx: sh.stop * mx].to(torch.float32).contiguous()
+    else:
+        x_local = torch.from_numpy(np.ascontiguousarray(host_array(input_padded)[sh.start * mx: sh.stop * mx])).to(
+            "cuda")
+    y_local = forward(weights, local_seqs, x_local, local_cfg)  # CUDA fp32 [n_r*mx, k]
+    if not gather or world == 1:
+        return y_local if device_io else Tensor(y_local.cpu().numpy())
+    packed_local = pack_device(y_local, plan_for_lengths(local_seqs))  # [T_r, k] fp32
+    on_host = dist.get_backend(group) != "nccl"
+    g = gather_packed(packed_local.cpu() if on_host else packed_local, shards, group)
+    full = unpack_device(g.to("cuda"), plan_for_lengths(seqs))
+    return full if device_io else Tensor(full.cpu().numpy())

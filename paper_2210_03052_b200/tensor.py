@@ -242,15 +242,24 @@ def gemm(
             raise ShapeError(f"epilogue bias must have length {bn}, got {got}")
     torch = _lib.require_device()
     device_mode = is_device(a)
-    if ak % 64 or bn % 64:
-        raise ShapeError(f"B200 GEMM needs K and N multiples of 64, got K={ak} N={bn}")
     A = to_device_bf16(a, torch)
     Bt = weight_t_bf16(b, torch)
     bias = None
     if hook.kind in _EPI and hook.kind != EpilogueKind.NONE:
         bias = to_device_f32(np.asarray(hook.bias, np.float32).reshape(-1), torch)
-    C = gemm_device(A, Bt, bias, None, _EPI.get(hook.kind, _lib.EPI_NONE))
-    out = C.float()
+    # the kernel tiles K and N by 64: any other shape (the reference accepts
+    # every shape) runs zero-padded on the device -- zero K columns add
+    # nothing, padded N columns are sliced off
+    kp, np_ = -(-ak // 64) * 64, -(-bn // 64) * 64
+    if kp != ak:
+        A = torch.nn.functional.pad(A, (0, kp - ak))
+        Bt = torch.nn.functional.pad(Bt, (0, kp - ak))
+    if np_ != bn:
+        Bt = torch.nn.functional.pad(Bt, (0, 0, 0, np_ - bn))
+        if bias is not None:
+            bias = torch.nn.functional.pad(bias, (0, np_ - bn))
+    C = gemm_device(A.contiguous(), Bt.contiguous(), bias, None, _EPI.get(hook.kind, _lib.EPI_NONE))
+    out = C[:, :bn].float()
     if hook.kind == EpilogueKind.SCALE:
         out *= float(hook.scale)
     if counter is not None:

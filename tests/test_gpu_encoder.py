@@ -49,7 +49,7 @@ def test_forward_golden(bt, golden, tag, layers, heads, mx, bs, seed, kind):
     if kind == "init":
         assert_close_bf16(y, want, max_abs_max=2e-2, what=tag)
     else:
-        assert_close_bf16(y, want, max_abs_max=0.1 * rms(want) * 10, what=tag)
+        assert_close_bf16(y, want, max_abs_max=0.1 * rms(want), what=tag)
     pad = ~orc.build_mask(lens, mx).reshape(-1).astype(bool)
     assert not y.array[pad].any(), "padded rows must be exactly zero"
 
@@ -79,7 +79,7 @@ def test_forward_c2_vs_oracle(bt, kind):
         assert_close_bf16(y, want, max_abs_max=2e-2, what="C2 init")
     else:
         valid = orc.build_mask(lens, 256).reshape(-1).astype(bool)
-        assert_close_bf16(y.array[valid], want[valid], max_abs_max=10 * rms(want[valid]), what="C2 stress")
+        assert_close_bf16(y.array[valid], want[valid], max_abs_max=0.1 * rms(want[valid]), what="C2 stress")
 
 
 def test_forward_device_api_and_isolation(bt):

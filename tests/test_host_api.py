@@ -119,16 +119,17 @@ def test_forward_validates_before_compute():
         bt.forward(w, seqs, np.zeros((16, 64), np.float32), cfg)
 
 
-def test_flop_counter_matches_exact_model():
-    from paper_2210_03052_b200.encoder import _count_flops
+def test_flop_model_matches_oracle():
+    """The exact FLOP model bench --check compares the instrumented counts
+    with (flops.count, reference flops.py:72-110) agrees with the oracle's
+    restatement for the packed and the padded variants."""
+    from paper_2210_03052_b200 import flops
 
     lens = orc.gen_lengths(16, 256, "fixed", seed=0, alpha=0.6)
+    seqs = bt.SeqLengths.of(lens, 256)
     cfg = bt.preset_config("bert_base", 16, 256, bt.OptFlags.all_on())
-    c = bt.FlopCounter()
-    _count_flops(c, cfg, bt.SeqLengths.of(lens, 256), cfg.layers)
-    exact = orc.exact_flops(lens, 768)
-    for key, val in exact.items():
-        assert c.get(key) == val * cfg.layers
+    assert flops.count(cfg, seqs, "zero_padding_fused_mha").exact == orc.exact_flops(lens, 768)
+    assert flops.count(cfg, seqs, "baseline").exact == orc.exact_flops(lens, 768, fused=False, max_seq_len=256)
 
 
 def test_harness_generators_match_reference(golden):
