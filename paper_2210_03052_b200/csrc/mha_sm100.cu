@@ -636,7 +636,8 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
     }
     if (p.flops != nullptr && warp_live) {
       // instrumentation: half 0 of each row pair counts the row's keys
-      const unsigned keys = (half == 0 && row < rows_here) ? static_cast<unsigned>(ke - ks) : 0u;
+      // (padded mode computes the whole mx x mx rectangle, reference mha_baseline)
+      const unsigned keys = (half == 0 && row < rows_here) ? static_cast<unsigned>(p.padded ? work : ke - ks) : 0u;
       const unsigned w = __reduce_add_sync(0xffffffffu, keys);
       if (lane == 0 && w) atomicAdd(p.flops, 4ull * MHA_D * w);
     }
