@@ -109,7 +109,9 @@ def load(build_if_missing: bool = False) -> C.CDLL:
                 raise ImportError(
                     f"{LIB_PATH} is missing: build it with `python -m paper_2210_03052_b200.build` "
                     "(there is no CPU fallback)")
-        lib = C.CDLL(str(LIB_PATH), mode=os.RTLD_NOW | os.RTLD_GLOBAL)
+        # BT_LIB_PATH: an A/B build variant (scripts/ab_build.sh); default the in-tree library
+        path = os.environ.get("BT_LIB_PATH") or str(LIB_PATH)
+        lib = C.CDLL(path, mode=os.RTLD_NOW | os.RTLD_GLOBAL)
         for name, (res, args) in SIGNATURES.items():
             fn = getattr(lib, name)
             fn.restype = res

@@ -51,6 +51,32 @@ def up_to_date() -> bool:
     return all(p.stat().st_mtime <= t for p in _deps())
 
 
+def build_variant(out: Path, defines: list[str], verbose: bool = False) -> Path:
+    """A/B variant: every source rebuilt with extra -D defines into `out`
+    (objects under a per-variant directory); the in-tree library is untouched."""
+    out = Path(out).resolve()
+    obj_dir = out.parent / (out.stem + "_obj")
+    obj_dir.mkdir(parents=True, exist_ok=True)
+    cc = nvcc()
+    flags = NVCC_FLAGS + [f"-D{d}" for d in defines]
+
+    def compile_one(src: Path) -> Path:
+        obj = obj_dir / (src.stem + ".o")
+        cmd = [cc, *flags, "-c", str(src), "-o", str(obj)]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"nvcc failed on {src.name}:\n{r.stdout}\n{r.stderr}")
+        return obj
+
+    with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
+        objs = list(ex.map(compile_one, _sources()))
+    r = subprocess.run([cc, *ARCH, "-shared", "-o", str(out), *map(str, objs), "-cudart", "static"],
+                       capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+    return out
+
+
 def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and up_to_date():
         return LIB
@@ -84,6 +110,11 @@ def build(force: bool = False, verbose: bool = False) -> Path:
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
+    ap.add_argument("--variant", default=None, help="build an A/B variant library at this path")
+    ap.add_argument("-D", dest="defines", action="append", default=[], help="extra -D define for --variant")
     a = ap.parse_args()
+    if a.variant:
+        print(build_variant(Path(a.variant), a.defines, verbose=True))
+        sys.exit(0)
     print(build(force=a.force, verbose=True))
     sys.exit(0)

@@ -64,7 +64,8 @@ struct GemmParams {
 // is installed with bt_debug_gemm_trace): 64 u64 globaltimer stamps per CTA.
 //   [0] setup done, [1] producer start, then per segment it (< 10):
 //   [2+6it] mma begin, [3+6it] mma last commit, [4+6it] epi begin,
-//   [5+6it] epi end, [6+6it] tile id
+//   [5+6it] epi end, [6+6it] tile id; [62] producer past griddepcontrol.wait,
+//   [63] first k-block landed (MMA warp)
 __device__ unsigned long long* g_gemm_trace = nullptr;
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -299,6 +300,7 @@ __global__ void __launch_bounds__(GemmCfg<PAIR, BN, EW>::THREADS, 1)
       }
     }
     ptx::griddep_wait();  // A (activations) is produced by the previous kernel
+    if (lane == 0) BT_TRACE(62, gtimer());
     int stage = 0;
     uint32_t phase = 0;
     int count = 0;  // k-blocks issued so far by this CTA
@@ -357,6 +359,7 @@ __global__ void __launch_bounds__(GemmCfg<PAIR, BN, EW>::THREADS, 1)
         for (int kb = sg.kb0; kb < sg.kb1; ++kb) {
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
+          if (it == 0 && kb == sg.kb0 && lane == 0) BT_TRACE(63, gtimer());
           const uint64_t ad0 = ptx::sdesc_sw128(a_base + stage * Cfg::A_BYTES, 1024, 16);
           const uint64_t bd0 = ptx::sdesc_sw128(b_base + stage * Cfg::B_BYTES, 1024, 16);
           if (ptx::elect_one()) {

@@ -1,12 +1,18 @@
-# A/B: bench the working tree against a copy of HEAD built under _ab/
-# usage: bash scripts/ab_bench.sh [configs...]   (default: c2 c3)
+#!/bin/bash
+# A/B of library variants on the C2 (or $CFG) step: bench.py per variant, alternated.
+#   bash scripts/ab_bench.sh "name=path name2=path2" [rounds]
 cd $GRAFT_REPO_ROOT
-CFGS=${@:-c2 c3}
-for i in 1 2 3; do
- for v in new old; do
-  if [ $v = new ]; then D=.; else D=_ab; fi
-  for c in $CFGS; do
-   (cd $D && timeout -s KILL 300 python bench.py --config $c --no-cpu-baseline 2>/dev/null | python -c "import sys,json; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('$v $c', d['ms_per_step'], d['e2e']['value'], d['clocks']['sm_mhz'], d['clocks']['reasons'], {k: round(v['us'],2) for k, v in d.get('kernels',{}).items() if k.startswith('gemm')})")
+CFG=${CFG:-c2}
+for r in $(seq 1 ${2:-2}); do
+  for kv in $1; do
+    name=${kv%%=*}; lib=${kv#*=}
+    [ "$lib" = "default" ] && lib=""
+    BT_LIB_PATH=$lib python bench.py --config $CFG --steps 30 --warmup 5 --no-e2e --no-cpu-baseline > gpurun_out/ab_${name}_$r.json 2> gpurun_out/ab_${name}_$r.err
+    python - "$name" "gpurun_out/ab_${name}_$r.json" <<'PY'
+import json, sys
+d = json.loads(open(sys.argv[2]).read().strip().splitlines()[-1])
+k = d["kernels"]
+print(sys.argv[1], "ms/step", d["ms_per_step"], " ".join(f"{n}={v['us']:.2f}" for n, v in k.items()))
+PY
   done
- done
 done

@@ -41,11 +41,16 @@ def main():
     t0 = t[used, 0].min()
     rel = lambda x: (x - t0) / 1e3  # noqa: E731
     print(f"CTAs traced: {used.sum()}  setup-done spread: {rel(t[used, 0]).min():.2f}..{rel(t[used, 0]).max():.2f} us")
+    w = t[used, 62]
+    f = t[used, 63]
+    if (w > 0).any():
+        print(f"griddep_wait returned: {rel(w[w > 0]).min():.2f}..{rel(w[w > 0]).max():.2f} us; first k-block landed: "
+              f"median {np.median(rel(f[f > 0])):.2f} us")
     last = []
     for c in np.nonzero(used)[0][:6].tolist() + np.nonzero(used)[0][-3:].tolist():
         row = t[c]
         s = f"cta {c:3d}: setup {rel(row[0]):6.2f}"
-        for it in range(10):
+        for it in range(9):
             mb, me, eb, ee = row[2 + 6 * it:6 + 6 * it]
             if mb == 0 and eb == 0:
                 break
@@ -54,15 +59,15 @@ def main():
     ends = []
     for c in np.nonzero(used)[0]:
         row = t[c]
-        e = max(row[5 + 6 * it] for it in range(10) if row[5 + 6 * it] > 0) if any(
-            row[5 + 6 * it] > 0 for it in range(10)) else row[0]
+        e = max(row[5 + 6 * it] for it in range(9) if row[5 + 6 * it] > 0) if any(
+            row[5 + 6 * it] > 0 for it in range(9)) else row[0]
         ends.append(rel(e))
     print(f"CTA finish times: min {min(ends):.2f} median {np.median(ends):.2f} max {max(ends):.2f} us")
     mm = []
     ep = []
     for c in np.nonzero(used)[0]:
         row = t[c]
-        for it in range(10):
+        for it in range(9):
             mb, me, eb, ee = row[2 + 6 * it:6 + 6 * it]
             if mb > 0 and me > 0:
                 mm.append((me - mb) / 1e3)
