@@ -12,17 +12,14 @@
 // that a one-tile-per-CTA launch pays in full (Q load ~0.4 us, first S ~0.5 us,
 // epilogue ~0.6 us, CTA turnover) is hidden behind the softmax.
 //
-// Per CTA (384 threads, two per SM):
-//   warps 0-7   softmax + epilogue: a warp owns 16 query rows (TMEM lanes)
-//               and TWO threads per row, lanes t and t + 16 -- the
-//               tcgen05.ld/st .16x32bx2 shape hands thread t keys 0-63 and
-//               thread t + 16 keys 64-127 of the row's block, so the row max
-//               and row sum combine with one shuffle (no shared memory, no
-//               barrier); P goes to TMEM as bf16 (the A operand of
-//               O += P V); O / l -> bf16 -> smem -> coalesced 16 B stores
-//   warp 8      TMA producer: unit claims, Q (double-buffered), K / V ring
-//   warp 9      tcgen05.mma issuer (elect.sync): S = Q K^T, O += P V
-//   warps 10-11 idle (complete warpgroup 2 for setmaxnreg)
+// Per CTA (256 threads, two per SM):
+//   warps 0-3   softmax + epilogue, thread = query row = TMEM lane: a row's
+//               128 scores of a key block are in one thread's registers (no
+//               cross-thread row max), P goes to TMEM as bf16 (the A operand
+//               of O += P V), O / l -> bf16 -> smem -> coalesced 16 B stores
+//   warp 4      TMA producer: unit claims, Q (double-buffered), K / V ring
+//   warp 5      tcgen05.mma issuer (elect.sync): S = Q K^T, O += P V
+//   warps 6-7   idle (complete warpgroup 1 for setmaxnreg)
 // TMEM (256 columns): S [0,128) fp32, P [128,192) bf16 pairs, O [192,256).
 // Softmax: single pass with a lazily moved reference max (it moves only when
 // the block max exceeds it by 2^8 in P units, then O and the row sum are
@@ -44,9 +41,9 @@ namespace bt {
 constexpr int M2_D = 64;
 constexpr int M2_BLK = 128;                  // keys per block = query rows per tile
 constexpr uint32_t M2_TILE = 128 * 128;      // bytes of one 128 x 64 bf16 tile
-constexpr int M2_THREADS = 384;
-constexpr int M2_REGS_SOFTMAX = 104;         // 256 x 104 + 128 x 32 = 30720 = 384 x 80: two CTAs per SM
-constexpr int M2_REGS_ISSUE = 32;
+constexpr int M2_THREADS = 256;
+constexpr int M2_REGS_SOFTMAX = 200;         // 128 x 200 + 128 x 56 = 32768: two CTAs per SM
+constexpr int M2_REGS_ISSUE = 56;
 constexpr float M2_RESCALE_LOG2 = 8.0f;
 #ifndef BT_MHA2_POLY
 #define BT_MHA2_POLY 2  // of every 16 exponentials, this many run as ex2_poly2 on the FMA pipe
@@ -126,10 +123,10 @@ __global__ void __launch_bounds__(M2_THREADS, 2) mha2_fwd_kernel(const __grid_co
       ptx::mbar_init(&kv_empty[i], 1);
     }
     ptx::mbar_init(s_full, 1);
-    ptx::mbar_init(s_read, 256);
-    ptx::mbar_init(p_full, 256);
+    ptx::mbar_init(s_read, 128);
+    ptx::mbar_init(p_full, 128);
     ptx::mbar_init(pv_done, 1);
-    ptx::mbar_init(o_free, 256);
+    ptx::mbar_init(o_free, 128);
     for (int i = 0; i < 4; ++i) ring[i] = 0xFFFFFFFFu;  // tag 0xFF: nothing published yet
     ptx::fence_mbar_init();
   }
@@ -159,9 +156,9 @@ __global__ void __launch_bounds__(M2_THREADS, 2) mha2_fwd_kernel(const __grid_co
 
   if (!active) {
     // no unit for this CTA: straight to the teardown
-  } else if (warp >= 8) {
+  } else if (warp >= 4) {
     ptx::setmaxnreg_dec<M2_REGS_ISSUE>();
-    if (warp == 8) {
+    if (warp == 4) {
       // ------------------------------------------------ TMA producer
       int kvg = 0;  // K / V blocks loaded so far (ring position)
       for (int t = 0;; ++t) {
@@ -199,7 +196,7 @@ __global__ void __launch_bounds__(M2_THREADS, 2) mha2_fwd_kernel(const __grid_co
           __syncwarp();
         }
       }
-    } else if (warp == 9) {
+    } else if (warp == 5) {
       // ------------------------------------------------ MMA issuer
       constexpr uint32_t idesc_s = ptx::idesc_bf16(128, M2_BLK, false, false);  // Q K^T, both K-major
       constexpr uint32_t idesc_o = ptx::idesc_bf16(128, M2_D, false, true);     // P (TMEM) x V (MN-major)
@@ -257,22 +254,21 @@ __global__ void __launch_bounds__(M2_THREADS, 2) mha2_fwd_kernel(const __grid_co
   } else {
     ptx::setmaxnreg_inc<M2_REGS_SOFTMAX>();
     // ------------------------------------------------ softmax + epilogue
-    const int quarter = warp & 3, sub = warp >> 2, half = lane >> 4;
-    const int lane0 = quarter * 32 + sub * 16;  // first TMEM lane (query row) of this warp
-    const int row = lane0 + (lane & 15);        // my query row; keys half * 64 .. + 63 of each block
-    const uint32_t trow = tmem + (static_cast<uint32_t>(lane0) << 16);
+    const int row = threadIdx.x;  // query row of the tile == TMEM lane
+    const uint32_t trow = tmem + (static_cast<uint32_t>(warp * 32) << 16);
     const float sl2 = p.sl2;
     int g = 0;
     for (int t = 0;; ++t) {
       const M2Unit w = unit_at(t);
       if (w.qrows == 0) break;
       const int nkb = (w.kvlen + M2_BLK - 1) / M2_BLK;
-      const bool warp_live = lane0 < w.qrows;
+      const bool warp_live = warp * 32 < w.qrows;
       const bool row_ok = row < w.qrows;
-      // my row's keys [ks, ke) relative to the unit's first key: a group's
-      // rows see only their own sequence
+      // my keys [ks, ke) relative to the unit's first key: a group's rows
+      // see only their own sequence
       int ks = 0, ke = w.kvlen;
-      if (w.sa < w.sb) {
+      const bool grouped = w.sa < w.sb;
+      if (grouped) {
         if (row_ok) {
           const int r = w.q0 + row;
           int lo = w.sa, hi = w.sb;
@@ -288,39 +284,43 @@ __global__ void __launch_bounds__(M2_THREADS, 2) mha2_fwd_kernel(const __grid_co
       }
       float mref = -INFINITY, lsum = 0.f;
       for (int j = 0; j < nkb; ++j, ++g) {
-        // my 64 keys of this block are key0 .. key0 + 63 of the unit's block j;
-        // the valid ones [klo, khi) in my local numbering
-        const int klo = ks - j * M2_BLK - half * 64, khi = min(ke - j * M2_BLK - half * 64, 64);
+        const int klo = ks - j * M2_BLK, khi = min(ke - j * M2_BLK, M2_BLK);  // my valid keys of this block
         ptx::mbar_wait(s_full, g & 1);
         ptx::tc_fence_after();
-        uint32_t a[32], b[32];  // my 64 scores
-        if (warp_live) {
-          ptx::tmem_ld_16x2_32<64>(trow + S_COL, a);
-          ptx::tmem_ld_16x2_32<64>(trow + S_COL + 32, b);
-          ptx::tmem_wait_ld(a);
-          m2_tie(b);
-        }
+        // Pass 1: the row max, 64 scores at a time (a thread holds a whole
+        // row: 128 scores would not fit next to the pipeline's registers at
+        // two CTAs per SM).  Pass 2 reloads each half for its exponentials;
+        // TMEM reads are cheap (~860 B/clk/SM measured, scripts/micro/tmem_bw.cu).
+        const bool masked = klo > 0 || khi < M2_BLK;
+        auto mask64 = [&](uint32_t (&a)[32], uint32_t (&b)[32], int base) {
+          // keys outside my row's problem: s = -inf (out of the max; exp -> 0)
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            if (base + i < klo || base + i >= khi) a[i] = 0xff800000u;
+            if (base + 32 + i < klo || base + 32 + i >= khi) b[i] = 0xff800000u;
+          }
+        };
         bool need = false;
         float alpha = 1.f;
         if (warp_live) {
-          if (klo > 0 || khi < 64) {
-            // keys outside my row's problem: s = -inf (out of the max; exp -> 0)
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              if (i < klo || i >= khi) a[i] = 0xff800000u;
-              if (32 + i < klo || 32 + i >= khi) b[i] = 0xff800000u;
-            }
-          }
           float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-          for (int i = 0; i < 32; i += 4) {
-            m4[0] = ptx::max3(m4[0], __uint_as_float(a[i]), __uint_as_float(a[i + 1]));
-            m4[1] = ptx::max3(m4[1], __uint_as_float(a[i + 2]), __uint_as_float(a[i + 3]));
-            m4[2] = ptx::max3(m4[2], __uint_as_float(b[i]), __uint_as_float(b[i + 1]));
-            m4[3] = ptx::max3(m4[3], __uint_as_float(b[i + 2]), __uint_as_float(b[i + 3]));
+          for (int hf = 0; hf < 2; ++hf) {
+            uint32_t a[32], b[32];
+            ptx::tmem_ld32(trow + S_COL + 64 * hf, a);
+            ptx::tmem_ld32(trow + S_COL + 64 * hf + 32, b);
+            ptx::tmem_wait_ld(a);
+            m2_tie(b);
+            if (masked) mask64(a, b, 64 * hf);
+#pragma unroll
+            for (int i = 0; i < 32; i += 4) {
+              m4[0] = ptx::max3(m4[0], __uint_as_float(a[i]), __uint_as_float(a[i + 1]));
+              m4[1] = ptx::max3(m4[1], __uint_as_float(a[i + 2]), __uint_as_float(a[i + 3]));
+              m4[2] = ptx::max3(m4[2], __uint_as_float(b[i]), __uint_as_float(b[i + 1]));
+              m4[3] = ptx::max3(m4[3], __uint_as_float(b[i + 2]), __uint_as_float(b[i + 3]));
+            }
           }
-          float bmax = fmaxf(ptx::max3(m4[0], m4[1], m4[2]), m4[3]);
-          bmax = fmaxf(bmax, __shfl_xor_sync(0xffffffffu, bmax, 16));  // the row's other 64 keys
+          const float bmax = fmaxf(ptx::max3(m4[0], m4[1], m4[2]), m4[3]);
           const float mnew = fmaxf(mref, bmax);
           need = (mnew - mref) * sl2 > M2_RESCALE_LOG2;  // true on the first block with a key (mref = -inf)
           alpha = (need && mref != -INFINITY) ? ptx::ex2_approx((mref - mnew) * sl2) : 1.f;
@@ -330,73 +330,78 @@ __global__ void __launch_bounds__(M2_THREADS, 2) mha2_fwd_kernel(const __grid_co
           ptx::mbar_wait(pv_done, (g - 1) & 1);  // P(g-1) V(g-1) is in O; the P columns are free
           ptx::tc_fence_after();
         }
-        if (warp_live) {
-          if (__any_sync(0xffffffffu, need && j > 0)) {
-            // the reference max moved (rare): my 32 O columns *= 2^((m_old - m_new) * scale)
-            const unsigned long long a2 = ptx::f2(alpha, alpha);
+        if (warp_live && __any_sync(0xffffffffu, need && j > 0)) {
+          // the reference max moved (rare): my O row *= 2^((m_old - m_new) * scale)
+          const unsigned long long a2 = ptx::f2(alpha, alpha);
+#pragma unroll
+          for (int hf = 0; hf < 2; ++hf) {
             uint32_t o[32];
-            ptx::tmem_ld_16x2_32<32>(trow + O_COL, o);
+            ptx::tmem_ld32(trow + O_COL + 32 * hf, o);
             ptx::tmem_wait_ld(o);
 #pragma unroll
             for (int i = 0; i < 32; i += 2) {
-              float x, y;
-              ptx::unf2(ptx::mul2(ptx::f2(__uint_as_float(o[i]), __uint_as_float(o[i + 1])), a2), x, y);
-              o[i] = __float_as_uint(x);
-              o[i + 1] = __float_as_uint(y);
+              float a, c;
+              ptx::unf2(ptx::mul2(ptx::f2(__uint_as_float(o[i]), __uint_as_float(o[i + 1])), a2), a, c);
+              o[i] = __float_as_uint(a);
+              o[i + 1] = __float_as_uint(c);
             }
-            ptx::tmem_st_16x2_32<32>(trow + O_COL, o);
+            ptx::tmem_st32(trow + O_COL + 32 * hf, o);
           }
-          // P = 2^((s - m_ref) * scale * log2 e).  (A row with no key in the
-          // blocks so far keeps m_ref = -inf; its scores are all -inf, so any
-          // finite offset gives P = 0.)
-          const float msc = (mref == -INFINITY) ? 0.f : mref * sl2;
-          const unsigned long long sl2x2 = ptx::f2(sl2, sl2), nm2 = ptx::f2(-msc, -msc);
-          unsigned long long sum4[4] = {0ull, 0ull, 0ull, 0ull};
-          // keys half * 64 + 32c .. -> P columns half * 32 + 16c .. (bf16 pairs)
-#define M2_EXPS32(V, C)                                                                                     \
-  {                                                                                                         \
-    uint32_t pp[16];                                                                                        \
-    const bool empty = 32 * (C) >= khi || 32 * (C) + 32 <= klo;                                             \
-    if (__all_sync(0xffffffffu, empty)) { /* no key of any row here: P = 0, no exponentials */              \
-      _Pragma("unroll") for (int i = 0; i < 16; ++i) pp[i] = 0u;                                            \
-    } else {                                                                                                \
-      _Pragma("unroll") for (int i = 0; i < 32; i += 2) {                                                   \
-        float x0, x1, e0, e1;                                                                               \
-        ptx::unf2(ptx::fma2(ptx::f2(__uint_as_float(V[i]), __uint_as_float(V[i + 1])), sl2x2, nm2), x0, x1); \
-        if ((i & 15) < BT_MHA2_POLY) {                                                                      \
-          ptx::ex2_poly2(x0, x1, e0, e1); /* masked key (x = -inf): exactly 0 */                            \
-        } else {                                                                                            \
-          e0 = ptx::ex2_approx(x0); /* ex2(-inf) = 0 */                                                     \
-          e1 = ptx::ex2_approx(x1);                                                                         \
-        }                                                                                                   \
-        sum4[(i >> 1) & 3] = ptx::add2(sum4[(i >> 1) & 3], ptx::f2(e0, e1));                                \
-        pp[i / 2] = ptx::pack_bf16x2(e0, e1);                                                               \
-      }                                                                                                     \
-    }                                                                                                       \
-    ptx::tmem_st_16x2_16<32>(trow + P_COL + 16 * (C), pp);                                                  \
-  }
-          M2_EXPS32(a, 0)
-          // my keys 32-63 again from TMEM (cheaper than holding them through
-          // the first half's exponentials: the registers are the softmax's bound)
-          ptx::tmem_ld_16x2_32<64>(trow + S_COL + 32, b);
-          ptx::tmem_wait_ld(b);
-          ptx::tc_fence_before();
-          ptx::mbar_arrive(s_read);  // every score of this block is read: the MMA warp may write S(g+1)
-          if (klo > 32 || khi < 64) {
+        }
+        // Pass 2: P = 2^((s - m_ref) * scale * log2 e), 64 keys at a time.
+        // (a row with no key in the blocks so far keeps m_ref = -inf; its
+        // scores are all -inf, so any finite offset gives P = 0)
+        const float msc = (mref == -INFINITY) ? 0.f : mref * sl2;
+        const unsigned long long sl2x2 = ptx::f2(sl2, sl2), nm2 = ptx::f2(-msc, -msc);
+        unsigned long long sum4[4] = {0ull, 0ull, 0ull, 0ull};
 #pragma unroll
-            for (int i = 0; i < 32; ++i)
-              if (32 + i < klo || 32 + i >= khi) b[i] = 0xff800000u;
+        for (int hf = 0; hf < 2; ++hf) {
+          uint32_t a[32], b[32];
+          if (warp_live) {
+            ptx::tmem_ld32(trow + S_COL + 64 * hf, a);
+            ptx::tmem_ld32(trow + S_COL + 64 * hf + 32, b);
+            ptx::tmem_wait_ld(a);
+            m2_tie(b);
           }
-          M2_EXPS32(b, 1)
-#undef M2_EXPS32
+          if (hf == 1) {
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(s_read);  // every S value is read: the MMA warp may write the next block's S
+          }
+          if (!warp_live) continue;
+          if (masked) mask64(a, b, 64 * hf);
+#pragma unroll
+          for (int c2 = 0; c2 < 2; ++c2) {
+            uint32_t (&v)[32] = c2 == 0 ? a : b;
+            const int key0 = 64 * hf + 32 * c2;
+            uint32_t pp[16];  // 32 keys as bf16 pairs -> P columns key0 / 2 ..
+            const bool empty = key0 >= khi || key0 + 32 <= klo;
+            if (__all_sync(0xffffffffu, empty)) {  // no key of any row here: P = 0, no exponentials
+#pragma unroll
+              for (int i = 0; i < 16; ++i) pp[i] = 0u;
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; i += 2) {
+                float x0, x1, e0, e1;
+                ptx::unf2(ptx::fma2(ptx::f2(__uint_as_float(v[i]), __uint_as_float(v[i + 1])), sl2x2, nm2), x0, x1);
+                if ((i & 15) < BT_MHA2_POLY) {
+                  ptx::ex2_poly2(x0, x1, e0, e1);  // masked key (x = -inf): exactly 0
+                } else {
+                  e0 = ptx::ex2_approx(x0);  // ex2(-inf) = 0
+                  e1 = ptx::ex2_approx(x1);
+                }
+                sum4[(i >> 1) & 3] = ptx::add2(sum4[(i >> 1) & 3], ptx::f2(e0, e1));
+                pp[i / 2] = ptx::pack_bf16x2(e0, e1);
+              }
+            }
+            ptx::tmem_st16(trow + P_COL + key0 / 2, pp);
+          }
+        }
+        if (warp_live) {
           const unsigned long long bsum2 = ptx::add2(ptx::add2(sum4[0], sum4[1]), ptx::add2(sum4[2], sum4[3]));
           float s0f, s1f;
           ptx::unf2(bsum2, s0f, s1f);
-          lsum = lsum * alpha + (s0f + s1f);  // my keys' partial row sum
+          lsum = lsum * alpha + (s0f + s1f);
           ptx::tmem_wait_st();
-        } else {
-          ptx::tc_fence_before();
-          ptx::mbar_arrive(s_read);
         }
         ptx::tc_fence_before();
         ptx::mbar_arrive(p_full);
@@ -404,52 +409,47 @@ __global__ void __launch_bounds__(M2_THREADS, 2) mha2_fwd_kernel(const __grid_co
       // ---- epilogue: O / l -> bf16 rows -> staging -> 16-byte coalesced stores
       ptx::mbar_wait(pv_done, (g - 1) & 1);  // this unit's last P V
       ptx::tc_fence_after();
-      uint32_t o[32];  // my 32 of the row's 64 output dims
+      uint32_t o0[32], o1[32];
       if (warp_live) {
-        ptx::tmem_ld_16x2_32<32>(trow + O_COL, o);
-        ptx::tmem_wait_ld(o);
+        ptx::tmem_ld32(trow + O_COL, o0);
+        ptx::tmem_ld32(trow + O_COL + 32, o1);
+        ptx::tmem_wait_ld(o0);
+        m2_tie(o1);
       }
       ptx::tc_fence_before();
       ptx::mbar_arrive(o_free);  // the next unit's first P V may overwrite O
-      // re-read the unit from the ring (an atomic: nothing derived from it can
-      // be hoisted above this point), so the store addresses are not kept live
-      // across the block loop -- that cost the block loop its registers
-      const M2Unit we = unit_at(t);
       if (warp_live) {
-        const bool row_ok2 = row < we.qrows;
-        const float l = lsum + __shfl_xor_sync(0xffffffffu, lsum, 16);
-        const float inv = row_ok2 ? 1.0f / l : 0.f;
+        const float inv = row_ok ? 1.0f / lsum : 0.f;
         const unsigned long long inv2 = ptx::f2(inv, inv);
-        // two passes of 16 columns keep fewer values live
+        uint8_t* mine = sOut + row * 128;
 #pragma unroll
-        for (int jj = 0; jj < 4; ++jj) {
+        for (int jj = 0; jj < 8; ++jj) {
           uint32_t wv[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            float x, y;
-            ptx::unf2(ptx::mul2(ptx::f2(__uint_as_float(o[8 * jj + 2 * e]), __uint_as_float(o[8 * jj + 2 * e + 1])),
-                                inv2),
-                      x, y);
-            wv[e] = ptx::pack_bf16x2(x, y);
+            const int k = 8 * jj + 2 * e;
+            const uint32_t lo = k < 32 ? o0[k] : o1[k - 32], hi = k < 32 ? o0[k + 1] : o1[k - 31];
+            float a, b2;
+            ptx::unf2(ptx::mul2(ptx::f2(__uint_as_float(lo), __uint_as_float(hi)), inv2), a, b2);
+            wv[e] = ptx::pack_bf16x2(a, b2);
           }
-          const int chunk = half * 4 + jj;
-          *reinterpret_cast<uint4*>(sOut + row * 128 + ((chunk ^ (row & 7)) << 4)) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+          *reinterpret_cast<uint4*>(mine + ((jj ^ (row & 7)) << 4)) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
         }
-        __syncwarp();  // this warp's 16 rows are staged
-        // lane -> (row of the warp's 16, 16 B chunk): 4 rows per store instruction
+        __syncwarp();  // this warp's 32 rows are staged
+        // lane -> (row of the warp's slab, 16 B chunk): 4 rows per store instruction
 #pragma unroll
-        for (int it = 0; it < 4; ++it) {
-          const int rr = lane0 + it * 4 + (lane >> 3);
+        for (int it = 0; it < 8; ++it) {
+          const int rr = warp * 32 + it * 4 + (lane >> 3);
           const int jj = lane & 7;
-          if (rr < we.qrows) {
+          if (rr < w.qrows) {
             const uint4 v = *reinterpret_cast<const uint4*>(sOut + rr * 128 + ((jj ^ (rr & 7)) << 4));
-            *reinterpret_cast<uint4*>(p.out + static_cast<size_t>(we.q0 + rr) * p.hidden + we.h * M2_D + jj * 8) = v;
+            *reinterpret_cast<uint4*>(p.out + static_cast<size_t>(w.q0 + rr) * p.hidden + w.h * M2_D + jj * 8) = v;
           }
         }
         __syncwarp();  // the slab is read: the next unit may stage into it
         if (p.flops != nullptr) {
           // instrumentation: 4 * d FLOPs per (row, key of its own problem)
-          const unsigned keys = (half == 0 && row_ok2) ? static_cast<unsigned>(ke - ks) : 0u;
+          const unsigned keys = row_ok ? static_cast<unsigned>(ke - ks) : 0u;
           const unsigned sumk = __reduce_add_sync(0xffffffffu, keys);
           if (lane == 0 && sumk) atomicAdd(p.flops, 4ull * M2_D * sumk);
         }

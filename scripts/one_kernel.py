@@ -39,19 +39,6 @@ def main():
         qkv = torch.randn(plan.valid_word_cnt, 3 * H * 64, device="cuda").to(torch.bfloat16)
         for _ in range(3):
             mha_device(qkv, plan, H, 64)
-    elif kind == "mha2":  # the forward's MHA call: bt_plan_sched schedule + bt_mha_varlen_sched
-        cfgs = {"c2": (16, 256, 12), "c3": (16, 512, 16), "c5": (2048, 512, 16)}
-        bs, mx, H = cfgs[sys.argv[2]]
-        seqs = harness.gen_lengths(bs, mx, "fixed", seed=0, alpha=0.6)
-        plan = plan_for_lengths(seqs)
-        T = plan.valid_word_cnt
-        qkv = torch.randn(T, 3 * H * 64, device="cuda").to(torch.bfloat16)
-        sched = torch.zeros(_lib.load().bt_plan_sched_bytes(bs, mx) // 4 + 4, dtype=torch.int32, device="cuda")
-        _lib.call("bt_plan_sched", plan.seq_starts_dev.data_ptr(), bs, mx, sched.data_ptr(), _lib.stream_ptr())
-        out = torch.empty(T, H * 64, device="cuda", dtype=torch.bfloat16)
-        for _ in range(3):
-            _lib.call("bt_mha_varlen_sched", qkv.data_ptr(), plan.seq_starts_dev.data_ptr(), sched.data_ptr(), bs, mx,
-                      H, 64, 384, out.data_ptr(), T, _lib.stream_ptr())
     elif kind == "ln":
         from paper_2210_03052_b200.fusion import ln_device
 
