@@ -256,11 +256,6 @@ BT_API int bt_debug_mha_seg(int mode);
 BT_API int bt_debug_mha_occupancy(int which, int* info);
 /* Debug hook: per-CTA globaltimer event trace of the MHA kernels (32 u64 slots per CTA). */
 BT_API int bt_debug_mha_trace(unsigned long long* buf);
-/* Test hooks of the persistent MHA (csrc/mha2_sm100.cu): 1 / 0 selects it or
- * the per-policy kernels of mha_sm100.cu for the forward (-1: the BT_MHA_V2
- * policy); pin its grid (0: one CTA per resident slot). */
-BT_API int bt_debug_mha_v2(int mode);
-BT_API int bt_debug_mha2_grid(int grid);
 
 /* Instrumented FlopCounter (replaces the counter.add calls of reference
  * tensor.py:198-199 / attention.py:232-236 with launch-level counting).

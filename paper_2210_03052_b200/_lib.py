@@ -87,8 +87,6 @@ SIGNATURES = {
     "bt_debug_forward_events": (_I, [_P, _I]),
     "bt_mha_varlen_path": (_I, [_P, _P, _I, _I, _I, _I, _P, _I, _I, _S]),
     "bt_flops_enable": (_I, [_P]),
-    "bt_debug_mha_v2": (_I, [_I]),
-    "bt_debug_mha2_grid": (_I, [_I]),
     "bt_flops_read": (_I, [_P]),
 }
 

@@ -720,33 +720,9 @@ static int mha_list_mode() {
 // tiles add their work to, null when off.
 unsigned long long* g_mha_flops = nullptr;
 
-int mha2_launch(const void* qkv, const int32_t* seq_starts, const void* sched, int bs, int mx, int H, int d, int T,
-                void* out, cudaStream_t s);
-
-// BT_MHA_V2=0 (A/B) or bt_debug_mha_v2(0): the forward's MHA runs the
-// one-launch-per-policy kernels of this file instead of the persistent one.
-static int g_mha_v2 = -1;
-static bool mha_v2_enabled() {
-  if (g_mha_v2 >= 0) return g_mha_v2 != 0;
-  static int env = -1;
-  if (env < 0) {
-    const char* e = getenv("BT_MHA_V2");
-    env = (e && e[0] == '0') ? 0 : 1;
-  }
-  return env != 0;
-}
-
 int mha_launch(const void* qkv, const int32_t* seq_starts, int bs, int mx, int H, int d, int cutoff, int T,
                void* out, int force_path, cudaStream_t s, int padded, const void* sched) {
   BT_REQUIRE(d == MHA_D, BT_ECONFIG, "fused MHA supports head_size 64, got %d", d);
-  // The forward (a bt_plan_sched schedule, packed layout): the persistent
-  // kernel of mha2_sm100.cu serves both reference paths (short and long are
-  // the same per-block algorithm on TMEM; the dispatch rule only decided the
-  // reference's data staging).  Debug hooks that pin one of this file's
-  // policies (tile list, query tiles per CTA, segment kernel) select them.
-  if (sched != nullptr && !padded && force_path == 0 && mha_v2_enabled() && g_mha_list_mode < 0 &&
-      g_mha_qg_override == 0 && g_mha_seg_mode < 0)
-    return mha2_launch(qkv, seq_starts, sched, bs, mx, H, d, T, out, s);
   BT_REQUIRE(bs >= 1 && mx >= 1 && H >= 1 && T >= 1, BT_ESHAPE, "mha: bad shape bs=%d mx=%d H=%d T=%d", bs, mx, H, T);
   const int hidden = H * d;
   CUtensorMap tm;
@@ -888,14 +864,6 @@ extern "C" int bt_debug_mha_list(int mode, int grid) {
 extern "C" int bt_debug_mha_seg(int mode) {
   BT_REQUIRE(mode >= -1 && mode <= 2, BT_ECONFIG, "bt_debug_mha_seg: mode -1..2");
   bt::g_mha_seg_mode = mode;
-  return BT_OK;
-}
-
-// Test hook: the persistent MHA (1) or this file's per-policy kernels (0) for
-// the forward; -1 back to the BT_MHA_V2 policy.
-extern "C" int bt_debug_mha_v2(int mode) {
-  BT_REQUIRE(mode >= -1 && mode <= 1, BT_ECONFIG, "bt_debug_mha_v2: mode -1..1");
-  bt::g_mha_v2 = mode;
   return BT_OK;
 }
 

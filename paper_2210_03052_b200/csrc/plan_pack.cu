@@ -377,56 +377,37 @@ __device__ __forceinline__ void plan_sched_body(const int32_t* __restrict__ seq_
     int2* u = units + ubase[bk] + (pos - bstart[bk]) * nb;
     for (int q = 0; q < nb; ++q) u[q] = make_int2(st, (q << 20) | len);
   }
-  // MHA work items (the segment list; what the fused MHA's persistent
-  // kernel claims, and the small-batch segment kernel runs): the 128-row
-  // query tiles of the sequences longer than 128 rows, longest sequences
-  // first (the tile units above, in the same order), then for batches of
-  // bs <= 256 and max_seq_len <= 256 groups of adjacent sequences of <= 128 rows whose rows
+  // MHA segments (short batches): the query tiles of sequences longer than
+  // 128 rows, then groups of adjacent sequences of <= 128 rows whose rows
   // fit one 128-row tile together (one key block; each row masked to its own
-  // sequence); for larger batches the short sequences follow as tiles of
-  // their own.  Header (16 B): nsegs, the persistent MHA's claim queue
-  // {next item, finished CTAs} (zeroed here, reset by the MHA), pad.
+  // sequence).  One thread, over seq_starts staged in shared memory.
   if (segs != nullptr) {
-    __syncthreads();  // ubase / bstart final
-    // groups only for short batches of short sequences (bs <= 256, max_seq_len
-    // <= 256): elsewhere every sequence keeps its own tiles, so its result
-    // does not depend on its neighbours (partition invariance)
-    const bool groups = bs <= SEG_MAX_BS && nbk * 128 <= SEG_MAX_MX;
-    // units of sequences with >= 2 blocks precede the one-block bucket (nbk - 1)
-    const int long_units = nbk > 1 ? ubase[nbk - 1] : 0;
-    const int nfull = groups ? long_units : nunits[0];
-    for (int u = threadIdx.x; u < nfull; u += blockDim.x) {
-      const int2 e = units[u];
-      const int st = e.x, len = e.y & 0xFFFFF, q = (e.y >> 20) * 128;
-      // the sequence index is not in the unit; items carry only the key
-      // range, so seg_a == seg_b == -1 marks "no per-row mask"
-      segs[2 * u] = make_int4(st, st + len, st + q, min(st + len, st + q + 128));
-      segs[2 * u + 1] = make_int4(-1, -1, 0, 0);
-    }
-    if (groups) {
-      __shared__ int ss[SEG_MAX_BS + 1];
-      for (int i = threadIdx.x; i <= bs; i += blockDim.x) ss[i] = seq_starts[i];
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        int n = long_units, g0 = -1;
-        for (int i = 0; i <= bs; ++i) {
-          const bool shortseq = i < bs && ss[i + 1] - ss[i] <= 128;
-          if (g0 >= 0 && (!shortseq || ss[i + 1] - ss[g0] > 128)) {  // close the open group [g0, i)
-            segs[2 * n] = make_int4(ss[g0], ss[i], ss[g0], ss[i]);
-            segs[2 * n + 1] = make_int4(g0, i - 1, 0, 0);
-            ++n;
-            g0 = -1;
-          }
-          if (shortseq && g0 < 0) g0 = i;
-        }
-        nsegs[0] = n;
-      }
-    } else if (threadIdx.x == 0) {
-      nsegs[0] = nfull;
-    }
+    __shared__ int ss[SEG_MAX_BS + 1];
+    for (int i = threadIdx.x; i <= bs; i += blockDim.x) ss[i] = seq_starts[i];
+    __syncthreads();
     if (threadIdx.x == 0) {
-      nsegs[1] = 0;
-      nsegs[2] = 0;
+      int n = 0;
+      for (int i = 0; i < bs; ++i) {
+        const int st = ss[i], en = ss[i + 1];
+        if (en - st <= 128) continue;
+        for (int q = st; q < en; q += 128) {
+          segs[2 * n] = make_int4(st, en, q, min(en, q + 128));
+          segs[2 * n + 1] = make_int4(i, i, 0, 0);
+          ++n;
+        }
+      }
+      int g0 = -1;
+      for (int i = 0; i <= bs; ++i) {
+        const bool shortseq = i < bs && ss[i + 1] - ss[i] <= 128;
+        if (g0 >= 0 && (!shortseq || ss[i + 1] - ss[g0] > 128)) {  // close the open group [g0, i)
+          segs[2 * n] = make_int4(ss[g0], ss[i], ss[g0], ss[i]);
+          segs[2 * n + 1] = make_int4(g0, i - 1, 0, 0);
+          ++n;
+          g0 = -1;
+        }
+        if (shortseq && g0 < 0) g0 = i;
+      }
+      *nsegs = n;
     }
   }
 }
@@ -529,7 +510,8 @@ int bt_plan_sched(const int32_t* seq_starts, int bs, int mx, void* sched, bt_str
   BT_LAUNCH(plan_sched_kernel, dim3(1), dim3(1024), 0, as_stream(stream), 1, seq_starts, bs, nbk,
             static_cast<int2*>(sched), nunits, reinterpret_cast<int2*>(nunits + 4),
             reinterpret_cast<int*>(base + sched_segs_offset(bs, mx)),
-            reinterpret_cast<int4*>(base + sched_segs_offset(bs, mx) + 16));
+            bs <= SEG_MAX_BS && mx <= SEG_MAX_MX ? reinterpret_cast<int4*>(base + sched_segs_offset(bs, mx) + 16)
+                                                 : nullptr);
   return BT_OK;
 }
 
@@ -545,7 +527,8 @@ int bt_plan_forward(const int32_t* lengths, int bs, int mx, int32_t* seq_starts,
   BT_LAUNCH(plan_forward_kernel, dim3(1), dim3(1024), 0, as_stream(stream), 1, lengths, bs, nbk, seq_starts,
             static_cast<int2*>(sched), nunits, reinterpret_cast<int2*>(nunits + 4),
             reinterpret_cast<int*>(base + sched_segs_offset(bs, mx)),
-            reinterpret_cast<int4*>(base + sched_segs_offset(bs, mx) + 16));
+            bs <= SEG_MAX_BS && mx <= SEG_MAX_MX ? reinterpret_cast<int4*>(base + sched_segs_offset(bs, mx) + 16)
+                                                 : nullptr);
   return BT_OK;
 }
 

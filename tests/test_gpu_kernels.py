@@ -312,12 +312,8 @@ def test_mha_sched_order_is_result_neutral(env):
     sched = torch.zeros(nbytes // 4, dtype=torch.int32, device="cuda")
     _lib.call("bt_plan_sched", plan.seq_starts_dev.data_ptr(), len(lens), mx, sched.data_ptr(), _lib.stream_ptr())
     out = torch.empty(T, H * 64, device="cuda", dtype=torch.bfloat16)
-    _lib.call("bt_debug_mha_v2", 0)  # this file's one-tile-per-CTA kernel in schedule order
-    try:
-        _lib.call("bt_mha_varlen_sched", qkv.data_ptr(), plan.seq_starts_dev.data_ptr(), sched.data_ptr(), len(lens),
-                  mx, H, 64, 384, out.data_ptr(), T, _lib.stream_ptr())
-    finally:
-        _lib.call("bt_debug_mha_v2", -1)
+    _lib.call("bt_mha_varlen_sched", qkv.data_ptr(), plan.seq_starts_dev.data_ptr(), sched.data_ptr(), len(lens), mx,
+              H, 64, 384, out.data_ptr(), T, _lib.stream_ptr())
     ref = mha_device(qkv, plan, H, 64)
     assert torch.equal(out, ref)
     pairs = sched[:2 * len(lens)].view(-1, 2).cpu().numpy()

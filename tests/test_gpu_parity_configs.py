@@ -91,29 +91,18 @@ def test_forward_c5_slice_many_wave_vs_oracle(bt):
     xd = torch.from_numpy(x).cuda()
     outs = {}
     try:
-        # the persistent MHA (default) at its own grid and at pinned small grids
-        for name, grid in {"default": 0, "persistent_grid_37": 37, "persistent_grid_5": 5}.items():
-            _lib.call("bt_debug_mha2_grid", grid)
-            _, w = _weights(bt, ocfg, 1, "stress")  # fresh engine per policy
-            outs[name] = bt.forward(w, seqs, xd, cfg).cpu().numpy()
-        _lib.call("bt_debug_mha2_grid", 0)
-        # the per-policy kernels it replaced: tile list (C5's many-wave policy), several query tiles per CTA
-        for name, (list_mode, grid, qg) in {"one_tile": (0, 0, 0), "tile_list": (2, 0, 0),
+        for name, (list_mode, grid, qg) in {"default": (-1, 0, 0), "tile_list": (2, 0, 0),
                                             "tile_list_small_grid": (2, 37, 0), "qg4": (0, 0, 4)}.items():
             _lib.call("bt_debug_mha_list", list_mode, grid)
             _lib.call("bt_debug_mha_qg", qg)
-            _, w = _weights(bt, ocfg, 1, "stress")
+            _, w = _weights(bt, ocfg, 1, "stress")  # fresh engine per policy
             outs[name] = bt.forward(w, seqs, xd, cfg).cpu().numpy()
     finally:
-        _lib.call("bt_debug_mha2_grid", 0)
         _lib.call("bt_debug_mha_list", -1, 0)
         _lib.call("bt_debug_mha_qg", 0)
-    _check(bt, outs["default"], want, lens, mx, "stress", "C5 slice, persistent MHA")
     _check(bt, outs["tile_list"], want, lens, mx, "stress", "C5 slice, tile list")
-    for name in ("persistent_grid_37", "persistent_grid_5"):
-        assert np.array_equal(outs[name], outs["default"]), f"{name} differs from the default grid"
-    for name in ("tile_list", "tile_list_small_grid", "qg4"):
-        assert np.array_equal(outs[name], outs["one_tile"]), f"{name} differs from one tile per CTA"
+    for name, y in outs.items():
+        assert np.array_equal(y, outs["default"]), f"{name} differs from the default policy"
 
 
 def test_pkbw_weights_forward_vs_oracle(bt, tmp_path):
