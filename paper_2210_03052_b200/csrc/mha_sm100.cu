@@ -81,10 +81,6 @@ struct MhaTile {
 // Tile-list ring entry: (tile ordinal & 0xFF) << 24 | item (0xFFFFFF: none left).
 constexpr uint32_t MHA_RING_NONE = 0xFFFFFFu;
 
-__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
-}
-
 // Tie a register array to a preceding tcgen05.wait::ld.
 __device__ __forceinline__ void reg_tie(uint32_t (&r)[32]) {
   asm volatile(""
@@ -104,26 +100,28 @@ __device__ __forceinline__ void reg_tie(uint32_t (&r)[32]) {
 //                     stream through an NST-deep TMA ring; work per CTA is the
 //                     sequence's true length (grouped problem sizes).
 // Softmax: single pass, online, with a lazily moved reference max.  For each
-// 128-key block a softmax thread (= query row = TMEM lane) loads its 128 S
-// values from TMEM ONCE into registers and releases the S columns at once, so
-// the MMA warp computes the next block's S while this block's exponentials
-// run.  P = 2^((s - m_ref) * scale * log2 e) goes to shared memory as bf16
-// (UMMA K-major SW128) and the MMA warp accumulates O += P V in TMEM across
-// blocks.  m_ref only moves when the row max exceeds it by more than 2^8 in
-// P units; then the thread rescales its O row in TMEM (ld / scale / st) and
-// its running sum.  O / l is exact for any reference point, so this is the
-// reference's long-path algorithm -- per-128-column tile partial (max, sum)
-// combined by a full reduction, then exp on load (tensor.py:166-173,
-// attention.py:104-122, grouped.py:202-206) -- with P never reaching HBM.
-// BT_MHA_POLY of every 16 exponentials run as a polynomial on the FMA pipe (ex2_poly2)
-// so the SFU (16 ex2 / clk / SM) is not the softmax's bound.  Keys past the
-// sequence end are masked (p = 0).
+// 128-key block the two softmax threads of a query row (lanes i and i + 16 of
+// one warp, 64 keys each) load their S values from TMEM ONCE into registers
+// and release the S columns at once, so the MMA warp computes the next block's
+// S while this block's exponentials run.  P = 2^((s - m_ref) * scale * log2 e)
+// is computed into registers, then -- once the previous block's P V is done --
+// written to TMEM as bf16 pairs, the A operand of O += P V (FA4-style: P never
+// touches shared memory).  m_ref only moves when the row max exceeds it by
+// more than 2^8 in P units; then the thread rescales its O columns in TMEM
+// (ld / scale / st) and its running sum.  O / l is exact for any reference
+// point, so this is the reference's long-path algorithm -- per-128-column tile
+// partial (max, sum) combined by a full reduction, then exp on load
+// (tensor.py:166-173, attention.py:104-122, grouped.py:202-206) -- with P
+// never reaching HBM.  BT_MHA_POLY of every 16 exponentials run as a
+// polynomial on the FMA pipe (ex2_poly2) so the SFU (16 ex2 / clk / SM) is not
+// the only exponential pipe.  Keys past the sequence end are masked (p = 0).
 //
-// Warp roles (384 threads): warps 0-7 softmax / epilogue (two threads per query
-// row, 64 keys each), warp 8 TMA producer, warp 9 MMA issuer, warps 10-11 idle
-// (they complete warpgroup 2 for setmaxnreg); both issuer warps walk their loops warp-uniformly and
-// issue through elect.sync.  TMEM: S [0,128), P [128,192), O [192,256) -> 256 columns;
-// ~112 KB smem -> two CTAs per SM, whose latency chains interleave.
+// Warp roles (384 threads): warps 0-7 softmax / epilogue (16 query rows each,
+// two threads per row), warp 8 TMA producer, warp 9 MMA issuer, warps 10-11
+// idle (they complete warpgroup 2 for setmaxnreg); both issuer warps walk
+// their loops warp-uniformly and issue through elect.sync.  TMEM: S [0,128)
+// fp32, P [128,192) bf16 pairs, O [192,256) fp32 -> 256 columns; ~80-112 KB
+// smem -> two CTAs per SM, whose latency chains interleave.
 template <bool RESIDENT, int NST, bool MULTI, bool SEG = false>
 struct MhaCfg {
   // MULTI (NST == 2 only: no room next to 2 CTAs per SM otherwise): a
@@ -134,9 +132,8 @@ struct MhaCfg {
   static constexpr uint32_t Q_OFF = 0;
   static constexpr uint32_t KV_OFF = MHA_TILE;                       // slot s: K at +32K*s, V at +32K*s+16K
   static constexpr uint32_t OUT_OFF = KV_OFF + NST * 2 * MHA_TILE;   // output staging (LOOP) else == Q
-  static constexpr uint32_t XCH_OFF = OUT_OFF + (LOOP ? MHA_TILE : 0);  // [3][2][128] fp32 row partials
-  static constexpr uint32_t BAR_OFF = XCH_OFF + 3 * 2 * 128 * 4;
-  static constexpr size_t SMEM = BAR_OFF + 160;
+  static constexpr uint32_t BAR_OFF = OUT_OFF + (LOOP ? MHA_TILE : 0);
+  static constexpr size_t SMEM = BAR_OFF + 256;
 };
 
 #ifndef BT_MHA_POLY
@@ -168,11 +165,10 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
   uint8_t* sQ = smem + Cfg::Q_OFF;
   uint8_t* sKV = smem + Cfg::KV_OFF;
   uint8_t* sOut = smem + (Cfg::LOOP ? Cfg::OUT_OFF : Cfg::Q_OFF);
-  float* xch = reinterpret_cast<float*>(smem + Cfg::XCH_OFF);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::BAR_OFF);
   uint64_t* q_full = bars;
   uint64_t* kv_full = bars + 1;         // [NST] K block landed
-  uint64_t* kv_empty = bars + 1 + NST;  // [NST]
+  uint64_t* kv_empty = bars + 1 + NST;  // [NST] K of the slot's block read by its S MMAs
   uint64_t* s_full = bars + 1 + 2 * NST;  // S(j) in TMEM
   uint64_t* s_read = s_full + 1;          // softmax has S(j) in registers: S columns free
   uint64_t* p_full = s_full + 2;          // P(j) in TMEM, O rescaled: issue P(j) V(j)
@@ -180,7 +176,8 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
   uint64_t* v_full = s_full + 4;          // [NST] V block landed (S(j) needs only K(j))
   uint64_t* q_empty = v_full + NST;       // the tile's last S MMA has read Q
   uint64_t* o_free = q_empty + 1;         // the softmax warps have read O (next tile may overwrite it)
-  uint32_t* holder = reinterpret_cast<uint32_t*>(o_free + 1);
+  uint64_t* v_empty = o_free + 1;         // [NST] V of the slot's block read by its P V MMAs
+  uint32_t* holder = reinterpret_cast<uint32_t*>(v_empty + NST);
   // [4] tile-list items of tiles t (slot t & 3), tagged with t; one word per
   // entry, written / polled with shared-memory atomics (a self-contained
   // handoff: readers use nothing else the writer stored)
@@ -195,6 +192,7 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
       ptx::mbar_init(&kv_full[i], 1);
       ptx::mbar_init(&kv_empty[i], 1);
       ptx::mbar_init(&v_full[i], 1);
+      ptx::mbar_init(&v_empty[i], 1);
     }
     ptx::mbar_init(s_full, 1);
     ptx::mbar_init(s_read, 256);
@@ -356,8 +354,12 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
       } else {
         for (int j = 0; j < nkb; ++j, ++kvg) {
           const int slot = kvg % NST;
+          // K and V slots are released separately: K(j) once S(j) has read it,
+          // V(j) once P(j) V(j) has -- the next K loads a block ahead of the
+          // P V chain, so S(j + 1) is ready when the softmax releases S(j)
           ptx::mbar_wait(&kv_empty[slot], ((kvg / NST) & 1) ^ 1u);
           load_k(j, slot);
+          ptx::mbar_wait(&v_empty[slot], ((kvg / NST) & 1) ^ 1u);
           load_v(j, slot);
         }
       }
@@ -382,7 +384,7 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
           ptx::mma_bf16_ts(tmem + O_COL, tmem + P_COL + 8 * ks, v_desc + ks * ((16 * 128) >> 4), idesc_o,
                            (jt > 0 || ks > 0) ? 1u : 0u);
         ptx::mma_commit(pv_done);
-        if (!RESIDENT) ptx::mma_commit(&kv_empty[pslot]);  // K and V of this block consumed
+        if (!RESIDENT) ptx::mma_commit(&v_empty[pslot]);  // V of this block consumed
       }
       __syncwarp();
     };
@@ -407,6 +409,7 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
           for (int kk = 0; kk < MHA_D / 16; ++kk)
             ptx::mma_bf16_ss(tmem + S_COL, q_desc + 2 * kk, k_desc + 2 * kk, idesc_s, kk > 0);
           ptx::mma_commit(s_full);
+          if (!RESIDENT) ptx::mma_commit(&kv_empty[slot]);  // K of this block consumed
           if (j == nkb - 1) ptx::mma_commit(q_empty);  // this tile's Q is no longer read
         }
         __syncwarp();
@@ -423,18 +426,21 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
   } else {
     ptx::setmaxnreg_inc<MHA_REGS_SOFTMAX>();  // warpgroups 0-1: softmax
     // ------------------------------------------------ softmax: a row of S is
-    // shared by two threads -- warp w (half 0: keys 0-63 of each block) and
-    // warp w+4 (half 1: keys 64-127) own TMEM lanes 32*(w%4)..+31.  Row max
-    // is combined through shared memory once per block; row sums stay
+    // shared by two threads of ONE warp (tcgen05 .16x32bx2 accesses): warp
+    // w = quarter + 4 * half owns the 16 TMEM lanes 32 * quarter + 16 * half
+    // .. +15 (query rows); lane i < 16 takes keys 0-63 of each block, lane
+    // i + 16 keys 64-127 of the same row.  The row max is combined with one
+    // shuffle (no shared memory, no barrier between warps); row sums stay
     // per-thread partials until the end.  Warp-uniform skipping: warps whose
-    // 32 query rows lie past the sequence end.
+    // 16 query rows lie past the tile's rows.
     const int quarter = warp & 3, half = warp >> 2;
-    const int row = quarter * 32 + lane;
-    const int pair_bar = 1 + quarter;  // named barrier of warps quarter and quarter + 4
-    const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
-    const uint32_t s_my = trow + S_COL + half * 64;
-    const uint32_t p_my = trow + P_COL + half * 32;
-    const uint32_t o_my = trow + O_COL + half * 32;
+    const int kh = lane >> 4;  // chunk c of a block: keys 64c + 32kh .. + 31
+    const int row0 = quarter * 32 + half * 16;
+    const int row = row0 + (lane & 15);
+    const uint32_t trow = tmem + (static_cast<uint32_t>(row0) << 16);
+    const uint32_t s_my = trow + S_COL;  // chunk c: columns 64c (+32 for kh = 1)
+    const uint32_t p_my = trow + P_COL;  // chunk c: columns 32c (+16 for kh = 1)
+    const uint32_t o_my = trow + O_COL;  // columns 0-31 (+32 for kh = 1)
     const float sl2 = p.sl2;
     int g = 0;  // items consumed, across query tiles
     for (int t = 0; t < nqt; ++t) {
@@ -446,7 +452,7 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
     // query rows of this tile that exist (sequence tiles: inside the
     // sequence; segments: the segment's rows)
     const int rows_here = SEG ? seg_rows : work - q0;
-    const bool warp_live = quarter * 32 < rows_here;
+    const bool warp_live = row0 < rows_here;
     // SEG: my row's keys [ks, ke) relative to s0 (its own sequence)
     int ks = 0, ke = len;
     if (SEG && seg_a < seg_b) {  // a group of short sequences
@@ -465,114 +471,107 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
     }
     float mref = -INFINITY, lsum = 0.f;
     for (int j = 0; j < nkb; ++j, ++g) {
-      const int kvalid = min(MHA_KB, len - j * MHA_KB) - half * 64;  // valid keys among my 64 (may be <= 0)
-      // SEG: valid keys of my row among my 64 are [klo, khi)
-      const int klo = SEG ? ks - j * MHA_KB - half * 64 : 0;
-      const int khi = SEG ? min(ke - j * MHA_KB - half * 64, 64) : kvalid;
+      const int kblk = min(MHA_KB, len - j * MHA_KB);  // keys of the problem in this block
+      // my keys of chunk c are 64c + 32kh + i (i < 32): valid iff i < kblk - 64c - 32kh
+      // (SEG: my row's own sequence's keys, 64c + 32kh + i in [ks, ke) - j*128)
+      const int kof = j * MHA_KB + kh * 32;
       ptx::mbar_wait(s_full, g & 1);
       ptx::tc_fence_after();
       if (threadIdx.x == 0 && t == 0) MHA_TRACE(2 + 2 * j);
-      uint32_t r0[32], r1[32];  // my 64 S values of this row
+      uint32_t r0[32], r1[32];  // my 64 S values of this row: chunk 0, chunk 1
       if (warp_live) {
-        ptx::tmem_ld32(s_my, r0);
-        ptx::tmem_ld32(s_my + 32, r1);
+        ptx::tmem_ld_16x2_32<32>(s_my, r0);
+        ptx::tmem_ld_16x2_32<32>(s_my + 64, r1);
         ptx::tmem_wait_ld(r0);
         reg_tie(r1);
       }
       ptx::tc_fence_before();
-      ptx::mbar_arrive(s_read);  // the MMA warp may overwrite S with the next block
+      ptx::mbar_arrive(s_read);  // S is in registers: the MMA warp may overwrite it with the next block
       if (threadIdx.x == 0 && t == 0 && j < 3) MHA_TRACE(16 + 4 * j);
-#define SV(c, i) __uint_as_float((c) == 0 ? r0[i] : r1[i])
-      bool need = false;
-      float mnew = mref, alpha = 1.f;
-      if (warp_live) {
-        if (SEG) {
-          if (klo > 0 || khi < 64) {
-            // keys outside my row's sequence: s = -inf (out of the max; exp -> 0)
+      // keys outside the problem (past its end; SEG: outside my row's own
+      // sequence) -> s = -inf: out of the max, exp -> exactly 0
+      auto mask = [&](uint32_t (&r)[32], int c) {
+        const int lo = SEG ? ks - kof - 64 * c : 0;
+        const int hi = (SEG ? ke : len) - kof - 64 * c;
+        if (lo > 0 || hi < 32) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              if (i < klo || i >= khi) r0[i] = 0xff800000u;
-              if (32 + i < klo || 32 + i >= khi) r1[i] = 0xff800000u;
-            }
-          }
-        } else if (kvalid < 64) {
-          // keys past the problem's end: s = -inf (out of the max; exp -> 0)
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            if (i >= kvalid) r0[i] = 0xff800000u;
-            if (32 + i >= kvalid) r1[i] = 0xff800000u;
-          }
+          for (int i = 0; i < 32; ++i)
+            if (i < lo || i >= hi) r[i] = 0xff800000u;
         }
+      };
+      bool need = false;
+      float alpha = 1.f;
+      if (warp_live) {
+        mask(r0, 0);
+        mask(r1, 1);
         float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-#pragma unroll
-          for (int i = 0; i < 32; i += 8) {
-            m4[0] = ptx::max3(m4[0], SV(c, i), SV(c, i + 1));
-            m4[1] = ptx::max3(m4[1], SV(c, i + 2), SV(c, i + 3));
-            m4[2] = ptx::max3(m4[2], SV(c, i + 4), SV(c, i + 5));
-            m4[3] = ptx::max3(m4[3], SV(c, i + 6), SV(c, i + 7));
-          }
+        for (int i = 0; i < 32; i += 4) {
+          m4[0] = ptx::max3(m4[0], __uint_as_float(r0[i]), __uint_as_float(r0[i + 1]));
+          m4[1] = ptx::max3(m4[1], __uint_as_float(r0[i + 2]), __uint_as_float(r0[i + 3]));
+          m4[2] = ptx::max3(m4[2], __uint_as_float(r1[i]), __uint_as_float(r1[i + 1]));
+          m4[3] = ptx::max3(m4[3], __uint_as_float(r1[i + 2]), __uint_as_float(r1[i + 3]));
         }
-        // exchange the partial max with the row's other thread
-        float* x = xch + (g & 1) * 256;
-        x[half * 128 + row] = fmaxf(ptx::max3(m4[0], m4[1], m4[2]), m4[3]);
-        named_bar_sync(pair_bar, 64);
-        const float bmax = fmaxf(x[row], x[128 + row]);
-        mnew = fmaxf(mref, bmax);
+        // the row's other half is lane ^ 16 of this warp
+        const float mloc = fmaxf(ptx::max3(m4[0], m4[1], m4[2]), m4[3]);
+        const float bmax = fmaxf(mloc, __shfl_xor_sync(0xffffffffu, mloc, 16));
+        const float mnew = fmaxf(mref, bmax);
         need = (mnew - mref) * sl2 > MHA_RESCALE_LOG2;  // true on the first block (mref = -inf)
         alpha = (need && mref != -INFINITY) ? ptx::ex2_approx((mref - mnew) * sl2) : 1.f;
         if (need) mref = mnew;
         if (threadIdx.x == 0 && t == 0 && j < 3) MHA_TRACE(17 + 4 * j);
       }
+      // P = 2^((s - m_ref) * scale * log2 e): BT_MHA_POLY of every 16 on the
+      // FMA pipe, the rest on the SFU.  (SEG: a row whose sequence has no key
+      // in the blocks so far keeps m_ref = -inf; its S are all -inf, so any
+      // finite offset gives P = 0)
+      const float msc = (SEG && mref == -INFINITY) ? 0.f : mref * sl2;
+      const unsigned long long sl2x2 = ptx::f2(sl2, sl2), nm2 = ptx::f2(-msc, -msc);
+      unsigned long long sum4[4] = {0ull, 0ull, 0ull, 0ull};  // 4 independent add chains
+      auto exps = [&](const uint32_t (&r)[32], uint32_t (&pp)[16]) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          float x0, x1, e0, e1;
+          ptx::unf2(ptx::fma2(ptx::f2(__uint_as_float(r[i]), __uint_as_float(r[i + 1])), sl2x2, nm2), x0, x1);
+          if ((i & 15) < BT_MHA_POLY) {
+            ptx::ex2_poly2(x0, x1, e0, e1);  // masked key (x = -inf): exactly 0
+          } else {
+            e0 = ptx::ex2_approx(x0);  // ex2(-inf) = 0
+            e1 = ptx::ex2_approx(x1);
+          }
+          sum4[(i >> 1) & 3] = ptx::add2(sum4[(i >> 1) & 3], ptx::f2(e0, e1));
+          pp[i / 2] = ptx::pack_bf16x2(e0, e1);
+        }
+      };
       if (j > 0) {
         ptx::mbar_wait(pv_done, (g - 1) & 1);  // P(g-1) V(g-1) is in O; the P columns are free
         ptx::tc_fence_after();
       }
       if (threadIdx.x == 0 && t == 0 && j < 3) MHA_TRACE(18 + 4 * j);
       if (warp_live) {
-        // (SEG: a row whose sequence has no key in the blocks so far keeps
-        // m_ref = -inf; its S are all -inf, so any finite offset gives P = 0)
-        const float msc = (SEG && mref == -INFINITY) ? 0.f : mref * sl2;
-        const unsigned long long sl2x2 = ptx::f2(sl2, sl2), nm2 = ptx::f2(-msc, -msc);
-        unsigned long long sum4[4] = {0ull, 0ull, 0ull, 0ull};  // 4 independent add chains
-        // P = 2^((s - m_ref) * scale * log2 e): BT_MHA_POLY of every 16 on the
-        // FMA pipe, the rest on the SFU; one branch-free block over 64 keys
+        uint32_t pp[16];  // my 32 keys of chunk c as bf16 pairs -> P columns 32c (+16 for kh = 1)
+        exps(r0, pp);
+        ptx::tmem_st_16x2_16<16>(p_my, pp);
+        if (64 >= kblk) {
+          // CTA-uniform: no key of the problem among keys 64-127 -> P = 0
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          uint32_t pp[16];  // 32 keys as bf16 pairs -> P columns half*32 + 16c .. +15
-          if (32 * c >= kvalid) {  // warp-uniform: no valid key in these 32 -> P = 0, no exponentials
-#pragma unroll
-            for (int i = 0; i < 16; ++i) pp[i] = 0u;
-            ptx::tmem_st16(p_my + 16 * c, pp);
-            continue;
-          }
-#pragma unroll
-          for (int i = 0; i < 32; i += 2) {
-            float x0, x1, e0, e1;
-            ptx::unf2(ptx::fma2(ptx::f2(SV(c, i), SV(c, i + 1)), sl2x2, nm2), x0, x1);
-            if ((i & 15) < BT_MHA_POLY) {
-              ptx::ex2_poly2(x0, x1, e0, e1);  // masked key (x = -inf): exactly 0
-            } else {
-              e0 = ptx::ex2_approx(x0);  // ex2(-inf) = 0
-              e1 = ptx::ex2_approx(x1);
-            }
-            sum4[(i >> 1) & 3] = ptx::add2(sum4[(i >> 1) & 3], ptx::f2(e0, e1));
-            pp[i / 2] = ptx::pack_bf16x2(e0, e1);
-          }
-          ptx::tmem_st16(p_my + 16 * c, pp);
+          for (int i = 0; i < 16; ++i) pp[i] = 0u;
+        } else {
+          exps(r1, pp);
         }
+        ptx::tmem_st_16x2_16<16>(p_my + 32, pp);
+      }
+
+      if (warp_live) {
         const unsigned long long bsum2 = ptx::add2(ptx::add2(sum4[0], sum4[1]), ptx::add2(sum4[2], sum4[3]));
         float s0f, s1f;
         ptx::unf2(bsum2, s0f, s1f);
         lsum = lsum * alpha + (s0f + s1f);  // my keys' partial row sum
-      }
-      if (warp_live) {
         if (__any_sync(0xffffffffu, need && j > 0)) {
           // the reference max moved (rare): my 32 O columns *= 2^((m_old - m_new) * scale)
           const unsigned long long a2 = ptx::f2(alpha, alpha);
           uint32_t o[32];
-          ptx::tmem_ld32(o_my, o);
+          ptx::tmem_ld_16x2_32<32>(o_my, o);
           ptx::tmem_wait_ld(o);
 #pragma unroll
           for (int i = 0; i < 32; i += 2) {
@@ -581,7 +580,7 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
             o[i] = __float_as_uint(a);
             o[i + 1] = __float_as_uint(c);
           }
-          ptx::tmem_st32(o_my, o);
+          ptx::tmem_st_16x2_32<32>(o_my, o);
         }
         ptx::tmem_wait_st();
       }
@@ -590,19 +589,15 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
       ptx::mbar_arrive(p_full);
       if (threadIdx.x == 0 && t == 0) MHA_TRACE(3 + 2 * j);
     }
-#undef SV
     ptx::mbar_wait(pv_done, (g - 1) & 1);  // this tile's last P V
     ptx::tc_fence_after();
     if (threadIdx.x == 0 && t == 0) MHA_TRACE(30);
     // O / l -> bf16 rows staged in shared memory -> coalesced 16-byte stores,
-    // 4 rows per warp instruction
+    // 4 rows per warp instruction; a warp stages and stores its own 16 rows
     if (warp_live) {
       uint32_t o[32];
-      ptx::tmem_ld32(o_my, o);
-      float* x = xch + 2 * 256;  // its own region: the pair's last max exchange may still be read
-      x[half * 128 + row] = lsum;
-      named_bar_sync(pair_bar, 64);
-      const float l = x[row] + x[128 + row];
+      ptx::tmem_ld_16x2_32<32>(o_my, o);
+      const float l = lsum + __shfl_xor_sync(0xffffffffu, lsum, 16);
       ptx::tmem_wait_ld(o);
       const float inv = (SEG ? row < rows_here : q0 + row < len) ? 1.0f / l : 0.f;
       const unsigned long long inv2 = ptx::f2(inv, inv);
@@ -617,27 +612,27 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
                     a, b2);
           w[e] = ptx::pack_bf16x2(a, b2);
         }
-        const int chunk = half * 4 + jj;
+        const int chunk = kh * 4 + jj;
         *reinterpret_cast<uint4*>(mine + ((chunk ^ (row & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
       }
-      named_bar_sync(pair_bar, 64);  // both halves of the pair's 32 rows are staged
+      __syncwarp();  // the warp's 16 rows are staged
       ptx::griddep_wait();  // out may still be read by the previous kernel
-      // lane -> (row in this pair's 32-row slab, 16 B chunk); warp half h stores rows h*16..h*16+15
+      // lane -> (row of the warp's 16, 16 B chunk)
 #pragma unroll
       for (int it = 0; it < 4; ++it) {
-        const int rr = quarter * 32 + half * 16 + it * 4 + (lane >> 3);
+        const int rr = row0 + it * 4 + (lane >> 3);
         const int jj = lane & 7;
         if (rr < rows_here) {
           const uint4 v = *reinterpret_cast<const uint4*>(sOut + rr * 128 + ((jj ^ (rr & 7)) << 4));
           *reinterpret_cast<uint4*>(p.out + static_cast<size_t>(s0 + q0 + rr) * p.hidden + hh * MHA_D + jj * 8) = v;
         }
       }
-      if (list || t + 1 < nqt) named_bar_sync(pair_bar, 64);  // the pair's rows are stored: sOut free for the next tile
+      if (list || t + 1 < nqt) __syncwarp();  // the warp's rows are stored: sOut free for the next tile
     }
     if (p.flops != nullptr && warp_live) {
-      // instrumentation: half 0 of each row pair counts the row's keys
+      // instrumentation: the key-half-0 thread of each row counts the row's keys
       // (padded mode computes the whole mx x mx rectangle, reference mha_baseline)
-      const unsigned keys = (half == 0 && row < rows_here) ? static_cast<unsigned>(p.padded ? work : ke - ks) : 0u;
+      const unsigned keys = (kh == 0 && row < rows_here) ? static_cast<unsigned>(p.padded ? work : ke - ks) : 0u;
       const unsigned w = __reduce_add_sync(0xffffffffu, keys);
       if (lane == 0 && w) atomicAdd(p.flops, 4ull * MHA_D * w);
     }
