@@ -141,6 +141,25 @@ BT_API int bt_plan_forward(const int32_t* lengths, int bs, int mx, int32_t* seq_
  * by seq_starts instead of an offsets array (k % 8 == 0). */
 BT_API int bt_pack_starts(const float* padded, const int32_t* seq_starts, int bs, int mx, int k, void* packed_bf16,
                           bt_stream_t stream);
+/* What bt_encoder_forward runs in front of the layers (one launch, bs <= 4096, k % 8 == 0): the plan
+ * (packing.py:96-123 seq_starts + the bt_plan_sched schedule) and pack (packing.py:141-148, fp32 ->
+ * bf16) of the valid rows.  x_padded non-NULL: padded input [bs*mx, k]; row_map[T] receives each packed
+ * row's padded row index (offsets, packing.py:123) and out_padded's padded rows are set to exact zeros
+ * (packing.py:158-159; bt_ln_bias_residual_out later writes the valid rows).  x_padded NULL: the input
+ * x_packed_in [T, k] is already packed (out_padded / row_map unused).  sched holds
+ * bt_plan_sched_bytes(bs, mx) bytes. */
+BT_API int bt_forward_prologue(const int32_t* lengths, int bs, int mx, int k, const float* x_padded,
+                               const float* x_packed_in, void* x_packed_bf16, int32_t* seq_starts, void* sched,
+                               float* out_padded, int32_t* row_map, int T, bt_stream_t stream);
+/* bt_ln_bias_residual whose rows go to an fp32 output: out_f32[row_map[r]] (row r itself when row_map
+ * is NULL) = the bf16-rounded LayerNorm row widened to fp32 -- the forward's last LayerNorm fused with
+ * unpack (packing.py:151-160). */
+BT_API int bt_ln_bias_residual_out(const void* x, const void* residual, const float* bias, const float* gamma,
+                                   const float* beta, float eps, float* out_f32, const int32_t* row_map, int T,
+                                   int k, bt_stream_t stream);
+/* 1 when bt_encoder_forward runs bt_forward_prologue + bt_ln_bias_residual_out at its ends (else
+ * bt_plan_forward + bt_pack_starts ... bt_unpack). */
+BT_API int bt_one_launch_ends(int k, int bs);
 /* bt_mha_varlen with the CTA order of a bt_plan_sched schedule (what bt_encoder_forward runs). */
 BT_API int bt_mha_varlen_sched(const void* qkv, const int32_t* seq_starts, const void* sched, int bs, int mx, int H,
                                int d, int cutoff, void* out, int T, bt_stream_t stream);

@@ -66,6 +66,9 @@ SIGNATURES = {
     "bt_plan_forward": (_I, [_P, _I, _I, _P, _P, _S]),
     "bt_pack_starts": (_I, [_P, _P, _I, _I, _I, _P, _S]),
     "bt_mha_varlen_sched": (_I, [_P, _P, _P, _I, _I, _I, _I, _I, _P, _I, _S]),
+    "bt_forward_prologue": (_I, [_P, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _I, _S]),
+    "bt_ln_bias_residual_out": (_I, [_P, _P, _P, _P, _P, _F, _P, _P, _I, _I, _S]),
+    "bt_one_launch_ends": (_I, [_I, _I]),
     "bt_layer_workspace_bytes": (_SZ, [C.POINTER(LayerCfgC), _I]),
     "bt_encoder_layer": (_I, [C.POINTER(LayerWeightsC), C.POINTER(LayerCfgC), _P, _I, _I, _P, _P, _SZ, _S]),
     "bt_forward_workspace_bytes": (_SZ, [C.POINTER(LayerCfgC), _I, _I]),

@@ -24,6 +24,8 @@ int gemm_launch(const void* A, const void* Bt, const float* bias, const void* re
 int mha_launch(const void* qkv, const int32_t* seq_starts, int bs, int mx, int H, int d, int cutoff, int T, void* out,
                int force_path, cudaStream_t s, int padded, const void* sched);
 bool gemm_ln_fits(int M, int N, int K);
+int ln_launch(const void* x, const void* residual, const float* bias, const float* gamma, const float* beta, float eps,
+              void* out, int T, int k, cudaStream_t s, float* outf, const int32_t* row_map);
 int gemm_ln_launch(const void* A, const void* Bt, const float* bias, const void* residual, const float* gamma,
                    const float* beta, float eps, void* Y, int M, int N, int K, cudaStream_t s);
 // BT_FUSED_LN: 0 = GEMM + separate LayerNorm kernel everywhere, 1 (default) =
@@ -51,6 +53,19 @@ static bool debug_skip(char c) {
 }
 
 static inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+// The forward's ends as one prologue launch (plan + pack + zeroing of padded
+// output rows) and a last LayerNorm that writes the fp32 output rows itself
+// (no unpack).  BT_ONE_LAUNCH_ENDS=0 restores plan_forward + pack_starts +
+// unpack (A/B); the fused FFN2+LN mode and very large batches use them too.
+static bool one_launch_ends(int k, int bs) {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("BT_ONE_LAUNCH_ENDS");
+    env = (e && e[0] == '0') ? 0 : 1;
+  }
+  return env == 1 && k % 8 == 0 && bs <= 4096 && fused_ln_mode() < 2 && !debug_skip('l');
+}
 
 // Instrumented FlopCounter (reference tensor.py:198-199, attention.py:232-236):
 // while enabled, every GEMM the layer launches adds 2*M*N*K under its module
@@ -108,6 +123,7 @@ extern "C" int bt_plan_lengths(const int32_t*, int, int, int32_t*, int32_t*, bt_
 extern "C" int bt_plan_sched(const int32_t*, int, int, void*, bt_stream_t);
 extern "C" int bt_bias_act(const void*, int, int, const float*, void*, int, int, int, int, int, bt_stream_t);
 
+
 extern "C" size_t bt_layer_workspace_bytes(const bt_layer_cfg* cfg, int T) {
   if (!cfg) return 0;
   const int k = cfg->head_num * cfg->head_size;
@@ -129,7 +145,8 @@ static int mark(cudaStream_t s) {
 // `sched` (optional): the MHA work schedule of the batch (bt_plan_sched).
 static int encoder_layer_impl(const bt_layer_weights* w, const bt_layer_cfg* cfg, const int32_t* seq_starts, int bs,
                               int T, void* x_inout, void* ws, size_t ws_bytes, bt_stream_t stream,
-                              const void* sched = nullptr) {
+                              const void* sched = nullptr, float* final_out = nullptr,
+                              const int32_t* row_map = nullptr) {
   BT_TRY(bt::check_cfg(cfg));
   BT_REQUIRE(w != nullptr, BT_ESHAPE, "null layer weights");
   BT_REQUIRE(T >= 1 && bs >= 1, BT_ESHAPE, "encoder_layer: T=%d bs=%d", T, bs);
@@ -171,13 +188,19 @@ static int encoder_layer_impl(const bt_layer_weights* w, const bt_layer_cfg* cfg
     if (!debug_skip('s')) BT_TRY(bt::gemm_launch(L.h1, w->w2, nullptr, nullptr, L.proj, T, k, f, BT_EPI_NONE, 0, s));
     count_gemm(3, T, k, f);
     BT_TRY(mark(s));
+    // (final_out: the forward's last layer writes its output rows as fp32
+    // straight into the caller's output -- padded rows via row_map -- instead
+    // of x + an unpack pass)
     if (!debug_skip('l'))
-      BT_TRY(bt_ln_bias_residual(L.proj, L.y0, w->b2, w->ln1_g, w->ln1_b, w->ln1_eps, x, T, k, stream));
+      BT_TRY(bt::ln_launch(L.proj, L.y0, w->b2, w->ln1_g, w->ln1_b, w->ln1_eps, final_out ? nullptr : x, T, k, s,
+                           final_out, row_map));
   }
   BT_TRY(mark(s));
   return BT_OK;
 }
 }  // namespace bt
+
+extern "C" int bt_one_launch_ends(int k, int bs) { return bt::one_launch_ends(k, bs) ? 1 : 0; }
 
 // 1 when the forward fuses the attention-output GEMM with add-bias + residual
 // + LayerNorm for this token count and hidden size (bench / tooling query).
@@ -223,7 +246,18 @@ extern "C" int bt_encoder_forward(const bt_layer_weights* layers, int n_layers, 
 
   bt::g_fwd_event_idx = 0;
   BT_TRY(bt::mark(bt::as_stream(stream)));
-  (void)offsets;  // the forward packs from seq_starts
+  if (bt::one_launch_ends(k, bs)) {
+    // plan + pack + zeroing of the output's padded rows in one launch; the
+    // last layer's LayerNorm writes the valid output rows (offsets = row_map)
+    BT_TRY(bt_forward_prologue(lengths, bs, mx, k, x_padded, nullptr, x, seq_starts, sched, out_padded, offsets, T,
+                            stream));
+    BT_TRY(bt::mark(bt::as_stream(stream)));
+    for (int li = 0; li < n_layers; ++li)
+      BT_TRY(bt::encoder_layer_impl(&layers[li], cfg, seq_starts, bs, T, x, lws, lws_bytes, stream, sched,
+                                    li == n_layers - 1 ? out_padded : nullptr, offsets));
+    BT_TRY(bt::mark(bt::as_stream(stream)));
+    return BT_OK;
+  }
   if (k % 8 == 0) {
     BT_TRY(bt_plan_forward(lengths, bs, mx, seq_starts, sched, stream));
     BT_TRY(bt_pack_starts(x_padded, seq_starts, bs, mx, k, x, stream));
@@ -271,6 +305,14 @@ extern "C" int bt_encoder_forward_packed(const bt_layer_weights* layers, int n_l
   p += bt::align_up(static_cast<size_t>(T) * k * 2);
   void* lws = p;
   const size_t lws_bytes = bt_layer_workspace_bytes(cfg, T);
+  if (bt::one_launch_ends(k, bs)) {
+    // plan + fp32 -> bf16 in one launch; the last LayerNorm writes fp32 rows
+    BT_TRY(bt_forward_prologue(lengths, bs, mx, k, nullptr, x_packed, x, seq_starts, sched, nullptr, nullptr, T, stream));
+    for (int li = 0; li < n_layers; ++li)
+      BT_TRY(bt::encoder_layer_impl(&layers[li], cfg, seq_starts, bs, T, x, lws, lws_bytes, stream, sched,
+                                    li == n_layers - 1 ? out_packed : nullptr, nullptr));
+    return BT_OK;
+  }
   BT_TRY(bt_plan_forward(lengths, bs, mx, seq_starts, sched, stream));
   BT_TRY(bt_bias_act(x_packed, BT_F32, k, nullptr, x, BT_BF16, k, T, k, 0, stream));  // fp32 -> bf16
   for (int li = 0; li < n_layers; ++li)

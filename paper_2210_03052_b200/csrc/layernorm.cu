@@ -11,6 +11,25 @@
 
 namespace bt {
 
+// One 8-column chunk of a LayerNorm output row: bf16 into out (packed rows),
+// or -- the forward's last LayerNorm -- the same bf16-rounded values widened
+// to fp32 straight into the final output row (row_map[row] of the padded
+// output, or row itself when row_map is null), which replaces the unpack
+// pass (packing.py:151-160) bit for bit.
+__device__ __forceinline__ void store_row_chunk(const uint4& o, __nv_bfloat16* out, float* outf,
+                                                const int32_t* row_map, int row, size_t base, int k, int c) {
+  if (outf == nullptr) {
+    reinterpret_cast<uint4*>(out + base)[c] = o;
+    return;
+  }
+  const size_t orow = row_map ? static_cast<size_t>(__ldg(row_map + row)) : static_cast<size_t>(row);
+  float4* d = reinterpret_cast<float4*>(outf + orow * k + 8 * c);
+  d[0] = make_float4(__uint_as_float(o.x << 16), __uint_as_float(o.x & 0xffff0000u), __uint_as_float(o.y << 16),
+                     __uint_as_float(o.y & 0xffff0000u));
+  d[1] = make_float4(__uint_as_float(o.z << 16), __uint_as_float(o.z & 0xffff0000u), __uint_as_float(o.w << 16),
+                     __uint_as_float(o.w & 0xffff0000u));
+}
+
 // Register-resident parameters: best while they fit with >= 2 CTAs per SM
 // (k <= 768: 126 registers); wider rows use the shared-memory variant.
 template <int NCH, bool HOIST>
@@ -19,7 +38,9 @@ __global__ void __launch_bounds__(256) ln_bias_residual_regs_kernel(const __nv_b
                                                                const float* __restrict__ bias,
                                                                const float* __restrict__ gamma,
                                                                const float* __restrict__ beta, float eps,
-                                                               __nv_bfloat16* __restrict__ out, int T, int k) {
+                                                               __nv_bfloat16* __restrict__ out, int T, int k,
+                                                               float* __restrict__ outf,
+                                                               const int32_t* __restrict__ row_map) {
   const int lane = threadIdx.x & 31;
   const int wpb = blockDim.x >> 5;
   const int nchunk = k >> 3;
@@ -116,7 +137,7 @@ __global__ void __launch_bounds__(256) ln_bias_residual_regs_kernel(const __nv_b
           const float y1 = gv[i][2 * e + 1] * ((z[i][2 * e + 1] - mean) * rstd) + ev[i][2 * e + 1];
           ow[e] = ptx::pack_bf16x2(y0, y1);
         }
-        reinterpret_cast<uint4*>(out + base)[c] = o;
+        store_row_chunk(o, out, outf, row_map, row, base, k, c);
       }
     }
   }
@@ -133,7 +154,9 @@ __global__ void __launch_bounds__(256) ln_bias_residual_kernel(const __nv_bfloat
                                                                const float* __restrict__ bias,
                                                                const float* __restrict__ gamma,
                                                                const float* __restrict__ beta, float eps,
-                                                               __nv_bfloat16* __restrict__ out, int T, int k) {
+                                                               __nv_bfloat16* __restrict__ out, int T, int k,
+                                                               float* __restrict__ outf,
+                                                               const int32_t* __restrict__ row_map) {
   extern __shared__ float4 sparams[];  // [3][k / 4]: bias (0 if none), gamma, beta
   const int lane = threadIdx.x & 31;
   const int wpb = blockDim.x >> 5;
@@ -219,7 +242,7 @@ __global__ void __launch_bounds__(256) ln_bias_residual_kernel(const __nv_bfloat
           const float y1 = gg[2 * e + 1] * ((z[i][2 * e + 1] - mean) * rstd) + ee[2 * e + 1];
           ow[e] = ptx::pack_bf16x2(y0, y1);
         }
-        reinterpret_cast<uint4*>(out + base)[c] = o;
+        store_row_chunk(o, out, outf, row_map, row, base, k, c);
       }
     }
   }
@@ -227,7 +250,7 @@ __global__ void __launch_bounds__(256) ln_bias_residual_kernel(const __nv_bfloat
 
 template <int NCH>
 static int launch_ln(const __nv_bfloat16* x, const __nv_bfloat16* r, const float* b, const float* g, const float* be,
-                      float eps, __nv_bfloat16* out, int T, int k, cudaStream_t s) {
+                      float eps, __nv_bfloat16* out, int T, int k, cudaStream_t s, float* outf, const int32_t* row_map) {
   const int threads = 256, wpb = threads / 32;
   if constexpr (NCH <= 3) {
     const int sms0 = num_sms() > 0 ? num_sms() : 148;
@@ -235,7 +258,7 @@ static int launch_ln(const __nv_bfloat16* x, const __nv_bfloat16* r, const float
     if (grid0 > sms0 * 8LL) grid0 = sms0 * 8LL;
     if (grid0 < 1) grid0 = 1;
     BT_LAUNCH((ln_bias_residual_regs_kernel<NCH, true>), dim3(static_cast<int>(grid0)), dim3(threads), 0, s, 1, x, r,
-              b, g, be, eps, out, T, k);
+              b, g, be, eps, out, T, k, outf, row_map);
     return BT_OK;
   }
   const int sms = num_sms() > 0 ? num_sms() : 148;
@@ -252,31 +275,48 @@ static int launch_ln(const __nv_bfloat16* x, const __nv_bfloat16* r, const float
   const long long cap = static_cast<long long>(sms) * (per_sm > 0 ? per_sm : 1);
   if (grid > cap) grid = cap;  // resident grid, rows grid-strided
   if (grid < 1) grid = 1;
-  BT_LAUNCH(kern, dim3(static_cast<int>(grid)), dim3(threads), smem, s, 1, x, r, b, g, be, eps, out, T, k);
+  BT_LAUNCH(kern, dim3(static_cast<int>(grid)), dim3(threads), smem, s, 1, x, r, b, g, be, eps, out, T, k, outf,
+            row_map);
   return BT_OK;
 }
 
 }  // namespace bt
 
-extern "C" int bt_ln_bias_residual(const void* x, const void* residual, const float* bias, const float* gamma,
-                                   const float* beta, float eps, void* out, int T, int k, bt_stream_t stream) {
+namespace bt {
+// LayerNorm with an optional fp32 final-output destination (see
+// store_row_chunk); out may be null when outf is given.
+int ln_launch(const void* x, const void* residual, const float* bias, const float* gamma, const float* beta, float eps,
+              void* out, int T, int k, cudaStream_t s, float* outf, const int32_t* row_map) {
   BT_REQUIRE(T >= 0 && k >= 8 && k % 8 == 0 && k <= 4096, BT_ESHAPE,
              "layernorm: need k %% 8 == 0 and 8 <= k <= 4096, got k=%d", k);
   BT_REQUIRE(eps > 0.f, BT_ESHAPE, "layernorm eps must be > 0, got %g", static_cast<double>(eps));
-  BT_REQUIRE(x && gamma && beta && out, BT_ESHAPE, "layernorm: null pointer");
+  BT_REQUIRE(x && gamma && beta && (out || outf), BT_ESHAPE, "layernorm: null pointer");
   if (T == 0) return BT_OK;
   const auto* xb = static_cast<const __nv_bfloat16*>(x);
   const auto* rb = static_cast<const __nv_bfloat16*>(residual);
   auto* ob = static_cast<__nv_bfloat16*>(out);
-  cudaStream_t s = bt::as_stream(stream);
   const int nch = (k / 8 + 31) / 32;
   switch (nch) {
-    case 1: return bt::launch_ln<1>(xb, rb, bias, gamma, beta, eps, ob, T, k, s);
-    case 2: return bt::launch_ln<2>(xb, rb, bias, gamma, beta, eps, ob, T, k, s);
-    case 3: return bt::launch_ln<3>(xb, rb, bias, gamma, beta, eps, ob, T, k, s);
-    case 4: return bt::launch_ln<4>(xb, rb, bias, gamma, beta, eps, ob, T, k, s);
-    case 5: case 6: return bt::launch_ln<6>(xb, rb, bias, gamma, beta, eps, ob, T, k, s);
-    case 7: case 8: return bt::launch_ln<8>(xb, rb, bias, gamma, beta, eps, ob, T, k, s);
-    default: return bt::launch_ln<16>(xb, rb, bias, gamma, beta, eps, ob, T, k, s);
+    case 1: return launch_ln<1>(xb, rb, bias, gamma, beta, eps, ob, T, k, s, outf, row_map);
+    case 2: return launch_ln<2>(xb, rb, bias, gamma, beta, eps, ob, T, k, s, outf, row_map);
+    case 3: return launch_ln<3>(xb, rb, bias, gamma, beta, eps, ob, T, k, s, outf, row_map);
+    case 4: return launch_ln<4>(xb, rb, bias, gamma, beta, eps, ob, T, k, s, outf, row_map);
+    case 5: case 6: return launch_ln<6>(xb, rb, bias, gamma, beta, eps, ob, T, k, s, outf, row_map);
+    case 7: case 8: return launch_ln<8>(xb, rb, bias, gamma, beta, eps, ob, T, k, s, outf, row_map);
+    default: return launch_ln<16>(xb, rb, bias, gamma, beta, eps, ob, T, k, s, outf, row_map);
   }
+}
+}  // namespace bt
+
+extern "C" int bt_ln_bias_residual(const void* x, const void* residual, const float* bias, const float* gamma,
+                                   const float* beta, float eps, void* out, int T, int k, bt_stream_t stream) {
+  BT_REQUIRE(out, BT_ESHAPE, "layernorm: null pointer");
+  return bt::ln_launch(x, residual, bias, gamma, beta, eps, out, T, k, bt::as_stream(stream), nullptr, nullptr);
+}
+
+extern "C" int bt_ln_bias_residual_out(const void* x, const void* residual, const float* bias, const float* gamma,
+                                       const float* beta, float eps, float* out_f32, const int32_t* row_map, int T,
+                                       int k, bt_stream_t stream) {
+  BT_REQUIRE(out_f32, BT_ESHAPE, "layernorm: null pointer");
+  return bt::ln_launch(x, residual, bias, gamma, beta, eps, nullptr, T, k, bt::as_stream(stream), out_f32, row_map);
 }

@@ -5,6 +5,7 @@
 // All kernels are HBM-bound data movement; 16-byte vector accesses, grids
 // sized in multiples of the SM count.
 
+#include <algorithm>
 #include <cstdarg>
 #include <cstdlib>
 #include <cstring>
@@ -459,6 +460,134 @@ __global__ void pack_starts_kernel(const Tin* __restrict__ padded, const int32_t
     if (j < __ldg(seq_starts + b + 1) - s0) move8(padded + prow * k + c, packed + static_cast<long long>(s0 + j) * k + c);
   }
 }
+
+// ---------------------------------------------------------------- forward prologue
+// The whole front of the forward in ONE launch (what plan_forward + pack_starts
+// do in two, plus the zeroing half of unpack): every CTA scans the lengths into
+// shared memory; CTA 0 publishes seq_starts and writes the MHA schedule
+// (plan_sched_body) while the other CTAs, one warp per row, gather the valid
+// rows fp32 -> bf16 (packed row r -> sequence b by a binary search over the
+// starts), record where each packed row goes in the padded output (row_map,
+// read by the last layer's LayerNorm, which writes the output rows itself),
+// and zero the output's padded rows (packing.py:158-159: exact zeros).
+// PADDED = false: the input is already packed ([T, k] fp32, e2e host path).
+constexpr int PRO_THREADS = 512;
+constexpr int PRO_MAX_BS = 4096;
+
+// Exclusive scan of lengths[0..bs) into ss[0..bs] (shared memory), any block
+// size that is a multiple of 32.
+__device__ __forceinline__ void block_scan_lengths(const int32_t* __restrict__ lengths, int bs, int32_t* ss) {
+  __shared__ int32_t wsum[32];
+  __shared__ int32_t carry_s;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+  if (tid == 0) carry_s = 0;
+  __syncthreads();
+  for (int base = 0; base < bs; base += blockDim.x) {
+    const int i = base + tid;
+    const int v = (i < bs) ? __ldg(lengths + i) : 0;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      int w = lane < nw ? wsum[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += y;
+      }
+      wsum[lane] = w;
+    }
+    __syncthreads();
+    const int incl = x + (wid ? wsum[wid - 1] : 0) + carry_s;
+    if (i < bs) ss[i] = incl - v;
+    __syncthreads();
+    if (tid == blockDim.x - 1) carry_s = incl;
+    __syncthreads();
+  }
+  if (tid == 0) ss[bs] = carry_s;
+  __syncthreads();
+}
+
+template <bool PADDED>
+__global__ void __launch_bounds__(PRO_THREADS) forward_prologue_kernel(
+    const int32_t* __restrict__ lengths, int bs, int mx, int nbk, int k, const float* __restrict__ x_in,
+    __nv_bfloat16* __restrict__ x_out, int32_t* __restrict__ seq_starts, int2* __restrict__ sched,
+    int* __restrict__ nunits, int2* __restrict__ units, int* __restrict__ nsegs, int4* __restrict__ segs,
+    float* __restrict__ out_padded, int32_t* __restrict__ row_map) {
+  __shared__ int32_t ss[PRO_MAX_BS + 1];
+  ptx::griddep_launch_dependents();
+  ptx::griddep_wait();  // lengths / input / output may belong to earlier work on the stream
+  block_scan_lengths(lengths, bs, ss);
+  if (blockIdx.x == 0) {
+    for (int i = threadIdx.x; i <= bs; i += blockDim.x) seq_starts[i] = ss[i];
+    plan_sched_body(ss, bs, nbk, sched, nunits, units, nsegs, segs);
+    return;
+  }
+  const int T = ss[bs];
+  const int lane = threadIdx.x & 31;
+  const int wpb = blockDim.x >> 5;
+  const int nwarps = (gridDim.x - 1) * wpb;
+  const int gw = (blockIdx.x - 1) * wpb + (threadIdx.x >> 5);
+  const int nchunk = k >> 3;
+  for (int r = gw; r < T; r += nwarps) {
+    long long src = r;
+    if (PADDED) {
+      int lo = 0, hi = bs - 1;  // sequence of packed row r: the last b with ss[b] <= r
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (ss[mid] <= r) lo = mid; else hi = mid - 1;
+      }
+      src = static_cast<long long>(lo) * mx + (r - ss[lo]);
+      if (lane == 0) row_map[r] = static_cast<int32_t>(src);
+    }
+    const float* srow = x_in + src * k;
+    __nv_bfloat16* drow = x_out + static_cast<long long>(r) * k;
+    if (nchunk <= 128) {
+      // every load of the row in flight before any use (k <= 1024: <= 4 chunks per lane)
+      float4 v[4][2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int c = lane + 32 * i;
+        if (c < nchunk) {
+          v[i][0] = __ldg(reinterpret_cast<const float4*>(srow) + 2 * c);
+          v[i][1] = __ldg(reinterpret_cast<const float4*>(srow) + 2 * c + 1);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int c = lane + 32 * i;
+        if (c < nchunk)
+          reinterpret_cast<uint4*>(drow)[c] =
+              make_uint4(ptx::pack_bf16x2(v[i][0].x, v[i][0].y), ptx::pack_bf16x2(v[i][0].z, v[i][0].w),
+                         ptx::pack_bf16x2(v[i][1].x, v[i][1].y), ptx::pack_bf16x2(v[i][1].z, v[i][1].w));
+      }
+    } else {
+      for (int c = lane; c < nchunk; c += 32) move8(srow + c * 8, drow + c * 8);
+    }
+  }
+  if (PADDED) {
+    // padded row q (0 <= q < bs*mx - T) is in sequence b = the last b whose
+    // preceding sequences hold <= q padded rows (b*mx - ss[b] of them)
+    const int nz = bs * mx - T;
+    const int k4 = k >> 2;
+    for (int q = gw; q < nz; q += nwarps) {
+      int lo = 0, hi = bs - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (mid * mx - ss[mid] <= q) lo = mid; else hi = mid - 1;
+      }
+      const long long prow = static_cast<long long>(lo) * mx + (ss[lo + 1] - ss[lo]) + (q - (lo * mx - ss[lo]));
+      float4* o = reinterpret_cast<float4*>(out_padded + prow * k);
+      for (int c = lane; c < k4; c += 32) o[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+}
+
 }  // namespace bt
 
 extern "C" {
@@ -539,6 +668,41 @@ int bt_pack_starts(const float* padded, const int32_t* seq_starts, int bs, int m
   BT_LAUNCH((pack_starts_kernel<float, __nv_bfloat16>), dim3(grid_for(static_cast<long long>(bs) * mx * (k / 8), threads)),
             dim3(threads), 0, as_stream(stream), 1, padded, seq_starts, bs, mx, k,
             static_cast<__nv_bfloat16*>(packed_bf16));
+  return BT_OK;
+}
+
+// The forward's front in one launch (forward_prologue_kernel).  x_padded
+// non-null: padded fp32 input [bs*mx, k], its packed bf16 rows go to x_packed,
+// row_map[T] receives each packed row's padded row and out_padded's padded
+// rows are zeroed; x_padded null: x_packed_in [T, k] fp32 is converted.
+int bt_forward_prologue(const int32_t* lengths, int bs, int mx, int k, const float* x_padded,
+                        const float* x_packed_in, void* x_packed, int32_t* seq_starts, void* sched, float* out_padded,
+                        int32_t* row_map, int T, bt_stream_t stream) {
+  BT_REQUIRE(lengths && x_packed && seq_starts && sched && (x_padded ? out_padded && row_map : x_packed_in != nullptr),
+             BT_ESHAPE, "forward_prologue: null pointer");
+  BT_REQUIRE(bs >= 1 && bs <= PRO_MAX_BS && mx >= 1 && k >= 8 && k % 8 == 0 && T >= 1, BT_ESHAPE,
+             "forward_prologue: bad shape bs=%d mx=%d k=%d", bs, mx, k);
+  const int nbk = (mx + 127) / 128;
+  BT_REQUIRE(nbk <= SCHED_MAX_BUCKETS && mx < (1 << 20), BT_ESHAPE, "forward_prologue: max_seq_len %d too large", mx);
+  uint8_t* base = static_cast<uint8_t*>(sched);
+  int* nunits = reinterpret_cast<int*>(base + sched_units_offset(bs));
+  int4* segs = bs <= SEG_MAX_BS && mx <= SEG_MAX_MX ? reinterpret_cast<int4*>(base + sched_segs_offset(bs, mx) + 16)
+                                                    : nullptr;
+  int* nsegs = reinterpret_cast<int*>(base + sched_segs_offset(bs, mx));
+  const int sms = num_sms() > 0 ? num_sms() : 148;
+  const long long rows = x_padded ? std::max<long long>(T, static_cast<long long>(bs) * mx - T) : T;
+  const int wpb = PRO_THREADS / 32;
+  const int grid = 1 + static_cast<int>(std::min<long long>(sms * 4LL, (rows + wpb - 1) / wpb));
+  if (x_padded) {
+    BT_LAUNCH(forward_prologue_kernel<true>, dim3(grid), dim3(PRO_THREADS), 0, as_stream(stream), 1, lengths, bs, mx,
+              nbk, k, x_padded, static_cast<__nv_bfloat16*>(x_packed), seq_starts, static_cast<int2*>(sched), nunits,
+              reinterpret_cast<int2*>(nunits + 4), nsegs, segs, out_padded, row_map);
+  } else {
+    BT_LAUNCH(forward_prologue_kernel<false>, dim3(grid), dim3(PRO_THREADS), 0, as_stream(stream), 1, lengths, bs,
+              mx, nbk, k, x_packed_in, static_cast<__nv_bfloat16*>(x_packed), seq_starts, static_cast<int2*>(sched),
+              nunits, reinterpret_cast<int2*>(nunits + 4), nsegs, segs, static_cast<float*>(nullptr),
+              static_cast<int32_t*>(nullptr));
+  }
   return BT_OK;
 }
 

@@ -81,4 +81,8 @@ def kernel_bytes(kind: str, T: int, k: int, bs: int = 0, mx: int = 0) -> int:
         return T * k * 2 + bs * mx * k * 4
     if kind == "plan":      # int32 lengths in, seq_starts + (start, length) schedule out
         return 4 * bs + 4 * (bs + 1) + 8 * bs
+    if kind == "prologue":  # plan + pack + the zeroed padded output rows (fp32) + row_map
+        return (4 * bs + 4 * (bs + 1) + 8 * bs) + (T * k * 4 + T * k * 2) + (bs * mx - T) * k * 4 + 4 * T
+    if kind == "ln_out":    # read x, read residual (bf16), write the fp32 output rows
+        return 2 * T * k * 2 + T * k * 4
     raise ValueError(kind)

@@ -222,3 +222,33 @@ def test_forward_schedule_boundaries_vs_oracle(bt, bs, mx, lens_kind):
     assert_close_bf16(y, want, max_abs_max=2e-2, what=f"bs{bs} mx{mx} {lens_kind}")
     valid = orc.build_mask(lens, mx).reshape(-1).astype(bool)
     assert not np.asarray(y.array)[~valid].any()
+
+
+@pytest.mark.parametrize("lens_kind", ["full", "ones", "mixed"])
+def test_forward_one_launch_ends(bt, lens_kind):
+    """The forward's prologue (plan + pack + zeroing of the output's padded
+    rows in one launch) and the last LayerNorm writing the fp32 output rows
+    (no unpack pass): the device path (padded input -> padded output, the
+    output buffer pre-filled with NaN) equals the host path (packed I/O)
+    bitwise, padded rows are exact zeros, and both match the oracle."""
+    import torch
+
+    mx, bs = 96, 7
+    lens = {"full": [mx] * bs, "ones": [1] * bs, "mixed": [96, 1, 50, 96, 3, 64, 95]}[lens_kind]
+    cfg = bt.ModelConfig(layers=2, head_num=2, head_size=64, max_seq_len=mx, batch_size=bs,
+                         flags=bt.OptFlags.all_on())
+    w = bt.init_weights(cfg, 4)
+    x = orc.gen_input(lens, mx, 128, 4)
+    y_host = bt.forward(w, bt.SeqLengths.of(lens, mx), bt.Tensor(x), cfg).array
+    eng = bt.encoder.engine_for(w, cfg)
+    xd = torch.from_numpy(x).cuda()
+    out = torch.full_like(xd, float("nan"))
+    eng.forward_device(torch.tensor(lens, dtype=torch.int32, device="cuda"), bs, sum(lens), xd, out)
+    torch.cuda.synchronize()
+    y_dev = out.cpu().numpy()
+    np.testing.assert_array_equal(y_dev, y_host)
+    pad = ~orc.build_mask(lens, mx).reshape(-1).astype(bool)
+    assert not np.any(y_dev[pad])
+    ocfg = orc.OracleConfig(2, 2, 64, mx, bs)
+    want = orc.forward(orc.init_weights(ocfg, 4), lens, x, ocfg)
+    assert_close_bf16(y_dev, want, max_abs_max=2e-2, what=f"one-launch ends ({lens_kind})")
