@@ -72,10 +72,19 @@ __device__ __forceinline__ unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+// Compiled in only with -DBT_TRACE_ON (scripts/gemm_trace.py builds that
+// variant): otherwise the pointer check would be a global load on the MMA
+// issuer's path.
+#ifdef BT_TRACE_ON
 #define BT_TRACE(slot, val)                                                          \
   do {                                                                               \
     if (g_gemm_trace && (slot) < 64) g_gemm_trace[blockIdx.x * 64 + (slot)] = (val); \
   } while (0)
+#else
+#define BT_TRACE(slot, val) \
+  do {                      \
+  } while (0)
+#endif
 
 constexpr int GEMM_BK = 64;
 constexpr size_t GEMM_SMEM_LIMIT = 232448;  // 227 KB opt-in per CTA

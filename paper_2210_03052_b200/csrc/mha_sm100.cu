@@ -26,12 +26,16 @@ constexpr int MHA_KB = 128;                  // keys per block (UMMA N of S)
 constexpr uint32_t MHA_TILE = 128 * 128;     // bytes of one 128 x 64 bf16 tile
 constexpr int MHA_SHORT_MAX_KEYS = 384;      // TMEM: 384 S columns + 64 O columns <= 512
 
-// Debug trace (off unless bt_debug_mha_trace installs a buffer): 32 u64
+// Debug trace (a -DBT_TRACE_ON build with a buffer installed by
+// bt_debug_mha_trace): 32 u64
 // globaltimer stamps per CTA, CTA index = linear block id.
 //   [0] prologue done  [1] Q landed (MMA warp)  [2+2t] S(t) ready (softmax)
 //   [3+2t] item t done (softmax)  [30] O ready  [31] output stored
 //   item t < 3: [16+4t] S in registers  [17+4t] max done  [18+4t] P V(t-1) done  [19+4t] P written
 __device__ unsigned long long* g_mha_trace = nullptr;
+// (compiled in only with -DBT_TRACE_ON, as the GEMM's: scripts/mha_trace.py
+// builds that variant; the pointer check is a global load per trace point)
+#ifdef BT_TRACE_ON
 #define MHA_TRACE(slot)                                                                                   \
   do {                                                                                                    \
     if (g_mha_trace && (slot) < 32) {                                                                     \
@@ -40,6 +44,11 @@ __device__ unsigned long long* g_mha_trace = nullptr;
       g_mha_trace[((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 32 + (slot)] = _t;   \
     }                                                                                                     \
   } while (0)
+#else
+#define MHA_TRACE(slot) \
+  do {                  \
+  } while (0)
+#endif
 
 struct MhaParams {
   const int32_t* seq_starts;

@@ -1,6 +1,10 @@
 """Per-CTA event timeline of one GEMM launch (globaltimer ns).
 
     python scripts/gemm_trace.py M N K EPI BN
+
+Needs a trace build of the library (the trace points are compiled out otherwise):
+    python -m paper_2210_03052_b200.build --variant scripts/ab/trace.so -D BT_TRACE_ON
+    BT_LIB_PATH=scripts/ab/trace.so python scripts/gemm_trace.py ...
 """
 
 import math

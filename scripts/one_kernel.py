@@ -37,7 +37,7 @@ def main():
         seqs = harness.gen_lengths(bs, mx, "fixed", seed=0, alpha=0.6)
         plan = plan_for_lengths(seqs)
         qkv = torch.randn(plan.valid_word_cnt, 3 * H * 64, device="cuda").to(torch.bfloat16)
-        for _ in range(3):
+        for _ in range(8):
             mha_device(qkv, plan, H, 64)
     elif kind == "ln":
         from paper_2210_03052_b200.fusion import ln_device
