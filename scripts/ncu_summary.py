@@ -23,7 +23,7 @@ METRICS = ("gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.
            "sm__warps_active.avg.pct_of_peak_sustained_active")
 
 # kernel-name prefix -> bench.py kernel-table name, in forward order per layer
-ROLES = (("plan_scan", "plan"), ("pack_kernel", "pack"), ("mha_fwd", "mha"), ("gemm_ln_kernel", "gemm_attn_out_ln"),
+ROLES = (("forward_prologue", "prologue"), ("plan_scan", "plan"), ("pack_kernel", "pack"), ("mha_fwd", "mha"), ("gemm_ln_kernel", "gemm_attn_out_ln"),
          ("ln_bias_residual", "ln"), ("unpack_kernel", "unpack"))
 GEMM_ORDER = ("gemm_qkv", "gemm_attn_out", "gemm_ffn1_gelu", "gemm_ffn2")
 

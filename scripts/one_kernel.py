@@ -27,7 +27,7 @@ def main():
         A = (torch.randn(M, K, device="cuda") * 0.5).to(torch.bfloat16)
         W = (torch.randn(N, K, device="cuda") / math.sqrt(K)).to(torch.bfloat16)
         bias = torch.randn(N, device="cuda") * 0.1
-        for _ in range(3):
+        for _ in range(8):
             gemm_device(A, W, bias if epi else None, None, epi, bn=bn if bn else None)
     elif kind == "mha":
         from paper_2210_03052_b200.attention import mha_device
