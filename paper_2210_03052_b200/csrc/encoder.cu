@@ -323,10 +323,8 @@ extern "C" int bt_encoder_forward_packed(const bt_layer_weights* layers, int n_l
 
 // Copy the valid rows of each sequence between a padded host / device buffer
 // [bs*mx, row_bytes] and a packed one [T, row_bytes] with async DMA copies
-// (adjacent sequences that are contiguous on both sides are merged).  The
-// copies go out as ONE cudaMemcpyBatchAsync when the stream allows it (not
-// the legacy default stream): per-copy submission overhead otherwise holds
-// ~0.5 MB row runs to ~38 GB/s over PCIe.
+// (adjacent sequences that are contiguous on both sides are merged), one
+// cudaMemcpyAsync per run.
 extern "C" int bt_copy_rows(void* dst, const void* src, const int32_t* lengths_host, int bs, int mx,
                             long long row_bytes, int to_packed, bt_stream_t stream) {
   BT_REQUIRE(bs >= 1 && mx >= 1 && row_bytes > 0 && lengths_host, BT_ESHAPE, "copy_rows: bad arguments");
@@ -353,15 +351,6 @@ extern "C" int bt_copy_rows(void* dst, const void* src, const int32_t* lengths_h
     sizes.push_back(static_cast<size_t>(rows * row_bytes));
     packed_row += rows;
     b = e;
-  }
-  if (s != nullptr && s != cudaStreamLegacy && sizes.size() > 1) {
-    cudaMemcpyAttributes attr = {};
-    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-    size_t attr_idx = 0, fail_idx = 0;
-    if (cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), sizes.size(), &attr, &attr_idx, 1, &fail_idx,
-                             s) == cudaSuccess)
-      return BT_OK;
-    (void)cudaGetLastError();  // not supported here: per-run copies below
   }
   for (size_t i = 0; i < sizes.size(); ++i)
     BT_CUDA_CHECK(cudaMemcpyAsync(dsts[i], srcs[i], sizes[i], cudaMemcpyDefault, s));

@@ -18,6 +18,7 @@ served by ``ladder.py`` from the same kernels.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import struct
 import threading
 import weakref
@@ -319,6 +320,10 @@ def layer_cfg_c(config: ModelConfig) -> _lib.LayerCfgC:
                           config.split_seq_len)
 
 
+# host-I/O pipeline depth of forward() on host buffers (BertEncoderB200.default_chunks)
+E2E_CHUNKS_DEFAULT = 1
+
+
 class BertEncoderB200:
     """Device-resident encoder: uploaded weights, cached workspace, and the
     stream-ordered forward used by ``forward()`` and ``bench.py``."""
@@ -346,7 +351,8 @@ class BertEncoderB200:
         # and their I/O buffers are shared state (the service runs requests on
         # a thread pool)
         self._lock = threading.RLock()
-        self._io_stream = None
+        self._io_streams = None  # host-I/O pipeline: H2D, compute, D2H
+        self._io_events = []
 
     def layer(self, i: int) -> DeviceLayer:
         return self._layers[i]
@@ -402,7 +408,7 @@ class BertEncoderB200:
                       out_ptr, ws.data_ptr(), ws_bytes, _lib.stream_ptr(stream))
             self._ws_used(stream)
 
-    GRAPH_CACHE = 4  # batch shapes whose packed forward is kept as a CUDA graph
+    GRAPH_CACHE = 8  # batch (range) shapes whose packed forward is kept as a CUDA graph
 
     def _graph_entry(self, seqs: SeqLengths, cfg: ModelConfig, cfg_c):
         """(graph, x_packed, y_packed) for this batch shape: device buffers
@@ -446,38 +452,97 @@ class BertEncoderB200:
             self._graphs.pop(next(iter(self._graphs)))
         return entry
 
-    def forward_host_packed(self, seqs: SeqLengths, x_pinned, out_pinned, config: ModelConfig | None = None):
+    @staticmethod
+    def chunk_bounds(lengths, chunks) -> list[tuple[int, int]]:
+        """Sequence ranges [b0, b1) of the host-I/O pipeline.  ``chunks`` is
+        a count n (token-balanced cut into n contiguous ranges) or a list of
+        token fractions (e.g. (0.3, 0.7)); sequences are never split."""
+        bs = len(lengths)
+        if isinstance(chunks, int):
+            fr = [1.0 / max(1, chunks)] * max(1, chunks)
+        else:
+            fr = [float(f) for f in chunks]
+        n = max(1, min(len(fr), bs))
+        fr = fr[:n]
+        tot = float(sum(lengths))
+        cum = np.cumsum(np.asarray(lengths, dtype=np.float64))
+        cuts, acc = [0], 0.0
+        for f in fr[:-1]:
+            acc += f / sum(fr) * tot
+            c = int(np.argmin(np.abs(cum - acc))) + 1  # the sequence boundary nearest the target
+            c = min(max(c, cuts[-1] + 1), bs - (n - len(cuts)))
+            cuts.append(c)
+        cuts.append(bs)
+        return [(cuts[i], cuts[i + 1]) for i in range(len(cuts) - 1) if cuts[i + 1] > cuts[i]]
+
+    def default_chunks(self, seqs: SeqLengths):
+        """Host-I/O pipeline depth (BT_E2E_CHUNKS overrides: "1", "3" or
+        fractions "0.25,0.5,0.25")."""
+        env = os.environ.get("BT_E2E_CHUNKS")
+        if env:
+            parts = [p for p in env.split(",") if p.strip()]
+            return int(parts[0]) if len(parts) == 1 else [float(p) for p in parts]
+        # PCIe moves ~40 GB/s each way: below ~1 MB of rows per direction the
+        # copy is short next to the launch-bound forward -- one chunk
+        if seqs.batch_size < 2 or seqs.total * self.config.hidden_dim * 4 < (1 << 20):
+            return 1
+        return E2E_CHUNKS_DEFAULT
+
+    def forward_host_packed(self, seqs: SeqLengths, x_pinned, out_pinned, config: ModelConfig | None = None,
+                            chunks=None):
         """End-to-end forward on pinned host buffers [bs*mx, k] fp32: only the
-        valid rows cross PCIe (async DMA per sequence, both directions), the
-        encoder runs packed -> packed as one CUDA graph (cached per batch
-        shape), and the padded output rows are zeroed on the host while the
-        GPU computes.  Synchronises."""
+        valid rows cross PCIe (async DMA per sequence, both directions).
+
+        The batch is cut into contiguous sequence ranges (``chunks``,
+        default ``default_chunks``) -- sequences are independent, so each
+        range is its own packed forward (a CUDA graph cached per range
+        shape) -- and the ranges are pipelined over three streams:
+        H2D(i + 1) || forward(i) || D2H(i - 1).  The padded output rows are
+        zeroed on the host while the GPU works.  Synchronises."""
         with self._lock:
             cfg = config or self.config
             cfg_c = self._cfg_c if config is None else layer_cfg_c(cfg)
             bs, mx, k = seqs.batch_size, seqs.max_seq_len, cfg.hidden_dim
-            graph, run, xp, yp, _, _ = self._graph_entry(seqs, cfg, cfg_c)
             lengths_h = np.ascontiguousarray(np.asarray(seqs.lengths, dtype=np.int32))
-            lp = lengths_h.ctypes.data
+            bounds = self.chunk_bounds(seqs.lengths, self.default_chunks(seqs) if chunks is None else chunks)
+            entries = [self._graph_entry(SeqLengths(seqs.lengths[b0:b1], mx), cfg, cfg_c) for b0, b1 in bounds]
             torch = self.torch
-            if self._io_stream is None:
-                self._io_stream = torch.cuda.Stream()  # not the legacy default stream: batched DMA submission
-            io = self._io_stream
-            io.wait_stream(torch.cuda.current_stream())
-            with torch.cuda.stream(io):
-                s = _lib.stream_ptr()
-                _lib.call("bt_copy_rows", xp.data_ptr(), x_pinned.data_ptr(), lp, bs, mx, k * 4, 1, s)
-                if graph is not None:
-                    graph.replay()
-                else:
-                    run()
-                _lib.call("bt_copy_rows", out_pinned.data_ptr(), yp.data_ptr(), lp, bs, mx, k * 4, 0, s)
+            if self._io_streams is None:
+                self._io_streams = (torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream())
+            h2d, comp, d2h = self._io_streams
+            while len(self._io_events) < 2 * len(bounds):
+                self._io_events.append(torch.cuda.Event())
+            ev_in, ev_done = self._io_events[0::2], self._io_events[1::2]
+            h2d.wait_stream(torch.cuda.current_stream())
+            comp.wait_stream(torch.cuda.current_stream())  # the cached graphs' buffers: previous call done
+            row_b = k * 4
+            lp = lengths_h.ctypes.data
+            xb, ob = x_pinned.data_ptr(), out_pinned.data_ptr()
+            for i, ((b0, b1), e) in enumerate(zip(bounds, entries)):
+                with torch.cuda.stream(h2d):
+                    _lib.call("bt_copy_rows", e[2].data_ptr(), xb + b0 * mx * row_b, lp + 4 * b0, b1 - b0, mx, row_b,
+                              1, _lib.stream_ptr())
+                    ev_in[i].record(h2d)
+            for i, e in enumerate(entries):
+                comp.wait_event(ev_in[i])
+                with torch.cuda.stream(comp):
+                    if e[0] is not None:
+                        e[0].replay()
+                    else:
+                        e[1]()
+                    ev_done[i].record(comp)
+            for i, ((b0, b1), e) in enumerate(zip(bounds, entries)):
+                d2h.wait_event(ev_done[i])
+                with torch.cuda.stream(d2h):
+                    _lib.call("bt_copy_rows", ob + b0 * mx * row_b, e[3].data_ptr(), lp + 4 * b0, b1 - b0, mx, row_b,
+                              0, _lib.stream_ptr())
             # padded rows of the output are exact zeros (packing.py:158-159)
             o = out_pinned.numpy().reshape(bs, mx, k)
             for b, n in enumerate(seqs.lengths):
                 if n < mx:
                     o[b, n:] = 0.0
-            io.synchronize()
+            d2h.synchronize()
+            torch.cuda.current_stream().wait_stream(d2h)
             return out_pinned
 
     def layer_device(self, li: int, x_bf16, plan: PackingPlan, stream=None, config: ModelConfig | None = None):

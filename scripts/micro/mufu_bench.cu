@@ -13,7 +13,9 @@ __global__ void k(float* out, int iters) {
   if (OP == 1) asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(x));             \
   if (OP == 2) asm volatile("rcp.approx.ftz.f32 %0, %0;" : "+f"(x));             \
   if (OP == 3) { unsigned r; asm volatile("cvt.rn.bf16x2.f32 %0, %1, %1;" : "=r"(r) : "f"(x)); x = __uint_as_float(r); } \
-  if (OP == 4) asm volatile("fma.rn.f32 %0, %0, %0, %0;" : "+f"(x));
+  if (OP == 4) asm volatile("fma.rn.f32 %0, %0, %0, %0;" : "+f"(x));                \
+  if (OP == 5) asm volatile("ex2.approx.f16x2 %0, %0;" : "+r"(*reinterpret_cast<unsigned*>(&x))); \
+  if (OP == 6) asm volatile("ex2.approx.ftz.bf16x2 %0, %0;" : "+r"(*reinterpret_cast<unsigned*>(&x)));
     OPX(a0) OPX(a1) OPX(a2) OPX(a3) OPX(a4) OPX(a5) OPX(a6) OPX(a7)
   }
   out[blockIdx.x * blockDim.x + threadIdx.x] = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
@@ -44,5 +46,7 @@ int main() {
   run<2>("rcp", out, sms);
   run<3>("cvt_bf16x2", out, sms);
   run<4>("ffma", out, sms);
+  run<5>("ex2_f16x2 (ops = packed instrs; x2 for elements)", out, sms);
+  run<6>("ex2_bf16x2 (ops = packed instrs; x2 for elements)", out, sms);
   return 0;
 }
