@@ -563,12 +563,13 @@ __global__ void __launch_bounds__(MHA_THREADS, 2) mha_fwd_kernel(const __grid_co
         ptx::tmem_st_16x2_16<16>(p_my, pp);
         if (64 >= kblk) {
           // CTA-uniform: no key of the problem among keys 64-127 -> P = 0
-#pragma unroll
-          for (int i = 0; i < 16; ++i) pp[i] = 0u;
+          // (stored from zero registers on this path of its own, so pp is
+          // never half-assigned and stays in registers)
+          ptx::tmem_st_16x2_16_zero<16>(p_my + 32);
         } else {
           exps(r1, pp);
+          ptx::tmem_st_16x2_16<16>(p_my + 32, pp);
         }
-        ptx::tmem_st_16x2_16<16>(p_my + 32, pp);
       }
 
       if (warp_live) {

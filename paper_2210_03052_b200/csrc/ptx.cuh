@@ -253,6 +253,16 @@ __device__ __forceinline__ void tmem_st_16x2_16(uint32_t taddr, const uint32_t (
       "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
       : "memory");
 }
+// the same, every column 0
+template <int OFF>
+__device__ __forceinline__ void tmem_st_16x2_16_zero(uint32_t taddr) {
+  const uint32_t z = 0u;
+  asm volatile(
+      "tcgen05.st.sync.aligned.16x32bx2.x16.b32 [%0], %1, "
+      "{%2,%2,%2,%2,%2,%2,%2,%2,%2,%2,%2,%2,%2,%2,%2,%2};" ::"r"(taddr),
+      "n"(OFF), "r"(z)
+      : "memory");
+}
 template <int OFF>
 __device__ __forceinline__ void tmem_st_16x2_8(uint32_t taddr, const uint32_t* r) {
   asm volatile(
