@@ -20,9 +20,15 @@ Prints ONE JSON line (rank 0).  Keys beyond the driver contract:
   roofline      dominant kernel: algorithmic FLOPs (or bytes) per launch /
                 CUDA-event launch time vs MEASURED_PEAKS.json
   kernels       per-kernel breakdown of one step (event-timed, alone)
-  cpu_baseline  the CPU oracle (numpy port of the reference) on host cores
-  e2e           the same metric through the public API forward() with pinned
-                host input/output, H2D + D2H inside the timed region
+  cpu_baseline  the unmodified reference (baseline/_ref) or, if it is not
+                installed, the CPU oracle, on a bounded sample on host cores
+  parity        the timed output against that CPU output (cosine, max-abs)
+  e2e           the same metric through the public API with host buffers,
+                every step's H2D + D2H inside the timed region: headline =
+                forward_stream (the K steps as one serving stream, copies of
+                batch i+-1 overlapping forward i); per_call = synchronous
+                forward() per step (pinned input; numpy_input: a pageable
+                reference-style Tensor, staging copy included)
 """
 
 from __future__ import annotations
@@ -528,6 +534,64 @@ def run_ours(args, wl):
                "api": "paper_2210_03052_b200.forward(weights, seqs, pinned fp32 [bs*mx,k] host tensor, config) -> "
                       "host Tensor (valid rows DMA'd to / from page-locked host memory around the cached "
                       "CUDA graph of the packed forward)"}
+
+        # serving mode: the same K steps as ONE stream of independent batches
+        # through bt.forward_stream -- every batch's H2D and D2H still inside the
+        # timed region, but overlapped with the neighbouring batches' forwards
+        x_pins = [x_pin, torch.from_numpy(x_host.copy()).pin_memory()]
+        stream_in = [(seqs, x_pins[i % 2]) for i in range(args.steps)]
+        # warm: both slots' graphs, and K pinned output blocks in torch's host
+        # caching allocator (freed again before the timed call reuses them)
+        ys = bt.forward_stream(weights, stream_in, cfg)
+        ys = None
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        flush_l2()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ys = bt.forward_stream(weights, stream_in, cfg)
+        st_ms = (time.perf_counter() - t0) * 1e3 / args.steps
+        assert all(np.array_equal(ys[0].array, yy.array) for yy in ys), "forward_stream batches differ"
+        assert np.array_equal(ys[0].array, y.array), "forward_stream != forward"
+        s_t = torch.tensor([st_ms], dtype=torch.float64, device="cuda" if backend == "nccl" else "cpu")
+        if dist is not None:
+            dist.all_reduce(s_t, op=dist.ReduceOp.MAX)
+        st_ms = float(s_t.item())
+        e2e["stream"] = {"value": round(bs_global / (st_ms / 1e3), 2), "unit": "seq/s", "ms_per_step": round(st_ms, 4),
+                         "h2d_bytes_per_step": e2e["h2d_bytes_per_step"],
+                         "d2h_bytes_per_step": e2e["d2h_bytes_per_step"],
+                         "api": f"paper_2210_03052_b200.forward_stream(weights, [(seqs, pinned fp32 input)] x "
+                                f"{args.steps}, config): the K steps as one stream of batches, H2D(i+1) and "
+                                f"D2H(i-1) overlapping forward(i); each output bitwise the forward() result"}
+        log(f"[bench] e2e stream per-step ms: {st_ms:.3f}")
+        # reference-style caller: a numpy-backed Tensor (pageable memory), so
+        # forward() stages it into page-locked memory inside the timed call
+        x_np = bt.Tensor(x_host)
+        for _ in range(2):
+            y = bt.forward(weights, seqs, x_np, cfg)
+        torch.cuda.synchronize()
+        tn = []
+        for _ in range(max(3, min(args.steps, 10))):
+            flush_l2()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            y = bt.forward(weights, seqs, x_np, cfg)
+            tn.append(time.perf_counter() - t0)
+        np_ms = statistics.median(tn) * 1e3
+        log(f"[bench] e2e per-call (numpy input) median ms: {np_ms:.3f}")
+        per_call = {k: e2e[k] for k in ("value", "unit", "ms_per_step", "ms_per_step_median", "h2d_bytes_per_step",
+                                        "d2h_bytes_per_step", "api")}
+        per_call["numpy_input"] = {"value": round(bs_global / (np_ms / 1e3), 2), "unit": "seq/s",
+                                   "ms_per_step_median": round(np_ms, 4),
+                                   "api": "forward(weights, seqs, reference-style numpy Tensor, config): includes "
+                                          "the copy of the pageable input into page-locked memory"}
+        stream = e2e.pop("stream")
+        # headline e2e: the serving stream (every step's H2D and D2H inside the
+        # timed region); the synchronous per-call numbers ride along
+        e2e = dict(stream)
+        e2e["mode"] = "stream"
+        e2e["per_call"] = per_call
 
     result = None
     if rank == 0:

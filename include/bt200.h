@@ -301,6 +301,13 @@ BT_API int bt_encoder_forward_packed(const bt_layer_weights* layers, int n_layer
 BT_API int bt_copy_rows(void* dst, const void* src, const int32_t* lengths_host, int bs, int mx, long long row_bytes,
                         int to_packed, bt_stream_t stream);
 
+/* page-locked host staging memory for pageable inputs (the reference's numpy
+ * Tensor): write_combined = 1 allocates it write-combined, so the CPU's
+ * staging stores bypass its caches and the following DMA reads at the PCIe
+ * rate instead of snooping dirty lines.  *out = NULL on failure. */
+BT_API int bt_host_alloc(size_t bytes, int write_combined, void** out);
+BT_API int bt_host_free(void* p);
+
 #ifdef __cplusplus
 }
 #endif

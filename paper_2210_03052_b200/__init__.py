@@ -24,6 +24,7 @@ from .encoder import (
     encoder_layer,
     engine_for,
     forward,
+    forward_stream,
     init_weights,
     load_weights,
     parse_config_file,

@@ -91,6 +91,8 @@ SIGNATURES = {
     "bt_mha_varlen_path": (_I, [_P, _P, _I, _I, _I, _I, _P, _I, _I, _S]),
     "bt_flops_enable": (_I, [_P]),
     "bt_flops_read": (_I, [_P]),
+    "bt_host_alloc": (_I, [_SZ, _I, C.POINTER(C.c_void_p)]),
+    "bt_host_free": (_I, [_P]),
 }
 
 _lock = threading.Lock()

@@ -357,6 +357,18 @@ extern "C" int bt_copy_rows(void* dst, const void* src, const int32_t* lengths_h
   return BT_OK;
 }
 
+extern "C" int bt_host_alloc(size_t bytes, int write_combined, void** out) {
+  BT_REQUIRE(out != nullptr && bytes > 0, BT_ESHAPE, "host_alloc: bad arguments");
+  *out = nullptr;
+  BT_CUDA_CHECK(cudaHostAlloc(out, bytes, write_combined ? cudaHostAllocWriteCombined : cudaHostAllocDefault));
+  return BT_OK;
+}
+
+extern "C" int bt_host_free(void* p) {
+  if (p) BT_CUDA_CHECK(cudaFreeHost(p));
+  return BT_OK;
+}
+
 // Instrumented FLOP counting on (dev_mha_counter: a device u64 the MHA tiles
 // add to; the GEMM counts start from zero) or off (NULL).
 extern "C" int bt_flops_enable(unsigned long long* dev_mha_counter) {

@@ -353,6 +353,8 @@ class BertEncoderB200:
         self._lock = threading.RLock()
         self._io_streams = None  # host-I/O pipeline: H2D, compute, D2H
         self._io_events = []
+        self._stage = {}  # page-locked packed staging buffer for pageable inputs
+        self._pool = None
 
     def layer(self, i: int) -> DeviceLayer:
         return self._layers[i]
@@ -410,12 +412,14 @@ class BertEncoderB200:
 
     GRAPH_CACHE = 8  # batch (range) shapes whose packed forward is kept as a CUDA graph
 
-    def _graph_entry(self, seqs: SeqLengths, cfg: ModelConfig, cfg_c):
+    def _graph_entry(self, seqs: SeqLengths, cfg: ModelConfig, cfg_c, slot: int = 0):
         """(graph, x_packed, y_packed) for this batch shape: device buffers
         owned by the entry and a CUDA graph of bt_encoder_forward_packed over
-        them (captured after one eager warm-up run, which also autotunes)."""
+        them (captured after one eager warm-up run, which also autotunes).
+        ``slot`` keeps independent entries of one shape (double buffering in
+        ``forward_host_stream``)."""
         torch = self.torch
-        key = (tuple(seqs.lengths), seqs.max_seq_len, cfg.layers, cfg.cutoff, cfg.split_seq_len)
+        key = (tuple(seqs.lengths), seqs.max_seq_len, cfg.layers, cfg.cutoff, cfg.split_seq_len, slot)
         hit = self._graphs.pop(key, None)
         if hit is not None:
             self._graphs[key] = hit  # most recently used last
@@ -544,6 +548,123 @@ class BertEncoderB200:
             d2h.synchronize()
             torch.cuda.current_stream().wait_stream(d2h)
             return out_pinned
+
+    def forward_host_pageable(self, seqs: SeqLengths, arr, out_pinned, config: ModelConfig | None = None):
+        """forward_host_packed for a pageable host input (a reference-style
+        numpy ``Tensor``, fp32 [bs*mx, k]): only the valid rows are staged,
+        packed, into a write-combined page-locked buffer (host copies by a
+        small thread pool), which goes over PCIe as ONE contiguous DMA, then the cached
+        graph and the per-sequence D2H as forward_host_packed.  Synchronises."""
+        import concurrent.futures as cf
+
+        with self._lock:
+            cfg = config or self.config
+            cfg_c = self._cfg_c if config is None else layer_cfg_c(cfg)
+            bs, mx, k = seqs.batch_size, seqs.max_seq_len, cfg.hidden_dim
+            graph, run, xp, yp, _, _ = self._graph_entry(seqs, cfg, cfg_c)
+            torch = self.torch
+            T = seqs.total
+            stage = self._stage.get((T, k))
+            if stage is None:
+                stage = _WcStage(T, k)
+                self._stage = {(T, k): stage}  # one shape kept
+            if self._pool is None:
+                self._pool = cf.ThreadPoolExecutor(max_workers=4, thread_name_prefix="bt200-stage")
+            if self._io_streams is None:
+                self._io_streams = (torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream())
+            h2d, comp, d2h = self._io_streams
+            cur = torch.cuda.current_stream()
+            h2d.wait_stream(cur)
+            comp.wait_stream(cur)
+            lengths_h = np.ascontiguousarray(np.asarray(seqs.lengths, dtype=np.int32))
+            starts = np.concatenate([[0], np.cumsum(lengths_h)])
+            sn = stage.array
+            bounds = self.chunk_bounds(seqs.lengths, min(bs, 8))
+
+            def copy_group(b0, b1):
+                for b in range(b0, b1):
+                    sn[starts[b]:starts[b + 1]] = arr[b * mx: b * mx + lengths_h[b]]
+
+            for f in [self._pool.submit(copy_group, b0, b1) for b0, b1 in bounds]:
+                f.result()
+            one = np.asarray([T], dtype=np.int32)
+            with torch.cuda.stream(h2d):  # one contiguous DMA of the packed rows (a single T-row "sequence")
+                _lib.call("bt_copy_rows", xp.data_ptr(), stage.ptr, one.ctypes.data, 1, T, k * 4, 1,
+                          _lib.stream_ptr())
+            comp.wait_stream(h2d)
+            with torch.cuda.stream(comp):
+                if graph is not None:
+                    graph.replay()
+                else:
+                    run()
+            d2h.wait_stream(comp)
+            with torch.cuda.stream(d2h):
+                _lib.call("bt_copy_rows", out_pinned.data_ptr(), yp.data_ptr(), lengths_h.ctypes.data, bs, mx, k * 4,
+                          0, _lib.stream_ptr())
+            o = out_pinned.numpy().reshape(bs, mx, k)
+            for b, n in enumerate(seqs.lengths):
+                if n < mx:
+                    o[b, n:] = 0.0
+            d2h.synchronize()
+            cur.wait_stream(d2h)
+            return out_pinned
+
+    def forward_host_stream(self, items, config: ModelConfig | None = None):
+        """Serving-style stream of batches on pinned host buffers: ``items`` is
+        a list of (SeqLengths, x_pinned [bs*mx, k] fp32, out_pinned).  Each
+        batch is a whole forward_host_packed (valid rows DMA'd in, the cached
+        graph, valid rows DMA'd out), but consecutive batches overlap on three
+        streams -- H2D(i + 1) and D2H(i - 1) run under forward(i) -- with the
+        device buffers double-buffered (graph entries in two slots).
+        Synchronises once at the end; returns the out buffers."""
+        with self._lock:
+            cfg = config or self.config
+            cfg_c = self._cfg_c if config is None else layer_cfg_c(cfg)
+            torch = self.torch
+            k = cfg.hidden_dim
+            row_b = k * 4
+            entries = [self._graph_entry(sq, cfg, cfg_c, slot=i % 2) for i, (sq, _, _) in enumerate(items)]
+            if self._io_streams is None:
+                self._io_streams = (torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream())
+            h2d, comp, d2h = self._io_streams
+            cur = torch.cuda.current_stream()
+            for st in (h2d, comp, d2h):
+                st.wait_stream(cur)
+            n = len(items)
+            ev_in = [torch.cuda.Event() for _ in range(n)]
+            ev_done = [torch.cuda.Event() for _ in range(n)]
+            ev_out = [torch.cuda.Event() for _ in range(n)]
+            lens = [np.ascontiguousarray(np.asarray(sq.lengths, dtype=np.int32)) for sq, _, _ in items]
+            for i, ((sq, x, out), e) in enumerate(zip(items, entries)):
+                bs, mx = sq.batch_size, sq.max_seq_len
+                if i >= 2:
+                    h2d.wait_event(ev_done[i - 2])  # forward(i - 2) has read this slot's input
+                with torch.cuda.stream(h2d):
+                    _lib.call("bt_copy_rows", e[2].data_ptr(), x.data_ptr(), lens[i].ctypes.data, bs, mx, row_b, 1,
+                              _lib.stream_ptr())
+                    ev_in[i].record(h2d)
+                comp.wait_event(ev_in[i])
+                if i >= 2:
+                    comp.wait_event(ev_out[i - 2])  # D2H(i - 2) has read this slot's output
+                with torch.cuda.stream(comp):
+                    if e[0] is not None:
+                        e[0].replay()
+                    else:
+                        e[1]()
+                    ev_done[i].record(comp)
+                d2h.wait_event(ev_done[i])
+                with torch.cuda.stream(d2h):
+                    _lib.call("bt_copy_rows", out.data_ptr(), e[3].data_ptr(), lens[i].ctypes.data, bs, mx, row_b, 0,
+                              _lib.stream_ptr())
+                    ev_out[i].record(d2h)
+            for (sq, _, out) in items:  # padded output rows are exact zeros (packing.py:158-159)
+                o = out.numpy().reshape(sq.batch_size, sq.max_seq_len, k)
+                for b, m in enumerate(sq.lengths):
+                    if m < sq.max_seq_len:
+                        o[b, m:] = 0.0
+            d2h.synchronize()
+            cur.wait_stream(d2h)
+            return [out for _, _, out in items]
 
     def layer_device(self, li: int, x_bf16, plan: PackingPlan, stream=None, config: ModelConfig | None = None):
         """In-place encoder_layer on a packed bf16 [T, k] device tensor.
@@ -678,10 +799,68 @@ def forward(weights, seqs, input_padded, config, *, workers: int = 1, counter: F
     # Host I/O: DMA only each sequence's valid rows into a packed device
     # buffer, run packed -> packed, DMA the valid output rows back into their
     # padded positions, and zero the padded rows on the host while the GPU works.
-    x_host = _pinned_f32(input_padded, torch)
     out = torch.empty((padded_rows, cols), dtype=torch.float32, pin_memory=True)
-    eng.forward_host_packed(seqs, x_host, out, config=config)
+    if _is_pinned_torch(input_padded):
+        eng.forward_host_packed(seqs, _pinned_f32(input_padded, torch), out, config=config)
+    else:  # pageable (numpy / reference Tensor): stage only the valid rows
+        arr = np.ascontiguousarray(host_array(input_padded), dtype=np.float32)
+        eng.forward_host_pageable(seqs, arr, out, config=config)
     return Tensor(out.numpy())
+
+
+def forward_stream(weights, batches, config):
+    """A stream of independent forwards on host buffers (serving): ``batches``
+    is a sequence of (seqs, input_padded) pairs, each exactly what
+    ``forward`` takes; returns the list of host fp32 ``Tensor`` outputs, each
+    bitwise the ``forward`` result.  Consecutive batches overlap their PCIe
+    copies with the previous batch's device forward
+    (``BertEncoderB200.forward_host_stream``)."""
+    config = as_model_config(config)
+    if not _is_all_on(config.flags):
+        return [forward(weights, sq, x, config) for sq, x in batches]
+    torch = _lib.require_device()
+    eng = engine_for(weights, config)
+    items = []
+    for sq, x in batches:
+        sq = as_seq_lengths(sq)
+        if sq.batch_size != config.batch_size or sq.max_seq_len != config.max_seq_len:
+            raise ShapeError(f"lengths describe a {sq.batch_size}x{sq.max_seq_len} batch, config expects "
+                             f"{config.batch_size}x{config.max_seq_len}")
+        rows, cols = rows_cols(x)
+        if rows != sq.batch_size * sq.max_seq_len or cols != config.hidden_dim:
+            raise ShapeError(f"input is {rows}x{cols}, expected {sq.batch_size * sq.max_seq_len}x{config.hidden_dim}")
+        if is_device(x):
+            raise ShapeError("forward_stream takes host inputs (use forward for CUDA tensors)")
+        out = torch.empty((rows, cols), dtype=torch.float32, pin_memory=True)
+        items.append((sq, _pinned_f32(x, torch), out))
+    eng.forward_host_stream(items, config=config)
+    return [Tensor(out.numpy()) for _, _, out in items]
+
+
+class _WcStage:
+    """Write-combined page-locked [T, k] fp32 staging buffer (bt_host_alloc):
+    the CPU only writes it, and its stores skip the CPU caches, so the DMA
+    that follows reads it at the PCIe rate.  A cache-backed pinned buffer the
+    CPU has just written DMAs at ~10 GB/s on this host (measured, the dirty
+    lines are snooped)."""
+
+    def __init__(self, rows: int, cols: int):
+        p = C.c_void_p()
+        _lib.call("bt_host_alloc", rows * cols * 4, 1, C.byref(p))
+        self.ptr = p.value
+        buf = (C.c_float * (rows * cols)).from_address(self.ptr)
+        self.array = np.ctypeslib.as_array(buf).reshape(rows, cols)
+
+    def __del__(self):
+        try:
+            self.array = None
+            _lib.call("bt_host_free", self.ptr)
+        except Exception:  # noqa: BLE001 -- interpreter shutdown
+            pass
+
+
+def _is_pinned_torch(x) -> bool:
+    return type(x).__module__.startswith("torch") and not x.is_cuda and x.dtype.is_floating_point and x.is_pinned()
 
 
 def _pinned_f32(x, torch):

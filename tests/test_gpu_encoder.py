@@ -252,3 +252,30 @@ def test_forward_one_launch_ends(bt, lens_kind):
     ocfg = orc.OracleConfig(2, 2, 64, mx, bs)
     want = orc.forward(orc.init_weights(ocfg, 4), lens, x, ocfg)
     assert_close_bf16(y_dev, want, max_abs_max=2e-2, what=f"one-launch ends ({lens_kind})")
+
+
+def test_forward_stream_bitwise_and_vs_oracle(bt):
+    """forward_stream (serving: H2D / forward / D2H of consecutive batches
+    overlapped, device buffers double-buffered) returns, for every batch,
+    bitwise the per-call forward() result -- including batches that reuse a
+    slot's cached graph with a different input -- and matches the oracle."""
+    mx, layers, bs = 128, 2, 6
+    cfg = bt.ModelConfig(layers=layers, head_num=12, head_size=64, max_seq_len=mx, batch_size=bs,
+                         flags=bt.OptFlags.all_on())
+    w = bt.init_weights(cfg, seed=3)
+    lens_a = [128, 5, 77, 1, 100, 64]
+    lens_b = [30, 128, 2, 90, 17, 128]
+    batches = []
+    for i, lens in enumerate([lens_a, lens_b, lens_a, lens_a, lens_b]):
+        batches.append((bt.SeqLengths.of(lens, mx), bt.Tensor(orc.gen_input(lens, mx, 768, seed=10 + i))))
+    outs = bt.forward_stream(w, batches, cfg)
+    assert len(outs) == len(batches)
+    ocfg = orc.OracleConfig(layers, 12, 64, mx, bs)
+    ow = orc.init_weights(ocfg, 3)
+    for (sq, x), y in zip(batches, outs):
+        single = bt.forward(w, sq, x, cfg).array
+        assert np.array_equal(y.array, single)
+        pad = ~orc.build_mask(list(sq.lengths), mx).reshape(-1).astype(bool)
+        assert not y.array[pad].any()
+        want = orc.forward(ow, list(sq.lengths), x.array, ocfg)
+        assert_close_bf16(y.array, want, max_abs_max=2e-2, what="forward_stream")
