@@ -36,6 +36,20 @@
 
 namespace bt {
 
+// GLN_MCAST = 1: the CL CTAs of a cluster share one row block of A, so each
+// A k-block is TMA-loaded ONCE per cluster (by CTA kb % CL) and multicast
+// into every CTA's ring; a ring stage is refilled only after all CL MMA
+// issuers have released it (their commits multicast to every CTA's empty
+// barrier).  L2 -> SM traffic per cluster drops from CL x (A + B) to
+// A + CL x B per k-block.  Correct (the GEMM+LN tests pass with it) but
+// measured SLOWER at C2: 8.8 vs 8.3 us per launch (the cluster-wide stage
+// release puts the six CTAs in lockstep; the per-SM feed is not what the L2
+// dedup of the six simultaneous unicast loads leaves short).  0 (default):
+// every CTA loads its own copy of A.
+#ifndef GLN_MCAST
+#define GLN_MCAST 0
+#endif
+
 constexpr int GLN_BN = 128;
 constexpr int GLN_BK = 64;
 constexpr int GLN_STAGES = 5;
@@ -106,10 +120,11 @@ __global__ void __launch_bounds__(GLN_THREADS, 1)
   const int n0 = rank * GLN_BN;
   const int row_base = rb * 128;
 
+  constexpr uint16_t all_ctas = static_cast<uint16_t>((1u << CL) - 1u);
   if (threadIdx.x == 0) {
     for (int s = 0; s < GLN_STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&empty[s], 1);
+      ptx::mbar_init(&empty[s], GLN_MCAST ? CL : 1);  // multicast A: every CTA's MMA must release the stage
     }
     ptx::mbar_init(tfull, 1);
     ptx::mbar_init(rfull, 1);
@@ -120,7 +135,11 @@ __global__ void __launch_bounds__(GLN_THREADS, 1)
     ptx::tmem_relinquish();
   }
   ptx::tc_fence_before();
-  __syncthreads();
+  if (GLN_MCAST) {
+    ptx::cluster_sync();  // every CTA's barriers exist before any multicast load / commit reaches them
+  } else {
+    __syncthreads();
+  }
   ptx::tc_fence_after();
   const uint32_t tmem = *holder;
   ptx::griddep_launch_dependents();
@@ -158,7 +177,12 @@ __global__ void __launch_bounds__(GLN_THREADS, 1)
           ptx::mbar_arrive_expect_tx(&full[stage], 2 * GLN_TILE);
           ptx::tma_load_2d(sB + stage * GLN_TILE, &tmB, &full[stage], kb * GLN_BK, n0);
         }
-        ptx::tma_load_2d(sA + stage * GLN_TILE, &tmA, &full[stage], kb * GLN_BK, row_base);
+        if (GLN_MCAST) {
+          if (kb % CL == rank)
+            ptx::tma_load_2d_mc(sA + stage * GLN_TILE, &tmA, &full[stage], kb * GLN_BK, row_base, all_ctas);
+        } else {
+          ptx::tma_load_2d(sA + stage * GLN_TILE, &tmA, &full[stage], kb * GLN_BK, row_base);
+        }
       }
       __syncwarp();
     }
@@ -175,7 +199,10 @@ __global__ void __launch_bounds__(GLN_THREADS, 1)
       if (ptx::elect_one()) {
 #pragma unroll
         for (int k = 0; k < GLN_BK / 16; ++k) ptx::mma_bf16_ss(tmem, ad + 2 * k, bd + 2 * k, idesc, (kb | k) ? 1u : 0u);
-        ptx::mma_commit(&empty[stage]);
+        if (GLN_MCAST)
+          ptx::mma_commit_mc(&empty[stage], all_ctas);
+        else
+          ptx::mma_commit(&empty[stage]);
       }
       __syncwarp();
     }
