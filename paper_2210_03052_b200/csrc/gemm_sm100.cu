@@ -487,6 +487,7 @@ __global__ void __launch_bounds__(GemmCfg<PAIR, BN, EW>::THREADS, 1)
         for (int c = colgrp * 64; c < BN; c += 64 * NGRP) {
           uint32_t r0[32], r1[32];
           const int col = nb * BN + c;
+          if (col >= p.N) continue;  // partial last N tile (N % BN != 0): columns past N are never stored
           // bias for the 64 columns, loaded before the TMEM wait so its latency
           // overlaps the accumulator load instead of heading the math chain
           // (stream-K variants keep the in-chain loads: the hoisted registers
@@ -653,6 +654,15 @@ struct GemmChoice {
 // ceil(work / units) k-blocks per unit plus a fix-up cost for split tiles.
 // Plus a fixed fill / drain cost.
 static bool g_auto_streamk = false;  // stream-K among the automatic candidates (off: see choose_tile)
+// Tile widths that need not divide N: the last N tile is partial (its B rows
+// past N are zero-filled by TMA, its columns past N are skipped by the
+// epilogue), worth it when the tile count fits the SMs better (e.g. N = 1024
+// as 6 x 192 at BERT-large).  Allowed while the padded columns are at most
+// a quarter of N.
+static bool bn_ok(int N, int bn) {
+  const int tiles = (N + bn - 1) / bn;
+  return N % bn == 0 || (N % 64 == 0 && 4 * (tiles * bn - N) <= N);
+}
 static GemmChoice choose_tile(int M, int N, int K, int sms) {
   struct Cand { int pair, bn; };
   const Cand cands[] = {{2, 256}, {2, 192}, {2, 128}, {1, 256}, {1, 192}, {1, 128}, {1, 64}};
@@ -660,9 +670,9 @@ static GemmChoice choose_tile(int M, int N, int K, int sms) {
   double best_cost = 1e300;
   const int nk = K / GEMM_BK;
   for (const Cand& c : cands) {
-    if (N % c.bn) continue;
+    if (!bn_ok(N, c.bn)) continue;
     const int bm = 128 * c.pair;
-    const long long tiles = static_cast<long long>((M + bm - 1) / bm) * (N / c.bn);
+    const long long tiles = static_cast<long long>((M + bm - 1) / bm) * ((N + c.bn - 1) / c.bn);
     const long long units = sms / c.pair;
     const double mma = 4.0 * (128.0 * c.bn / 256.0);                      // MMA cycles per k-block
     const double feed = (128.0 + c.bn / c.pair) * GEMM_BK * 2.0 / 55.0;  // TMA cycles per k-block
@@ -682,7 +692,7 @@ static GemmChoice choose_tile(int M, int N, int K, int sms) {
     // summation order with the unit count, and the forward guarantees
     // results that do not depend on M (a shard equals its rows of the full
     // batch, bit for bit).
-    if (g_auto_streamk && tiles % units != 0 && tiles <= 4 * units && units <= MAX_UNITS) {
+    if (g_auto_streamk && N % c.bn == 0 && tiles % units != 0 && tiles <= 4 * units && units <= MAX_UNITS) {
       const long long work = tiles * nk;
       const double per_unit = static_cast<double>((work + units - 1) / units);
       const double fixup = 8000.0;  // measured: partial write + fence/flag + read costs ~4 us per split tile
@@ -709,7 +719,8 @@ static int dispatch_sk(bool sk, int epi, const CUtensorMap& ta, const CUtensorMa
 static int gemm_run(const void* A, const void* Bt, const float* bias, const void* residual, void* C, int M, int N,
                     int K, int epi, GemmChoice ch, cudaStream_t s) {
   const int sms = num_sms() > 0 ? num_sms() : 148;
-  BT_REQUIRE(N % ch.bn == 0, BT_ESHAPE, "gemm: N=%d not a multiple of BN=%d", N, ch.bn);
+  BT_REQUIRE(N % 64 == 0, BT_ESHAPE, "gemm: N=%d not a multiple of 64", N);
+  if (N % ch.bn) ch.streamk = false;  // stream-K partials assume whole tiles
   const int bm = 128 * ch.pair;
   CUtensorMap ta, tb, tc;
   BT_TRY(make_tmap_bf16_2d(&ta, A, M, K, K, 128, GEMM_BK));
@@ -723,7 +734,7 @@ static int gemm_run(const void* A, const void* Bt, const float* bias, const void
   p.bias = bias;
   p.residual = static_cast<const __nv_bfloat16*>(residual);
   p.num_m_blocks = (M + bm - 1) / bm;
-  p.num_n_blocks = N / ch.bn;
+  p.num_n_blocks = (N + ch.bn - 1) / ch.bn;
   p.num_tiles = p.num_m_blocks * p.num_n_blocks;
   p.num_k = K / GEMM_BK;
   p.work = static_cast<long long>(p.num_tiles) * p.num_k;
@@ -814,12 +825,12 @@ static int autotune(const void* A, const void* Bt, const float* bias, const void
   float best_ms = 1e30f;
   GemmChoice best = choose_tile(M, N, K, sms);
   for (const Cand& c : cands) {
-    if (N % c.bn) continue;
+    if (!bn_ok(N, c.bn)) continue;
     const int bm = 128 * c.pair;
-    const long long tiles = static_cast<long long>((M + bm - 1) / bm) * (N / c.bn);
+    const long long tiles = static_cast<long long>((M + bm - 1) / bm) * ((N + c.bn - 1) / c.bn);
     const long long units = sms / c.pair;
     for (int sk = 0; sk < 2; ++sk) {
-      if (sk && !(g_auto_streamk && tiles % units != 0 && tiles <= 4 * units)) continue;
+      if (sk && !(g_auto_streamk && N % c.bn == 0 && tiles % units != 0 && tiles <= 4 * units)) continue;
       const GemmChoice ch{c.pair, c.bn, sk != 0};
       BT_TRY(gemm_run(A, Bt, bias, residual, C, M, N, K, epi, ch, s));  // warm (module load, L2)
       // three rounds of 5 back-to-back launches, each queued behind a ~40 us

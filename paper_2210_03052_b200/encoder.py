@@ -282,10 +282,11 @@ class DeviceLayer:
     vectors, plus the C struct the library reads."""
 
     def __init__(self, layer, torch):
-        def mat(w):  # [in, out] -> [out, in] bf16
+        def mat(w):  # [in, out] -> [out, in] bf16: the fp32 matrix goes up as is, transpose + cast on the device
             if is_device(w):
                 return w.t().to(torch.bfloat16).contiguous()
-            return torch.from_numpy(np.ascontiguousarray(np.asarray(w, np.float32).T)).to("cuda").to(torch.bfloat16)
+            return torch.from_numpy(np.ascontiguousarray(w, dtype=np.float32)).to("cuda").t().to(
+                torch.bfloat16).contiguous()
 
         def vec(v):
             if is_device(v):

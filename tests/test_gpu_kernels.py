@@ -43,8 +43,8 @@ def test_gemm(env, bn, epi, M, N, K):
     bt, torch = env
     from paper_2210_03052_b200.tensor import gemm_device
 
-    if N % abs(bn):
-        pytest.skip("N not a multiple of BN")
+    # N % BN != 0 (e.g. N = 1024 with 192-wide tiles) runs a partial last N
+    # tile: B rows past N zero-filled by TMA, columns past N never stored
     a = (torch.randn(M, K, device="cuda") * 0.5).to(torch.bfloat16)
     w = (torch.randn(N, K, device="cuda") / math.sqrt(K)).to(torch.bfloat16)
     bias = torch.randn(N, device="cuda") * 0.1
