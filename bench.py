@@ -527,8 +527,8 @@ def run_ours(args, wl):
         e2e_ms = float(e_t.item())
         e2e = {"value": round(bs_global / (e2e_ms / 1e3), 2), "unit": "seq/s", "ms_per_step": round(e2e_ms, 4),
                "ms_per_step_median": round(statistics.median(t) * 1e3, 4),
-               # bytes that cross PCIe per step: each sequence's valid fp32 rows, in and out (batched
-               # DMA; padded output rows are zeroed on the host while the GPU computes)
+               # bytes that cross PCIe per step: each sequence's valid fp32 rows, in and out (one
+               # cudaMemcpyAsync per run of rows; padded output rows are zeroed on the host meanwhile)
                "h2d_bytes_per_step": int(T * hidden * 4) * world,
                "d2h_bytes_per_step": int(T * hidden * 4) * world,
                "api": "paper_2210_03052_b200.forward(weights, seqs, pinned fp32 [bs*mx,k] host tensor, config) -> "
