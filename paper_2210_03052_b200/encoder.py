@@ -323,6 +323,9 @@ def layer_cfg_c(config: ModelConfig) -> _lib.LayerCfgC:
 
 # host-I/O pipeline depth of forward() on host buffers (BertEncoderB200.default_chunks)
 E2E_CHUNKS_DEFAULT = 1
+# forward_host_stream: batches of more sequences than this move their padded
+# buffers as one DMA each way instead of one DMA per sequence
+STREAM_ROW_COPIES_MAX = 512
 
 
 class BertEncoderB200:
@@ -436,9 +439,47 @@ class BertEncoderB200:
             _lib.call("bt_encoder_forward_packed", self._c_layers, cfg.layers, C.byref(cfg_c), lengths_dev.data_ptr(),
                       bs, T, xp.data_ptr(), yp.data_ptr(), ws.data_ptr(), ws_bytes, _lib.stream_ptr())
 
-        run()  # warm-up: module load, GEMM autotune
+        entry = (self._capture(run), run, xp, yp, lengths_dev, ws)
+        self._graphs[key] = entry
+        while len(self._graphs) > self.GRAPH_CACHE:
+            self._graphs.pop(next(iter(self._graphs)))
+        return entry
+
+    def _padded_entry(self, seqs: SeqLengths, cfg: ModelConfig, cfg_c, slot: int = 0):
+        """As _graph_entry, over the PADDED layout: device buffers [bs*mx, k]
+        fp32 in and out and a CUDA graph of bt_encoder_forward (device plan,
+        pack, layers, fp32 output rows with exact-zero padded rows), so the
+        host copies are one contiguous DMA each way.  Used where per-sequence
+        row copies would be thousands of DMA commands per batch."""
+        torch = self.torch
+        key = ("padded", tuple(seqs.lengths), seqs.max_seq_len, cfg.layers, cfg.cutoff, cfg.split_seq_len, slot)
+        hit = self._graphs.pop(key, None)
+        if hit is not None:
+            self._graphs[key] = hit
+            return hit
+        bs, T, k, mx = seqs.batch_size, seqs.total, cfg.hidden_dim, seqs.max_seq_len
+        lengths_dev = torch.tensor(seqs.lengths, dtype=torch.int32, device="cuda")
+        xp = torch.empty((bs * mx, k), dtype=torch.float32, device="cuda")
+        yp = torch.empty((bs * mx, k), dtype=torch.float32, device="cuda")
+        ws_bytes = int(_lib.load().bt_forward_workspace_bytes(C.byref(cfg_c), bs, T))
+        ws = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
+
+        def run():
+            _lib.call("bt_encoder_forward", self._c_layers, cfg.layers, C.byref(cfg_c), lengths_dev.data_ptr(), bs, T,
+                      xp.data_ptr(), yp.data_ptr(), ws.data_ptr(), ws_bytes, _lib.stream_ptr())
+
+        entry = (self._capture(run), run, xp, yp, lengths_dev, ws)
+        self._graphs[key] = entry
+        while len(self._graphs) > self.GRAPH_CACHE:
+            self._graphs.pop(next(iter(self._graphs)))
+        return entry
+
+    def _capture(self, run):
+        """A CUDA graph of run() (after one eager warm-up, which also
+        autotunes the GEMMs), or None where capture is unsupported."""
+        torch = self.torch
+        run()
         torch.cuda.synchronize()
-        graph = None
         try:
             g = torch.cuda.CUDAGraph()
             side = torch.cuda.Stream()
@@ -448,14 +489,9 @@ class BertEncoderB200:
             torch.cuda.current_stream().wait_stream(side)
             with torch.cuda.graph(g):
                 run()
-            graph = g
+            return g
         except Exception:  # noqa: BLE001 -- graph capture unsupported here: launch eagerly
-            graph = None
-        entry = (graph, run, xp, yp, lengths_dev, ws)
-        self._graphs[key] = entry
-        while len(self._graphs) > self.GRAPH_CACHE:
-            self._graphs.pop(next(iter(self._graphs)))
-        return entry
+            return None
 
     @staticmethod
     def chunk_bounds(lengths, chunks) -> list[tuple[int, int]]:
@@ -644,7 +680,14 @@ class BertEncoderB200:
             torch = self.torch
             k = cfg.hidden_dim
             row_b = k * 4
-            entries = [self._graph_entry(sq, cfg, cfg_c, slot=i % 2) for i, (sq, _, _) in enumerate(items)]
+            # per-sequence valid-row DMA for small batches; a whole padded
+            # buffer per direction for large ones (C5: 2 x 2048 row copies per
+            # batch fill the DMA command queue and stall the host's enqueue
+            # of the next batch -- 91 ms gaps between forwards, measured)
+            padded = [sq.batch_size > STREAM_ROW_COPIES_MAX for sq, _, _ in items]
+            entries = [self._padded_entry(sq, cfg, cfg_c, slot=i % 2) if pd else
+                       self._graph_entry(sq, cfg, cfg_c, slot=i % 2)
+                       for i, ((sq, _, _), pd) in enumerate(zip(items, padded))]
             if self._io_streams is None:
                 self._io_streams = (torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream())
             h2d, comp, d2h = self._io_streams
@@ -656,13 +699,18 @@ class BertEncoderB200:
             ev_done = [torch.cuda.Event() for _ in range(n)]
             ev_out = [torch.cuda.Event() for _ in range(n)]
             lens = [np.ascontiguousarray(np.asarray(sq.lengths, dtype=np.int32)) for sq, _, _ in items]
+            whole = [np.asarray([sq.batch_size * sq.max_seq_len], dtype=np.int32) for sq, _, _ in items]
             for i, ((sq, x, out), e) in enumerate(zip(items, entries)):
                 bs, mx = sq.batch_size, sq.max_seq_len
                 if i >= 2:
                     h2d.wait_event(ev_done[i - 2])  # forward(i - 2) has read this slot's input
                 with torch.cuda.stream(h2d):
-                    _lib.call("bt_copy_rows", e[2].data_ptr(), x.data_ptr(), lens[i].ctypes.data, bs, mx, row_b, 1,
-                              _lib.stream_ptr())
+                    if padded[i]:  # one contiguous copy of the padded input
+                        _lib.call("bt_copy_rows", e[2].data_ptr(), x.data_ptr(), whole[i].ctypes.data, 1, bs * mx,
+                                  row_b, 1, _lib.stream_ptr())
+                    else:
+                        _lib.call("bt_copy_rows", e[2].data_ptr(), x.data_ptr(), lens[i].ctypes.data, bs, mx, row_b,
+                                  1, _lib.stream_ptr())
                     ev_in[i].record(h2d)
                 comp.wait_event(ev_in[i])
                 if i >= 2:
@@ -675,11 +723,16 @@ class BertEncoderB200:
                     ev_done[i].record(comp)
                 d2h.wait_event(ev_done[i])
                 with torch.cuda.stream(d2h):
-                    _lib.call("bt_copy_rows", out.data_ptr(), e[3].data_ptr(), lens[i].ctypes.data, bs, mx, row_b, 0,
-                              _lib.stream_ptr())
+                    if padded[i]:  # the device wrote the exact-zero padded rows
+                        _lib.call("bt_copy_rows", out.data_ptr(), e[3].data_ptr(), whole[i].ctypes.data, 1, bs * mx,
+                                  row_b, 1, _lib.stream_ptr())
+                    else:
+                        _lib.call("bt_copy_rows", out.data_ptr(), e[3].data_ptr(), lens[i].ctypes.data, bs, mx, row_b,
+                                  0, _lib.stream_ptr())
                     ev_out[i].record(d2h)
-            for (sq, _, out) in items:  # padded output rows are exact zeros (packing.py:158-159)
-                self._zero_padded_rows(out, sq, k)
+            for (sq, _, out), pd in zip(items, padded):  # padded output rows are exact zeros (packing.py:158-159)
+                if not pd:
+                    self._zero_padded_rows(out, sq, k)
             d2h.synchronize()
             cur.wait_stream(d2h)
             return [out for _, _, out in items]

@@ -279,3 +279,22 @@ def test_forward_stream_bitwise_and_vs_oracle(bt):
         assert not y.array[pad].any()
         want = orc.forward(ow, list(sq.lengths), x.array, ocfg)
         assert_close_bf16(y.array, want, max_abs_max=2e-2, what="forward_stream")
+
+
+def test_forward_stream_padded_copies(bt, monkeypatch):
+    """Large batches stream their padded buffers as one DMA each way (the
+    device forward writes the exact-zero padded rows): forced here by a low
+    threshold; outputs bitwise equal to forward()."""
+    from paper_2210_03052_b200 import encoder as enc
+
+    monkeypatch.setattr(enc, "STREAM_ROW_COPIES_MAX", 2)
+    mx, layers, bs = 96, 2, 5
+    cfg = bt.ModelConfig(layers=layers, head_num=12, head_size=64, max_seq_len=mx, batch_size=bs,
+                         flags=bt.OptFlags.all_on())
+    w = bt.init_weights(cfg, seed=4)
+    batches = []
+    for i, lens in enumerate([[96, 3, 50, 1, 70], [10, 96, 96, 2, 33], [96, 3, 50, 1, 70]]):
+        batches.append((bt.SeqLengths.of(lens, mx), bt.Tensor(orc.gen_input(lens, mx, 768, seed=20 + i))))
+    outs = bt.forward_stream(w, batches, cfg)
+    for (sq, x), y in zip(batches, outs):
+        assert np.array_equal(y.array, bt.forward(w, sq, x, cfg).array)
