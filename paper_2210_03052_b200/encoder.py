@@ -572,14 +572,16 @@ class BertEncoderB200:
                     else:
                         e[1]()
                     ev_done[i].record(comp)
+            # padded rows of the output are exact zeros (packing.py:158-159),
+            # written on the host while the GPU computes -- before the D2H
+            # enqueue, which can block the host once a large batch's per-sequence
+            # copies fill the DMA queue (disjoint rows: no ordering needed)
+            self._zero_padded_rows(out_pinned, seqs, k)
             for i, ((b0, b1), e) in enumerate(zip(bounds, entries)):
                 d2h.wait_event(ev_done[i])
                 with torch.cuda.stream(d2h):
                     _lib.call("bt_copy_rows", ob + b0 * mx * row_b, e[3].data_ptr(), lp + 4 * b0, b1 - b0, mx, row_b,
                               0, _lib.stream_ptr())
-            # padded rows of the output are exact zeros (packing.py:158-159),
-            # written on the host while the GPU works
-            self._zero_padded_rows(out_pinned, seqs, k)
             d2h.synchronize()
             torch.cuda.current_stream().wait_stream(d2h)
             return out_pinned
@@ -657,11 +659,11 @@ class BertEncoderB200:
                     graph.replay()
                 else:
                     run()
+            self._zero_padded_rows(out_pinned, seqs, k)  # while the GPU computes (see forward_host_packed)
             d2h.wait_stream(comp)
             with torch.cuda.stream(d2h):
                 _lib.call("bt_copy_rows", out_pinned.data_ptr(), yp.data_ptr(), lengths_h.ctypes.data, bs, mx, k * 4,
                           0, _lib.stream_ptr())
-            self._zero_padded_rows(out_pinned, seqs, k)
             d2h.synchronize()
             cur.wait_stream(d2h)
             return out_pinned
