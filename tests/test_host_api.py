@@ -159,3 +159,23 @@ def test_token_balanced_partition():
         assert imbalance(sh) < 1.01
     with pytest.raises(ValueError):
         token_balanced_partition([3, 4], 3)
+
+
+def test_host_io_chunk_bounds():
+    """Sequence ranges of the host-I/O pipeline (BertEncoderB200.chunk_bounds):
+    contiguous, non-empty, covering every sequence once, at most the asked
+    count, cut near the token-balanced targets."""
+    from paper_2210_03052_b200 import harness
+    from paper_2210_03052_b200.encoder import BertEncoderB200
+
+    lens = harness.gen_lengths(16, 256, "fixed", seed=0, alpha=0.6).lengths
+    for chunks in (1, 2, 3, 4, 16, 40, [0.3, 0.7], [0.2, 0.6, 0.2]):
+        b = BertEncoderB200.chunk_bounds(lens, chunks)
+        n = chunks if isinstance(chunks, int) else len(chunks)
+        assert 1 <= len(b) <= min(n, len(lens))
+        assert b[0][0] == 0 and b[-1][1] == len(lens)
+        assert all(b0 < b1 for b0, b1 in b) and all(b[i][1] == b[i + 1][0] for i in range(len(b) - 1))
+    two = BertEncoderB200.chunk_bounds(lens, 2)
+    first = sum(lens[two[0][0]:two[0][1]])
+    assert abs(first - sum(lens) / 2) <= max(lens)  # the boundary nearest the half-way token count
+    assert BertEncoderB200.chunk_bounds([7], 3) == [(0, 1)]
