@@ -173,12 +173,15 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
 // Epilogue math on 32 consecutive columns of one row, packed to 16 bf16x2.
 template <int EPI>
 __device__ __forceinline__ void epi_math32(float (&v)[32], const GemmParams& p, int row, int col, bool row_ok,
-                                           uint32_t* out16, const float4* bias) {
+                                           uint32_t* out16, const float4* bias, int lim = 32) {
+  // lim: columns of these 32 that exist (a tile narrower than its last
+  // 64-column chunk, or the matrix edge); residual loads stop there
   if constexpr (EPI == BT_EPI_BIAS_RESIDUAL) {
     if (row_ok) {
       const uint4* r = reinterpret_cast<const uint4*>(p.residual + static_cast<size_t>(row) * p.N + col);
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
+        if (8 * q >= lim) break;
         const uint4 rv = __ldg(r + q);
         const __nv_bfloat162* rh = reinterpret_cast<const __nv_bfloat162*>(&rv);
 #pragma unroll
@@ -488,6 +491,9 @@ __global__ void __launch_bounds__(GemmCfg<PAIR, BN, EW>::THREADS, 1)
           uint32_t r0[32], r1[32];
           const int col = nb * BN + c;
           if (col >= p.N) continue;  // partial last N tile (N % BN != 0): columns past N are never stored
+          // columns of this 64-wide chunk that exist: fewer when BN is not a
+          // multiple of 64 (last chunk of the tile) or at the matrix edge
+          const int w = min(64, min(BN - c, p.N - col));
           // bias for the 64 columns, loaded before the TMEM wait so its latency
           // overlaps the accumulator load instead of heading the math chain
           // (stream-K variants keep the in-chain loads: the hoisted registers
@@ -496,7 +502,7 @@ __global__ void __launch_bounds__(GemmCfg<PAIR, BN, EW>::THREADS, 1)
           if constexpr (EPI != BT_EPI_NONE && !STREAMK) {
             const float4* b4 = reinterpret_cast<const float4*>(p.bias + col);
 #pragma unroll
-            for (int q = 0; q < 16; ++q) bias4[q] = __ldg(b4 + q);
+            for (int q = 0; q < 16; ++q) bias4[q] = 4 * q < w ? __ldg(b4 + q) : make_float4(0.f, 0.f, 0.f, 0.f);
           }
           if (p.dbg != 7) {
             ptx::tmem_ld32(taddr + c, r0);
@@ -522,8 +528,20 @@ __global__ void __launch_bounds__(GemmCfg<PAIR, BN, EW>::THREADS, 1)
             add_partial32(v1, src + 8 * 32);
           }
           uint32_t pk[32];
-          epi_math32<EPI>(v0, p, row, col, row_ok, pk, STREAMK ? nullptr : bias4);
-          epi_math32<EPI>(v1, p, row, col + 32, row_ok, pk + 16, STREAMK ? nullptr : bias4 + 8);
+          epi_math32<EPI>(v0, p, row, col, row_ok, pk, STREAMK ? nullptr : bias4, w);
+          epi_math32<EPI>(v1, p, row, col + 32, row_ok, pk + 16, STREAMK ? nullptr : bias4 + 8, w - 32);
+          if (BN % 64 != 0 && w < 64) {
+            // narrow last chunk (BN % 64 != 0): this row's w columns go out as
+            // 16-byte stores straight from the registers (a 64-wide TMA box
+            // would overwrite the neighbouring tile)
+            if (row_ok) {
+              uint4* dst = reinterpret_cast<uint4*>(p.C + static_cast<size_t>(row) * p.N + col);
+#pragma unroll
+              for (int q = 0; q < 8; ++q)
+                if (8 * q < w) dst[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+            }
+            continue;
+          }
           if (p.dbg == 6) {  // debug: everything but the output store
             if (pk[0] == 0x12345678u && pk[31] == 0x9abcdef0u) p.C[row] = __float2bfloat16(0.f);
             continue;
@@ -665,7 +683,8 @@ static bool bn_ok(int N, int bn) {
 }
 static GemmChoice choose_tile(int M, int N, int K, int sms) {
   struct Cand { int pair, bn; };
-  const Cand cands[] = {{2, 256}, {2, 192}, {2, 128}, {1, 256}, {1, 192}, {1, 128}, {1, 64}};
+  const Cand cands[] = {{2, 256}, {2, 240}, {2, 224}, {2, 192}, {2, 176}, {2, 128}, {2, 112},
+                        {1, 256}, {1, 192}, {1, 128}, {1, 64}};
   GemmChoice best{1, 64, false};
   double best_cost = 1e300;
   const int nk = K / GEMM_BK;
@@ -692,7 +711,8 @@ static GemmChoice choose_tile(int M, int N, int K, int sms) {
     // summation order with the unit count, and the forward guarantees
     // results that do not depend on M (a shard equals its rows of the full
     // batch, bit for bit).
-    if (g_auto_streamk && N % c.bn == 0 && tiles % units != 0 && tiles <= 4 * units && units <= MAX_UNITS) {
+    if (g_auto_streamk && N % c.bn == 0 && c.bn % 64 == 0 && tiles % units != 0 && tiles <= 4 * units &&
+        units <= MAX_UNITS) {
       const long long work = tiles * nk;
       const double per_unit = static_cast<double>((work + units - 1) / units);
       const double fixup = 8000.0;  // measured: partial write + fence/flag + read costs ~4 us per split tile
@@ -712,15 +732,19 @@ static int g_force_streamk = -1;  // -1 auto, 0 off, 1 on (test hook)
 template <int PAIR, int BN, int EW>
 static int dispatch_sk(bool sk, int epi, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
                        const GemmParams& p, int units, cudaStream_t s) {
-  return sk ? dispatch_epi<PAIR, BN, EW, true>(epi, ta, tb, tc, p, units, s)
-            : dispatch_epi<PAIR, BN, EW, false>(epi, ta, tb, tc, p, units, s);
+  if constexpr (BN % 64 != 0) {  // round-robin only (gemm_run clears sk for these widths)
+    return dispatch_epi<PAIR, BN, EW, false>(epi, ta, tb, tc, p, units, s);
+  } else {
+    return sk ? dispatch_epi<PAIR, BN, EW, true>(epi, ta, tb, tc, p, units, s)
+              : dispatch_epi<PAIR, BN, EW, false>(epi, ta, tb, tc, p, units, s);
+  }
 }
 
 static int gemm_run(const void* A, const void* Bt, const float* bias, const void* residual, void* C, int M, int N,
                     int K, int epi, GemmChoice ch, cudaStream_t s) {
   const int sms = num_sms() > 0 ? num_sms() : 148;
   BT_REQUIRE(N % 64 == 0, BT_ESHAPE, "gemm: N=%d not a multiple of 64", N);
-  if (N % ch.bn) ch.streamk = false;  // stream-K partials assume whole tiles
+  if (N % ch.bn || ch.bn % 64) ch.streamk = false;  // stream-K partials assume whole 64-column chunks
   const int bm = 128 * ch.pair;
   CUtensorMap ta, tb, tc;
   BT_TRY(make_tmap_bf16_2d(&ta, A, M, K, K, 128, GEMM_BK));
@@ -753,8 +777,12 @@ static int gemm_run(const void* A, const void* Bt, const float* bias, const void
   }
   if (ch.pair == 2) {
     switch (ch.bn) {
+      case 112: return dispatch_sk<2, 112, 8>(ch.streamk, epi, ta, tb, tc, p, units, s);
       case 128: return dispatch_sk<2, 128, 8>(ch.streamk, epi, ta, tb, tc, p, units, s);
+      case 176: return dispatch_sk<2, 176, 8>(ch.streamk, epi, ta, tb, tc, p, units, s);
       case 192: return dispatch_sk<2, 192, 8>(ch.streamk, epi, ta, tb, tc, p, units, s);
+      case 224: return dispatch_sk<2, 224, 8>(ch.streamk, epi, ta, tb, tc, p, units, s);
+      case 240: return dispatch_sk<2, 240, 8>(ch.streamk, epi, ta, tb, tc, p, units, s);
       case 256: return dispatch_sk<2, 256, 8>(ch.streamk, epi, ta, tb, tc, p, units, s);
       default: BT_REQUIRE(false, BT_ECONFIG, "gemm: SM-pair tile width %d unsupported", ch.bn);
     }
@@ -818,7 +846,8 @@ static int autotune(const void* A, const void* Bt, const float* bias, const void
                     int K, int epi, cudaStream_t s, GemmChoice* best_out) {
   const int sms = num_sms() > 0 ? num_sms() : 148;
   struct Cand { int pair, bn; };
-  const Cand cands[] = {{2, 256}, {2, 192}, {2, 128}, {1, 256}, {1, 192}, {1, 128}, {1, 64}};
+  const Cand cands[] = {{2, 256}, {2, 240}, {2, 224}, {2, 192}, {2, 176}, {2, 128}, {2, 112},
+                        {1, 256}, {1, 192}, {1, 128}, {1, 64}};
   cudaEvent_t e0, e1;
   BT_CUDA_CHECK(cudaEventCreate(&e0));
   BT_CUDA_CHECK(cudaEventCreate(&e1));
@@ -830,7 +859,8 @@ static int autotune(const void* A, const void* Bt, const float* bias, const void
     const long long tiles = static_cast<long long>((M + bm - 1) / bm) * ((N + c.bn - 1) / c.bn);
     const long long units = sms / c.pair;
     for (int sk = 0; sk < 2; ++sk) {
-      if (sk && !(g_auto_streamk && N % c.bn == 0 && tiles % units != 0 && tiles <= 4 * units)) continue;
+      if (sk && !(g_auto_streamk && N % c.bn == 0 && c.bn % 64 == 0 && tiles % units != 0 && tiles <= 4 * units))
+        continue;
       const GemmChoice ch{c.pair, c.bn, sk != 0};
       BT_TRY(gemm_run(A, Bt, bias, residual, C, M, N, K, epi, ch, s));  // warm (module load, L2)
       // three rounds of 5 back-to-back launches, each queued behind a ~40 us
@@ -933,7 +963,10 @@ extern "C" int bt_debug_gemm_mode(int mode) {
 // Test hook: force a tile (+bn: one CTA 128 x bn; -bn: SM pair 256 x bn) so every instantiation is covered.
 extern "C" int bt_gemm_bn(const void* A, const void* Bt, const float* bias, const void* residual, void* C, int M,
                           int N, int K, int epilogue, int bn, bt_stream_t stream) {
-  BT_REQUIRE(bn == 64 || bn == 128 || bn == 192 || bn == 256 || bn == -128 || bn == -192 || bn == -256, BT_ECONFIG,
-             "bt_gemm_bn: bn must be 64/128/192/256 (one CTA) or -128/-192/-256 (SM pair), got %d", bn);
+  BT_REQUIRE(bn == 64 || bn == 128 || bn == 192 || bn == 256 || bn == -112 || bn == -128 || bn == -176 ||
+                 bn == -192 || bn == -224 || bn == -240 || bn == -256,
+             BT_ECONFIG,
+             "bt_gemm_bn: bn must be 64/128/192/256 (one CTA) or -112/-128/-176/-192/-224/-240/-256 (SM pair), got %d",
+             bn);
   return bt::gemm_launch(A, Bt, bias, residual, C, M, N, K, epilogue, bn, bt::as_stream(stream));
 }

@@ -17,7 +17,7 @@ SHAPES = {
     "c3": [(4915, 3072, 1024, 1), (4915, 1024, 1024, 0), (4915, 4096, 1024, 2), (4915, 1024, 4096, 0)],
     "big": [(78643, 3072, 1024, 1), (78643, 4096, 1024, 2), (78643, 1024, 4096, 0), (8192, 8192, 8192, 0)],
 }
-VARIANTS = [None, 64, 128, 192, 256, -128, -192, -256]
+VARIANTS = [None, 64, 128, 192, 256, -112, -128, -176, -192, -224, -240, -256]
 
 
 def main():

@@ -52,9 +52,7 @@ def test_gemm_tile_shape_invariance(env, M, N, K, epi):
     bias = torch.randn(N, device="cuda", generator=g) * 0.1
     res = torch.randn(M, N, device="cuda", generator=g).to(torch.bfloat16)
     outs = {}
-    for bn in (64, 128, 192, 256, -128, -192, -256):
-        if N % abs(bn):
-            continue
+    for bn in (64, 128, 192, 256, -112, -128, -176, -192, -224, -240, -256):  # incl. partial last N tiles
         outs[bn] = gemm_device(a, w, bias if epi else None, res if epi == 3 else None, epi, bn=bn)
     outs["auto"] = gemm_device(a, w, bias if epi else None, res if epi == 3 else None, epi)
     ref = outs[128]

@@ -35,7 +35,7 @@ def torch_tanh(t):
     return torch.tanh(t)
 
 
-@pytest.mark.parametrize("bn", [64, 128, 192, 256, -128, -192, -256])
+@pytest.mark.parametrize("bn", [64, 128, 192, 256, -112, -128, -176, -192, -224, -240, -256])
 @pytest.mark.parametrize("epi", [0, 1, 2, 3])
 @pytest.mark.parametrize("M,N,K", [(1, 768, 64), (200, 768, 768), (2458, 2304, 768), (129, 1024, 4096),
                                    (300, 3072, 128)])
