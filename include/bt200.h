@@ -301,6 +301,11 @@ BT_API int bt_encoder_forward_packed(const bt_layer_weights* layers, int n_layer
 BT_API int bt_copy_rows(void* dst, const void* src, const int32_t* lengths_host, int bs, int mx, long long row_bytes,
                         int to_packed, bt_stream_t stream);
 
+/* test hook: the four-CTAs-per-SM fused MHA (64-key blocks, P over S in TMEM)
+ * on (1) / off (0) for the packed launches outside the segment kernel; -1
+ * restores the BT_MHA64 policy (default on). */
+BT_API int bt_debug_mha64(int mode);
+
 /* page-locked host staging memory for pageable inputs (the reference's numpy
  * Tensor): write_combined = 1 allocates it write-combined, so the CPU's
  * staging stores bypass its caches and the following DMA reads at the PCIe

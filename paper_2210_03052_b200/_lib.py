@@ -92,6 +92,7 @@ SIGNATURES = {
     "bt_flops_enable": (_I, [_P]),
     "bt_flops_read": (_I, [_P]),
     "bt_host_alloc": (_I, [_SZ, _I, C.POINTER(C.c_void_p)]),
+    "bt_debug_mha64": (_I, [_I]),
     "bt_host_free": (_I, [_P]),
 }
 

@@ -30,12 +30,14 @@ def main():
         x = torch.randn(bs * mx, 64, device="cuda")
         pk = torch.empty(T, 64, device="cuda", dtype=torch.bfloat16)
         _lib.call("bt_pack_starts", x.data_ptr(), starts.data_ptr(), bs, mx, 64, pk.data_ptr(), _lib.stream_ptr())
-        for seg, lst, grid in ((0, 0, 0), (2, 0, 0), (0, 2, 0), (0, 2, 3)):
+        for m64, seg, lst, grid in ((1, 0, 0, 0), (0, 0, 0, 0), (0, 2, 0, 0), (0, 0, 2, 0), (0, 0, 2, 3)):
+            _lib.call("bt_debug_mha64", m64)  # the four-CTA kernel, then the two-CTA kernels' modes
             _lib.call("bt_debug_mha_seg", seg)
             _lib.call("bt_debug_mha_list", lst, grid)
             _lib.call("bt_mha_varlen_sched", qkv.data_ptr(), starts.data_ptr(), sched.data_ptr(), bs, mx, H, 64, 384,
                       out.data_ptr(), T, _lib.stream_ptr())
             torch.cuda.synchronize()
+        _lib.call("bt_debug_mha64", -1)
         _lib.call("bt_debug_mha_seg", -1)
         _lib.call("bt_debug_mha_list", -1, 0)
     print("sanitize run done")

@@ -183,6 +183,7 @@ def test_forward_mha_tile_list_bitwise():
     x = orc.gen_input(lens, 512, 768, seed=5)
     seqs = bt.SeqLengths.of(lens, 512)
     _lib.call("bt_debug_mha_list", 0, 0)
+    _lib.call("bt_debug_mha64", 0)  # the two-CTA kernels' modes (mha_sm100.cu)
     try:
         # a fresh weights object per mode: each gets its own engine, so the
         # forward's cached CUDA graph is captured under that mode
@@ -195,6 +196,7 @@ def test_forward_mha_tile_list_bitwise():
                 assert np.array_equal(out, ref), f"grid {grid}"
     finally:
         _lib.call("bt_debug_mha_list", -1, 0)
+        _lib.call("bt_debug_mha64", -1)
 
 
 @pytest.mark.parametrize("bs,mx,lens_kind", [(256, 256, "short"), (257, 64, "uniform"), (3, 257, "uniform"),

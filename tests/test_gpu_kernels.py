@@ -25,6 +25,18 @@ def env():
     return bt, torch
 
 
+@pytest.fixture
+def two_cta_mha(env):
+    """The two-CTAs-per-SM MHA kernels (mha_sm100.cu) for the packed launches
+    the four-CTA kernel (mha64_sm100.cu) serves by default: their scheduling
+    modes are pinned bitwise against each other and against the oracle."""
+    from paper_2210_03052_b200 import _lib
+
+    _lib.call("bt_debug_mha64", 0)
+    yield
+    _lib.call("bt_debug_mha64", -1)
+
+
 def _gelu(t):
     return 0.5 * t * (1.0 + torch_tanh(math.sqrt(2 / math.pi) * (t + 0.044715 * t ** 3)))
 
@@ -156,21 +168,29 @@ def _oracle_mha(qkv, plan, heads, mx, cutoff=384):
                             cutoff)
 
 
+@pytest.mark.parametrize("mha64", [1, 0])
 @pytest.mark.parametrize("path", [1, 2])
 @pytest.mark.parametrize("lens,mx", [([1, 2, 3, 127, 128, 129, 200, 256], 256), ([384, 1, 383, 257, 77], 384),
-                                     ([5] * 40, 8), ([128] * 6, 128)])
-def test_mha_paths_random(env, path, lens, mx):
-    """Both kernels on edge lengths (1, tile boundaries 127/128/129, 384)
-    with N(0,1) q/k/v (sharp softmax), vs the fp32 oracle."""
+                                     ([5] * 40, 8), ([128] * 6, 128), ([64, 63, 65, 1, 191, 193], 200)])
+def test_mha_paths_random(env, path, lens, mx, mha64):
+    """Every kernel on edge lengths (1, the 64- and 128-key block boundaries,
+    384) with N(0,1) q/k/v (sharp softmax), vs the fp32 oracle: the
+    four-CTA kernel (mha64 = 1, 64-key blocks) and the two-CTA resident
+    (path 1) / streamed (path 2) kernels."""
     bt, torch = env
+    from paper_2210_03052_b200 import _lib
     from paper_2210_03052_b200.attention import mha_device
 
     heads = 3
     plan = bt.plan_for_lengths(bt.SeqLengths.of(lens, mx))
     qkv = _rand_qkv(torch, plan.valid_word_cnt, heads * 64, seed=len(lens))
-    out = mha_device(qkv, plan, heads, 64, path=path)
+    _lib.call("bt_debug_mha64", mha64)
+    try:
+        out = mha_device(qkv, plan, heads, 64, path=path)
+    finally:
+        _lib.call("bt_debug_mha64", -1)
     ref = _oracle_mha(qkv, plan, heads, mx)
-    assert_close_bf16(out, ref, what=f"path{path} {lens[:4]}")
+    assert_close_bf16(out, ref, what=f"mha64={mha64} path{path} {lens[:4]}")
 
 
 @pytest.mark.parametrize("lens,mx", [([1000, 1, 513, 640, 129], 1024), ([512] * 3 + [300], 512)])
@@ -326,7 +346,7 @@ def test_mha_sched_order_is_result_neutral(env):
 @pytest.mark.parametrize("grid", [0, 1, 3, 7, 64])
 @pytest.mark.parametrize("lens,mx", [([5, 300, 129, 1, 512, 128, 257, 77], 512), ([256, 140, 9, 255, 1, 2], 256),
                                      ([1000, 3, 700, 129], 1024)])
-def test_mha_tile_list(env, lens, mx, grid):
+def test_mha_tile_list(env, two_cta_mha, lens, mx, grid):
     """The tile-list MHA (a fixed grid claims bt_plan_sched's query tiles x
     heads longest-first from a queue; what the forward runs for launches of
     many waves) is bitwise the one-tile-per-CTA kernel,
@@ -370,7 +390,7 @@ def test_mha_tile_list(env, lens, mx, grid):
 
 @pytest.mark.parametrize("lens,mx", [([512, 300, 129, 1, 450, 257], 512), ([256, 140, 9, 255], 256),
                                      ([1000, 3, 700], 1024)])
-def test_mha_query_tiles_per_cta(env, lens, mx):
+def test_mha_query_tiles_per_cta(env, two_cta_mha, lens, mx):
     """The multi-tile MHA variant (a CTA walks several query tiles of its
     sequence-head; chosen automatically for launches of many waves) is bitwise
     the single-tile kernel, which the other tests pin to the oracle."""

@@ -91,6 +91,12 @@ def test_forward_c5_slice_many_wave_vs_oracle(bt):
     xd = torch.from_numpy(x).cuda()
     outs = {}
     try:
+        # the default: the four-CTA MHA (mha64_sm100.cu), one tile per CTA
+        _, w = _weights(bt, ocfg, 1, "stress")
+        y64 = bt.forward(w, seqs, xd, cfg).cpu().numpy()
+        # the two-CTA kernels' many-wave modes (mha_sm100.cu), pinned bitwise
+        # against each other
+        _lib.call("bt_debug_mha64", 0)
         for name, (list_mode, grid, qg) in {"default": (-1, 0, 0), "tile_list": (2, 0, 0),
                                             "tile_list_small_grid": (2, 37, 0), "qg4": (0, 0, 4)}.items():
             _lib.call("bt_debug_mha_list", list_mode, grid)
@@ -100,9 +106,11 @@ def test_forward_c5_slice_many_wave_vs_oracle(bt):
     finally:
         _lib.call("bt_debug_mha_list", -1, 0)
         _lib.call("bt_debug_mha_qg", 0)
+        _lib.call("bt_debug_mha64", -1)
+    _check(bt, y64, want, lens, mx, "stress", "C5 slice, four-CTA MHA")
     _check(bt, outs["tile_list"], want, lens, mx, "stress", "C5 slice, tile list")
     for name, y in outs.items():
-        assert np.array_equal(y, outs["default"]), f"{name} differs from the default policy"
+        assert np.array_equal(y, outs["default"]), f"{name} differs from the two-CTA default policy"
 
 
 def test_pkbw_weights_forward_vs_oracle(bt, tmp_path):
