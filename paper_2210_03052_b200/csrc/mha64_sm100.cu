@@ -33,10 +33,16 @@ constexpr int M64_QT = 128;
 constexpr int M64_KB = 64;
 constexpr uint32_t M64_QTILE = 128 * 128;  // 128 rows x 64 bf16
 constexpr uint32_t M64_KVTILE = 64 * 128;  // 64 rows x 64 bf16
-constexpr int M64_NST = 2;
+#ifndef BT_M64_NST
+#define BT_M64_NST 2  // K/V ring depth (2: four CTAs fit an SM's shared memory)
+#endif
+#ifndef BT_M64_CTAS
+#define BT_M64_CTAS 4  // resident CTAs per SM the launch bounds target
+#endif
+constexpr int M64_NST = BT_M64_NST;
 constexpr int M64_THREADS = 256;
 constexpr int M64_REGS_ISSUE = 24;
-constexpr int M64_REGS_SOFTMAX = 104;  // 128 x 104 + 128 x 24 = 256 x 64
+constexpr int M64_REGS_SOFTMAX = BT_M64_CTAS == 4 ? 104 : 128;  // 128 x 104 + 128 x 24 = 256 x 64
 constexpr uint32_t M64_KV_OFF = M64_QTILE;
 constexpr uint32_t M64_BAR_OFF = M64_KV_OFF + M64_NST * 2 * M64_KVTILE;
 constexpr size_t M64_SMEM = M64_BAR_OFF + 256;
@@ -63,7 +69,7 @@ __device__ __forceinline__ void m64_tie(uint32_t (&r)[32]) {
                  "+r"(r[29]), "+r"(r[30]), "+r"(r[31]));
 }
 
-__global__ void __launch_bounds__(M64_THREADS, 4)
+__global__ void __launch_bounds__(M64_THREADS, BT_M64_CTAS)
     mha64_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKV,
                      const Mha64Params p) {
   extern __shared__ __align__(1024) uint8_t smem[];
