@@ -9,8 +9,8 @@
 //     softmax holds S in registers, so four CTAs fit the 512 columns.
 //   * thread = query row (warps 0-3, TMEM lane = thread): row max and row
 //     sum are thread-local, no shuffles, 64 S values per thread.
-//   * the MMA warp issues S(j+1) only after P(j) V(j) has consumed P(j)
-//     (they share columns); the four interleaved CTAs keep the SFU busy
+//   * the MMA warp issues S(j+1) right behind P(j) V(j) (they share
+//     columns; MMAs of one thread execute in order); the four CTAs keep the SFU busy
 //     while a CTA waits for its MMAs -- the two-CTA kernel's chain is gated
 //     by two all-thread barriers per 128-key block with only two chains per SM.
 //   * O is rescaled (rarely) after block j's exponentials, before P(j) is
@@ -83,7 +83,6 @@ __global__ void __launch_bounds__(M64_THREADS, BT_M64_CTAS)
   uint64_t* v_empty = k_empty + M64_NST;
   uint64_t* s_full = v_empty + M64_NST;  // S(j) in TMEM (and every earlier MMA done)
   uint64_t* p_full = s_full + 1;         // P(j) written over S by all 128 softmax threads
-  uint64_t* pv_done = s_full + 2;        // P(j) V(j) done: S columns free for S(j+1)
   uint64_t* o_full = s_full + 3;         // the tile's last P V done
   uint32_t* holder = reinterpret_cast<uint32_t*>(o_full + 1);
 
@@ -102,7 +101,6 @@ __global__ void __launch_bounds__(M64_THREADS, BT_M64_CTAS)
     }
     ptx::mbar_init(s_full, 1);
     ptx::mbar_init(p_full, 128);
-    ptx::mbar_init(pv_done, 1);
     ptx::mbar_init(o_full, 1);
     ptx::fence_mbar_init();
   }
@@ -191,14 +189,13 @@ __global__ void __launch_bounds__(M64_THREADS, BT_M64_CTAS)
             ptx::mma_bf16_ts(tmem + O_COL, tmem + S_COL + 8 * ks, v_desc + ks * ((16 * 128) >> 4), idesc_o,
                              (j > 0 || ks > 0) ? 1u : 0u);
           ptx::mma_commit(&v_empty[slot]);
-          ptx::mma_commit(j + 1 < nkb ? pv_done : o_full);
+          if (j + 1 == nkb) ptx::mma_commit(o_full);
         }
         __syncwarp();
-        if (j + 1 < nkb) {
-          ptx::mbar_wait(pv_done, static_cast<uint32_t>(j & 1));  // P(j) read: its columns may take S(j+1)
-          ptx::tc_fence_after();
-          issue_s(j + 1);
-        }
+        // S(j+1) overwrites the columns P(j) V(j) reads P(j) from: issued
+        // right behind it -- tcgen05.mma ops of one thread execute in issue
+        // order (CUTLASS's Blackwell FMHA aliases P into S the same way)
+        if (j + 1 < nkb) issue_s(j + 1);
       }
     }
   } else {
