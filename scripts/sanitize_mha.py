@@ -17,7 +17,10 @@ def main():
 
     _lib.require_device()
     L = _lib.load()
-    for lens, mx, H in (([5, 300, 129, 1, 200, 128, 77], 512, 2), ([1, 2, 3, 127, 128, 129, 200, 256, 30, 40], 256, 2)):
+    # the third batch has enough query tiles x heads (> 16 x SMs) for the
+    # four-CTA MHA's persistent mode
+    for lens, mx, H in (([5, 300, 129, 1, 200, 128, 77], 512, 2), ([1, 2, 3, 127, 128, 129, 200, 256, 30, 40], 256, 2),
+                        ([512, 511, 385, 200, 64, 1] * 7, 512, 16)):
         bs = len(lens)
         plan = bt.plan_for_lengths(bt.SeqLengths.of(lens, mx))
         T = plan.valid_word_cnt
