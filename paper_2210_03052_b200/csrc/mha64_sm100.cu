@@ -273,11 +273,9 @@ __global__ void __launch_bounds__(M64_THREADS, BT_M64_CTAS)
     int g = 0;  // blocks consumed across tiles
     for (int t = 0; t < max_tiles; ++t) {
       int len, rows_here;
-      {
-        const M64Tile tl = tile_at(t);  // (s0, h re-read at the store: fewer live registers)
-        len = tl.len;
-        rows_here = tl.len - tl.q0;
-      }
+      M64Tile tl0 = tile_at(t);  // (persistent: s0, h re-read at the store -- fewer live registers)
+      len = tl0.len;
+      rows_here = tl0.len - tl0.q0;
       if (len == 0) break;
       const int nkb = (len + M64_KB - 1) / M64_KB;
       const bool warp_live = warp * 32 < rows_here;
@@ -387,7 +385,7 @@ __global__ void __launch_bounds__(M64_THREADS, BT_M64_CTAS)
         ptx::tmem_wait_ld(o0);
         m64_tie(o1);
         if (row < rows_here) {
-          const M64Tile tl = tile_at(t);
+          const M64Tile tl = PERSIST ? tile_at(t) : tl0;
           const float inv = 1.0f / lsum;
           const unsigned long long inv2 = ptx::f2(inv, inv);
           uint4* dst =
