@@ -701,7 +701,8 @@ static int mha_qtiles_per_cta(int nqt, bool many_waves) {
 // grid size (tests: many claims per CTA on a small batch).
 static int g_mha_list_mode = -1, g_mha_list_grid = 0, g_mha_seg_mode = -1;
 // Segment-kernel policy (batches of bs <= 256, max_seq_len <= 256):
-// BT_MHA_SEG=0 disables it; bt_debug_mha_seg overrides (0 off, 1 / 2 on).
+// BT_MHA_SEG=0 disables it, 2 forces it in its domain; bt_debug_mha_seg
+// overrides (0 off, 1 by size, 2 forced).
 static int mha_seg_mode() {
   if (g_mha_seg_mode >= 0) return g_mha_seg_mode;
   static int env = -1;
@@ -775,9 +776,17 @@ int mha_launch(const void* qkv, const int32_t* seq_starts, int bs, int mx, int H
   // Few waves (C2, C3) keep one tile per CTA: there the multi-tile kernel's
   // longer per-tile chain (its issuer warps spill at 32 registers) costs more
   // than the balance gains (C2 13.9 vs 10.7 us, C3 26.6 vs 26.1 us).
-  // Segment kernel (short batches): adjacent short sequences share a CTA
+  // Segment kernel (short batches): adjacent short sequences share a CTA.
+  // Mode 1 keeps it where it measured faster than the four-CTA kernel: launches
+  // of about one wave (C2 16 x 256: 8.1 vs 12.0 us in the graph) and
+  // max_seq_len <= 64, where it packs several sequences per query tile
+  // (64 x 64: 8.4 vs 9.1 us); beyond that the four-CTA kernel wins (32 x 256:
+  // 13.7 vs 15.6, 256 x 256: 71.5 vs 106.8, 256 x 128: 35.5 vs 48.6 us;
+  // scripts/mha_time.py).  Mode 2 forces it inside its domain.
   const int seg_mode = mha_seg_mode();
-  if (p.sched && seg_mode > 0 && bs <= SEG_MAX_BS && mx <= SEG_MAX_MX) {
+  const bool m64 = !padded && mha64_enabled();
+  const bool seg_small = !m64 || mx <= 64 || ctas1 <= 3LL * sms;
+  if (p.sched && bs <= SEG_MAX_BS && mx <= SEG_MAX_MX && (seg_mode == 2 || (seg_mode == 1 && seg_small))) {
     p.nsegs = reinterpret_cast<const int*>(static_cast<const uint8_t*>(sched) + sched_segs_offset(bs, mx));
     p.segs = reinterpret_cast<const int4*>(p.nsegs + 4);
     static bool set = false;
@@ -792,7 +801,7 @@ int mha_launch(const void* qkv, const int32_t* seq_starts, int bs, int mx, int H
   // the four-CTAs-per-SM kernel (mha64_sm100.cu) for every other packed
   // launch: measured faster than both the one-tile and the tile-list modes
   // below (C3 24.5 -> 21.9 us, C5 2.84-2.96 -> 2.45-2.55 ms per launch)
-  if (!padded && mha64_enabled()) return mha64_launch(qkv, seq_starts, p.sched, bs, mx, H, T, out, s);
+  if (m64) return mha64_launch(qkv, seq_starts, p.sched, bs, mx, H, T, out, s);
   const int list_mode = mha_list_mode();
   if (p.sched && list_mode > 0) {
     static int slots = 0;

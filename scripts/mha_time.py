@@ -2,7 +2,7 @@
 forward's schedule), back-to-back launches timed with CUDA events.
 BT_LIB_PATH selects a library variant (A/B).
 
-    python scripts/mha_time.py [c2 c3 c5]
+    python scripts/mha_time.py [c2 c3 c5 | bs:mx:heads ...]
 """
 import sys
 from pathlib import Path
@@ -18,7 +18,8 @@ def main():
 
     _lib.require_device()
     for cfg in sys.argv[1:] or ["c2", "c3", "c5"]:
-        bs, mx, H = {"c2": (16, 256, 12), "c3": (16, 512, 16), "c5": (2048, 512, 16)}[cfg]
+        known = {"c2": (16, 256, 12), "c3": (16, 512, 16), "c5": (2048, 512, 16)}
+        bs, mx, H = known[cfg] if cfg in known else tuple(int(v) for v in cfg.split(":"))  # or "bs:mx:heads"
         seqs = harness.gen_lengths(bs, mx, "fixed", seed=0, alpha=0.6)
         plan = plan_for_lengths(seqs)
         T = plan.valid_word_cnt
