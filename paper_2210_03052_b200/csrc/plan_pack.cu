@@ -381,35 +381,74 @@ __device__ __forceinline__ void plan_sched_body(const int32_t* __restrict__ seq_
   // MHA segments (short batches): the query tiles of sequences longer than
   // 128 rows, then groups of adjacent sequences of <= 128 rows whose rows
   // fit one 128-row tile together (one key block; each row masked to its own
-  // sequence).  One thread, over seq_starts staged in shared memory.
+  // sequence), greedily from the left of each run of short sequences.  In
+  // parallel over the sequences (a serial walk by one thread cost ~3 us at
+  // bs = 16): each short sequence i finds where a group starting at i would
+  // end (gend), each run start walks its chain of group starts, and two warp
+  // scans place the long tiles and the groups -- the same list, in the same
+  // order, as the serial greedy.
   if (segs != nullptr) {
     __shared__ int ss[SEG_MAX_BS + 1];
+    __shared__ int gend[SEG_MAX_BS];
+    __shared__ int ntile[SEG_MAX_BS];   // long: its query tiles; then exclusive offsets
+    __shared__ int gstart[SEG_MAX_BS];  // 1 if a group starts at i; then exclusive offsets
+    __shared__ int tot[2];
     for (int i = threadIdx.x; i <= bs; i += blockDim.x) ss[i] = seq_starts[i];
     __syncthreads();
-    if (threadIdx.x == 0) {
-      int n = 0;
-      for (int i = 0; i < bs; ++i) {
-        const int st = ss[i], en = ss[i + 1];
-        if (en - st <= 128) continue;
-        for (int q = st; q < en; q += 128) {
+    for (int i = threadIdx.x; i < bs; i += blockDim.x) {
+      const int len = ss[i + 1] - ss[i];
+      ntile[i] = len > 128 ? (len + 127) / 128 : 0;
+      gstart[i] = 0;
+      int j = i;
+      if (len <= 128)
+        while (j < bs && ss[j + 1] - ss[j] <= 128 && ss[j + 1] - ss[i] <= 128) ++j;
+      gend[i] = j;  // the group [i, j) if one starts at i
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < bs; i += blockDim.x) {
+      const bool shortseq = ss[i + 1] - ss[i] <= 128;
+      if (shortseq && (i == 0 || ss[i] - ss[i - 1] > 128))
+        for (int j = i; j < bs && ss[j + 1] - ss[j] <= 128; j = gend[j]) gstart[j] = 1;
+    }
+    __syncthreads();
+    if (threadIdx.x < 64) {  // warp 0 scans ntile, warp 1 gstart (<= 8 entries per lane)
+      int* a = threadIdx.x < 32 ? ntile : gstart;
+      const int lane = threadIdx.x & 31, per = (bs + 31) / 32, b0 = min(bs, lane * per), b1 = min(bs, b0 + per);
+      int run = 0;
+      for (int i = b0; i < b1; ++i) run += a[i];
+      int x = run;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      int off = x - run;
+      for (int i = b0; i < b1; ++i) {
+        const int v = a[i];
+        a[i] = off;
+        off += v;
+      }
+      if (lane == 31) tot[threadIdx.x >> 5] = x;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < bs; i += blockDim.x) {
+      const int st = ss[i], en = ss[i + 1];
+      if (en - st > 128) {
+        int n = ntile[i];
+        for (int q = st; q < en; q += 128, ++n) {
           segs[2 * n] = make_int4(st, en, q, min(en, q + 128));
           segs[2 * n + 1] = make_int4(i, i, 0, 0);
-          ++n;
+        }
+      } else {
+        const bool starts = (i + 1 < bs ? gstart[i + 1] : tot[1]) != gstart[i];
+        if (starts) {
+          const int n = tot[0] + gstart[i], e = gend[i];
+          segs[2 * n] = make_int4(st, ss[e], st, ss[e]);
+          segs[2 * n + 1] = make_int4(i, e - 1, 0, 0);
         }
       }
-      int g0 = -1;
-      for (int i = 0; i <= bs; ++i) {
-        const bool shortseq = i < bs && ss[i + 1] - ss[i] <= 128;
-        if (g0 >= 0 && (!shortseq || ss[i + 1] - ss[g0] > 128)) {  // close the open group [g0, i)
-          segs[2 * n] = make_int4(ss[g0], ss[i], ss[g0], ss[i]);
-          segs[2 * n + 1] = make_int4(g0, i - 1, 0, 0);
-          ++n;
-          g0 = -1;
-        }
-        if (shortseq && g0 < 0) g0 = i;
-      }
-      *nsegs = n;
     }
+    if (threadIdx.x == 0) *nsegs = tot[0] + tot[1];
   }
 }
 

@@ -144,3 +144,81 @@ def test_forward_plan_and_pack_starts(bt, bs, mx):
               _lib.stream_ptr())
     torch.cuda.synchronize()
     assert torch.equal(out, pack_device(x, plan, out_dtype=torch.bfloat16))
+
+
+def _segs_serial(lens):
+    """The MHA segment list (plan_pack.cu plan_sched_body) as the serial greedy:
+    long sequences' 128-row query tiles in order, then per run of adjacent
+    sequences of <= 128 rows, groups closed when the next would pass 128 rows."""
+    ss = np.concatenate([[0], np.cumsum(lens)]).astype(int)
+    bs, out = len(lens), []
+    for i in range(bs):
+        st, en = ss[i], ss[i + 1]
+        if en - st > 128:
+            for q in range(st, en, 128):
+                out.append((st, en, q, min(en, q + 128), i, i, 0, 0))
+    g0 = -1
+    for i in range(bs + 1):
+        short = i < bs and ss[i + 1] - ss[i] <= 128
+        if g0 >= 0 and (not short or ss[i + 1] - ss[g0] > 128):
+            out.append((ss[g0], ss[i], ss[g0], ss[i], g0, i - 1, 0, 0))
+            g0 = -1
+        if short and g0 < 0:
+            g0 = i
+    return out
+
+
+@pytest.mark.parametrize("case", ["mixed16", "all_short", "all_long", "edges", "bs256", "one", "mx64"])
+def test_mha_segment_list(bt, case):
+    """The parallel segment builder writes the serial greedy's list exactly,
+    through all three launches that plan (bt_plan_sched, bt_plan_forward,
+    bt_forward_prologue)."""
+    import torch
+
+    from paper_2210_03052_b200 import _lib
+
+    rng = np.random.default_rng(len(case))
+    lens, mx = {
+        "mixed16": (orc.gen_lengths(16, 256, "fixed", seed=0, alpha=0.6), 256),
+        "all_short": (rng.integers(1, 129, 40), 128),
+        "all_long": (rng.integers(129, 257, 12), 256),
+        "edges": (np.array([128, 1, 127, 129, 64, 64, 1, 128, 256, 65, 63, 1, 1, 200, 128]), 256),
+        "bs256": (rng.integers(1, 257, 256), 256),
+        "one": (np.array([77]), 128),
+        "mx64": (rng.integers(1, 65, 64), 64),
+    }[case]
+    lens = [int(v) for v in lens]
+    bs, k = len(lens), 64
+    want = _segs_serial(lens)
+    L = _lib.load()
+    nb = L.bt_plan_sched_bytes(bs, mx) // 4
+    nbk = (mx + 127) // 128
+    units_off = (bs * 8 + 15) // 16 * 16
+    segs_off = (units_off + 16 + (bs * nbk * 8 + 15) // 16 * 16) // 4
+    lengths_dev = torch.tensor(lens, dtype=torch.int32, device="cuda")
+    starts = torch.tensor(np.concatenate([[0], np.cumsum(lens)]), dtype=torch.int32, device="cuda")
+    T = int(sum(lens))
+    x = torch.randn(bs * mx, k, device="cuda")
+    xp = torch.empty(T, k, dtype=torch.bfloat16, device="cuda")
+    upad = torch.empty(bs * mx, k, device="cuda")
+    row_map = torch.empty(T, dtype=torch.int32, device="cuda")
+    st2 = torch.empty_like(starts)
+    runs = {
+        "plan_sched": lambda sc: _lib.call("bt_plan_sched", starts.data_ptr(), bs, mx, sc.data_ptr(),
+                                           _lib.stream_ptr()),
+        "plan_forward": lambda sc: _lib.call("bt_plan_forward", lengths_dev.data_ptr(), bs, mx, st2.data_ptr(),
+                                             sc.data_ptr(), _lib.stream_ptr()),
+        "prologue": lambda sc: _lib.call("bt_forward_prologue", lengths_dev.data_ptr(), bs, mx, k, x.data_ptr(), None,
+                                         xp.data_ptr(), st2.data_ptr(), sc.data_ptr(), upad.data_ptr(),
+                                         row_map.data_ptr(), T, _lib.stream_ptr()),
+    }
+    for name, run in runs.items():
+        sched = torch.full((nb,), -7, dtype=torch.int32, device="cuda")
+        run(sched)
+        torch.cuda.synchronize()
+        h = sched.cpu().numpy()
+        n = int(h[segs_off])
+        got = [tuple(int(v) for v in h[segs_off + 4 + 8 * i: segs_off + 12 + 8 * i]) for i in range(n)]
+        assert n == len(want), (name, n, len(want))
+        # the second int4's last two words are padding (not written)
+        assert [g[:6] for g in got] == [w[:6] for w in want], name
