@@ -201,11 +201,16 @@ def test_forward_mha_tile_list_bitwise():
 
 @pytest.mark.parametrize("bs,mx,lens_kind", [(256, 256, "short"), (257, 64, "uniform"), (3, 257, "uniform"),
                                               (200, 8, "ones"), (40, 256, "mixed")])
-def test_forward_schedule_boundaries_vs_oracle(bt, bs, mx, lens_kind):
+@pytest.mark.parametrize("seg", [-1, 2])
+def test_forward_schedule_boundaries_vs_oracle(bt, bs, mx, lens_kind, seg):
     """Forward vs the fp32 oracle at the MHA scheduling boundaries: the
     segment kernel's limits (bs 256 / 257, max_seq_len 256 / 257), hundreds of
     one-token sequences in one segment, and runs of short sequences between
-    long ones (1 layer, 2 heads, so the oracle stays fast)."""
+    long ones (1 layer, 2 heads, so the oracle stays fast).  seg = -1: the
+    size policy (larger launches inside the segment domain take the four-CTA
+    kernel); 2: the segment kernel forced wherever its domain allows."""
+    from paper_2210_03052_b200 import _lib
+
     rng = np.random.default_rng(bs * 1000 + mx)
     if lens_kind == "ones":
         lens = [1] * bs
@@ -220,8 +225,12 @@ def test_forward_schedule_boundaries_vs_oracle(bt, bs, mx, lens_kind):
     ocfg = orc.OracleConfig(1, 2, 64, mx, bs)
     x = orc.gen_input(lens, mx, 128, 3)
     want = orc.forward(orc.init_weights(ocfg, 3), lens, x, ocfg)
-    y = bt.forward(bt.init_weights(cfg, 3), bt.SeqLengths.of(lens, mx), bt.Tensor(x), cfg)
-    assert_close_bf16(y, want, max_abs_max=2e-2, what=f"bs{bs} mx{mx} {lens_kind}")
+    _lib.call("bt_debug_mha_seg", seg)
+    try:
+        y = bt.forward(bt.init_weights(cfg, 3), bt.SeqLengths.of(lens, mx), bt.Tensor(x), cfg)
+    finally:
+        _lib.call("bt_debug_mha_seg", -1)
+    assert_close_bf16(y, want, max_abs_max=2e-2, what=f"bs{bs} mx{mx} {lens_kind} seg{seg}")
     valid = orc.build_mask(lens, mx).reshape(-1).astype(bool)
     assert not np.asarray(y.array)[~valid].any()
 
