@@ -1,5 +1,5 @@
-"""One small launch of every MHA scheduling mode, the forward plan and the
-seq_starts pack, for compute-sanitizer runs:
+"""One small launch of every MHA scheduling mode, the forward plan, the
+seq_starts pack and the one-launch prologue, for compute-sanitizer runs:
 
     compute-sanitizer --tool memcheck python scripts/sanitize_mha.py
 """
@@ -33,6 +33,12 @@ def main():
         x = torch.randn(bs * mx, 64, device="cuda")
         pk = torch.empty(T, 64, device="cuda", dtype=torch.bfloat16)
         _lib.call("bt_pack_starts", x.data_ptr(), starts.data_ptr(), bs, mx, 64, pk.data_ptr(), _lib.stream_ptr())
+        # the one-launch prologue (plan + segment list + pack + zero rows)
+        upad = torch.empty(bs * mx, 64, device="cuda")
+        row_map = torch.empty(T, dtype=torch.int32, device="cuda")
+        sched2 = torch.zeros_like(sched)
+        _lib.call("bt_forward_prologue", lengths.data_ptr(), bs, mx, 64, x.data_ptr(), None, pk.data_ptr(),
+                  starts.data_ptr(), sched2.data_ptr(), upad.data_ptr(), row_map.data_ptr(), T, _lib.stream_ptr())
         for m64, seg, lst, grid in ((1, 0, 0, 0), (0, 0, 0, 0), (0, 2, 0, 0), (0, 0, 2, 0), (0, 0, 2, 3)):
             _lib.call("bt_debug_mha64", m64)  # the four-CTA kernel, then the two-CTA kernels' modes
             _lib.call("bt_debug_mha_seg", seg)
