@@ -76,6 +76,31 @@ struct Mha64Params {
   unsigned long long* flops;
 };
 
+// Debug trace (a -DBT_TRACE_ON build, buffer installed by bt_debug_mha_trace;
+// grid mode, the CTA's tile): 32 u64 globaltimer stamps per CTA, index =
+// linear block id.  [0] set-up done  [1] Q landed (MMA warp)  block j < 7:
+// [2+2j] S(j) seen by the softmax  [3+2j] P(j) released  [16+j] P(j) seen by
+// the MMA warp (P V(j) issued)  [30] O seen  [31] output stored.
+__device__ unsigned long long* g_m64_trace = nullptr;
+#ifdef BT_TRACE_ON
+#define M64_TRACE(slot)                                                                                  \
+  do {                                                                                                   \
+    if (g_m64_trace) {                                                                                   \
+      unsigned long long _t;                                                                             \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));                                             \
+      g_m64_trace[((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 32 + (slot)] = _t;  \
+    }                                                                                                    \
+  } while (0)
+#else
+#define M64_TRACE(slot) \
+  do {                  \
+  } while (0)
+#endif
+int mha64_set_trace(unsigned long long* buf) {
+  BT_CUDA_CHECK(cudaMemcpyToSymbol(g_m64_trace, &buf, sizeof(buf)));
+  return BT_OK;
+}
+
 struct M64Tile {
   int s0, len, q0, h;  // keys [s0, s0 + len); query rows s0 + q0 .. ; len 0: no tile
 };
@@ -140,6 +165,7 @@ __global__ void __launch_bounds__(M64_THREADS, BT_M64_CTAS)
   const uint32_t tmem = *holder;
   ptx::griddep_launch_dependents();
   ptx::griddep_wait();  // the schedule and qkv come from earlier kernels
+  if (!PERSIST && threadIdx.x == 0) M64_TRACE(0);
   constexpr bool persistent = PERSIST;
   const int nitems = persistent ? __ldg(p.nunits) * p.heads : 1;
   constexpr int max_tiles = PERSIST ? 0x7FFFFFFF : 1;
@@ -235,11 +261,13 @@ __global__ void __launch_bounds__(M64_THREADS, BT_M64_CTAS)
         if (tl.len == 0) break;
         const int nkb = (tl.len + M64_KB - 1) / M64_KB;
         ptx::mbar_wait(q_full, static_cast<uint32_t>(t & 1));
+        if (!PERSIST && lane == 0) M64_TRACE(1);
         const int kv0 = kvg;
         issue_s(nkb == 1);
         for (int j = 0; j < nkb; ++j, ++g) {
           const int slot = (kv0 + j) % M64_NST;
           ptx::mbar_wait(p_full, static_cast<uint32_t>(g & 1));
+          if (!PERSIST && lane == 0 && j < 7) M64_TRACE(16 + j);
           if (PERSIST && j == 0 && t > 0)
             ptx::mbar_wait(o_free, static_cast<uint32_t>((t - 1) & 1));  // O of tile t-1 read
           ptx::mbar_wait(&v_full[slot], static_cast<uint32_t>(((kv0 + j) / M64_NST) & 1));
@@ -284,6 +312,7 @@ __global__ void __launch_bounds__(M64_THREADS, BT_M64_CTAS)
         const int kblk = min(M64_KB, len - j * M64_KB);
         ptx::mbar_wait(s_full, static_cast<uint32_t>(g & 1));
         ptx::tc_fence_after();
+        if (!PERSIST && threadIdx.x == 0 && j < 7) M64_TRACE(2 + 2 * j);
         uint32_t r0[32], r1[32];
         if (warp_live) {
           ptx::tmem_ld32(trow + S_COL, r0);
@@ -374,10 +403,12 @@ __global__ void __launch_bounds__(M64_THREADS, BT_M64_CTAS)
         }
         ptx::tc_fence_before();
         ptx::mbar_arrive(p_full);
+        if (!PERSIST && threadIdx.x == 0 && j < 7) M64_TRACE(3 + 2 * j);
       }
       // ---- the tile's output: O / l -> bf16, each thread stores its row
       ptx::mbar_wait(o_full, static_cast<uint32_t>(t & 1));
       ptx::tc_fence_after();
+      if (!PERSIST && threadIdx.x == 0) M64_TRACE(30);
       if (warp_live) {
         uint32_t o0[32], o1[32];
         ptx::tmem_ld32(trow + O_COL, o0);
@@ -404,6 +435,7 @@ __global__ void __launch_bounds__(M64_THREADS, BT_M64_CTAS)
             dst[c] = make_uint4(w[0], w[1], w[2], w[3]);
           }
         }
+        if (!PERSIST && threadIdx.x == 0) M64_TRACE(31);
         if (p.flops != nullptr) {
           const unsigned keys = row < rows_here ? static_cast<unsigned>(len) : 0u;
           const unsigned wsum = __reduce_add_sync(0xffffffffu, keys);

@@ -727,6 +727,7 @@ static int mha_list_mode() {
 unsigned long long* g_mha_flops = nullptr;
 
 bool mha64_enabled();
+int mha64_set_trace(unsigned long long* buf);
 int mha64_launch(const void* qkv, const int32_t* seq_starts, const void* sched, int bs, int mx, int H, int T,
                  void* out, cudaStream_t s);
 
@@ -891,7 +892,7 @@ extern "C" int bt_debug_mha_seg(int mode) {
 
 extern "C" int bt_debug_mha_trace(unsigned long long* buf) {
   BT_CUDA_CHECK(cudaMemcpyToSymbol(bt::g_mha_trace, &buf, sizeof(buf)));
-  return BT_OK;
+  return bt::mha64_set_trace(buf);  // the four-CTA kernel's trace points (mha64_sm100.cu)
 }
 
 extern "C" int bt_mha_varlen(const void* qkv, const int32_t* seq_starts, int bs, int mx, int H, int d, int cutoff,
