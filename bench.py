@@ -285,6 +285,7 @@ def time_kernels(torch, bt, eng, shard_seqs, x_dev, reps: int = 30):
     lf = harness.layer_flops(shard_seqs.lengths, k, cfg.ffn_scale)
 
     fused_ln0 = bool(_lib.load().bt_fused_attn_out_ln(T, k))  # what the forward runs for this shape
+    fused_ffn2 = bool(_lib.load().bt_fused_ffn2_ln(T, k, f))
     sched = torch.empty(_lib.load().bt_plan_sched_bytes(bs, mx) // 4 + 1, dtype=torch.int32, device="cuda")
     _lib.call("bt_plan_sched", plan.seq_starts_dev.data_ptr(), bs, mx, sched.data_ptr(), _lib.stream_ptr())
     sched2 = torch.empty_like(sched)  # scratch schedule for timing bt_plan_forward
@@ -335,12 +336,25 @@ def time_kernels(torch, bt, eng, shard_seqs, x_dev, reps: int = 30):
                             harness.kernel_bytes("prologue", T, k, bs, mx), 1), **ops}
         ln1 = ops.pop("ln1")
         ops["ln1"] = (ln1[0], cfg.layers - 1) + ln1[2:]
+        if fused_ffn2:
+            # every layer but the last runs FFN2 + bias + residual + LN1 as one kernel
+            ops.pop("ln1")
+            ffn2 = ops.pop("gemm_ffn2")
+            ops["gemm_ffn2_ln"] = (lambda: gemm_ln_device(h1, L0.w2, L0.b2, y0, L0.ln1_g, L0.ln1_b, 1e-12, out=out),
+                                   cfg.layers - 1, "tensor", lf["gemm3"], 1)
+            ops["gemm_ffn2"] = (ffn2[0], 1) + ffn2[2:]
         ops["ln1_out"] = (lambda: _lib.call("bt_ln_bias_residual_out", h2.data_ptr(), y0.data_ptr(), L0.b2.data_ptr(),
                                             L0.ln1_g.data_ptr(), L0.ln1_b.data_ptr(), C.c_float(1e-12),
                                             upad.data_ptr(), row_map.data_ptr(), T, k, _lib.stream_ptr()),
                           1, "hbm", harness.kernel_bytes("ln_out", T, k), 1)
         if cfg.layers == 1:
-            ops.pop("ln1")
+            ops.pop("ln1", None)
+            ops.pop("gemm_ffn2_ln", None)
+    elif fused_ffn2:
+        ops.pop("ln1")
+        ops.pop("gemm_ffn2")
+        ops["gemm_ffn2_ln"] = (lambda: gemm_ln_device(h1, L0.w2, L0.b2, y0, L0.ln1_g, L0.ln1_b, 1e-12, out=out),
+                               cfg.layers, "tensor", lf["gemm3"], 1)
     res = {}
     s = torch.cuda.current_stream()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")

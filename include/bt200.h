@@ -167,6 +167,10 @@ BT_API int bt_mha_varlen_sched(const void* qkv, const int32_t* seq_starts, const
 /* 1 if bt_encoder_layer / bt_encoder_forward use bt_gemm_bias_residual_ln after the attention-output
  * projection for T tokens of hidden size k (else GEMM + bt_ln_bias_residual). */
 BT_API int bt_fused_attn_out_ln(int T, int k);
+/* 1 if bt_encoder_layer / bt_encoder_forward use bt_gemm_bias_residual_ln after the FFN2 projection
+ * (encoder.py:404-407) for T tokens, hidden size k and FFN width f -- every layer except the last of a
+ * forward that ends in bt_ln_bias_residual_out (bt_one_launch_ends). */
+BT_API int bt_fused_ffn2_ln(int T, int k, int f);
 
 /* Fused attention-output / FFN2 projection + add-bias + residual + LayerNorm (encoder.py:385-388 and
  * :404-407, i.e. gemm then fusion.py:79 add_bias_residual_layernorm):

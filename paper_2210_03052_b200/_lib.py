@@ -61,6 +61,7 @@ SIGNATURES = {
     "bt_ln_bias_residual": (_I, [_P, _P, _P, _P, _P, _F, _P, _I, _I, _S]),
     "bt_gemm_bias_residual_ln": (_I, [_P, _P, _P, _P, _P, _P, _F, _P, _I, _I, _I, _S]),
     "bt_fused_attn_out_ln": (_I, [_I, _I]),
+    "bt_fused_ffn2_ln": (_I, [_I, _I, _I]),
     "bt_plan_sched": (_I, [_P, _I, _I, _P, _S]),
     "bt_plan_sched_bytes": (_SZ, [_I, _I]),
     "bt_plan_forward": (_I, [_P, _I, _I, _P, _P, _S]),

@@ -28,20 +28,25 @@ int ln_launch(const void* x, const void* residual, const float* bias, const floa
               void* out, int T, int k, cudaStream_t s, float* outf, const int32_t* row_map);
 int gemm_ln_launch(const void* A, const void* Bt, const float* bias, const void* residual, const float* gamma,
                    const float* beta, float eps, void* Y, int M, int N, int K, cudaStream_t s);
-// BT_FUSED_LN: 0 = GEMM + separate LayerNorm kernel everywhere, 1 (default) =
-// the fused GEMM+LN kernel after the attention-output GEMM (K = k), 2 = after
-// both projections (where gemm_ln_fits).  Measured at C2 (ms/step): 0.802 /
-// 0.787 / 0.809 -- at K = 4k the fused kernel's 128 x 128 tiles lose more
-// mainloop efficiency than the separate LayerNorm launch costs.
+// BT_FUSED_LN: 0 = GEMM + separate LayerNorm kernel everywhere, 1 = the
+// fused GEMM+LN kernel after the attention-output GEMM (K = k), 2 (default) =
+// after both projections (each where gemm_ln_fits: one wave of clusters).  The
+// forward's last layer keeps FFN2 + the LayerNorm that writes the fp32 output
+// rows (one-launch ends).  Round 1 measured mode 2 slower at C2 (0.809 vs
+// 0.787 ms/step); after the GEMM+LN kernel's deeper weight prefetch and the
+// GEMM changes it is faster: C2 0.685 vs 0.700 ms/step (three alternations,
+// scripts/ab_gemm_ln_ffn2.sh); C3's row blocks exceed one wave (unchanged).
 static int fused_ln_mode() {
   static int mode = -1;
   if (mode < 0) {
     const char* e = getenv("BT_FUSED_LN");
-    mode = (e && e[0] >= '0' && e[0] <= '2') ? e[0] - '0' : 1;
+    mode = (e && e[0] >= '0' && e[0] <= '2') ? e[0] - '0' : 2;
   }
   return mode;
 }
 
+
+static bool fused_ffn2_ln(int T, int k, int f) { return fused_ln_mode() >= 2 && gemm_ln_fits(T, k, f); }
 
 // Diagnostics only (results are wrong when set): BT_DEBUG_SKIP = a set of
 // letters naming launches of every layer to leave out -- q (QKV GEMM), m
@@ -64,7 +69,7 @@ static bool one_launch_ends(int k, int bs) {
     const char* e = getenv("BT_ONE_LAUNCH_ENDS");
     env = (e && e[0] == '0') ? 0 : 1;
   }
-  return env == 1 && k % 8 == 0 && bs <= 4096 && fused_ln_mode() < 2 && !debug_skip('l');
+  return env == 1 && k % 8 == 0 && bs <= 4096 && !debug_skip('l');
 }
 
 // Instrumented FlopCounter (reference tensor.py:198-199, attention.py:232-236):
@@ -180,7 +185,7 @@ static int encoder_layer_impl(const bt_layer_weights* w, const bt_layer_cfg* cfg
   if (!debug_skip('f')) BT_TRY(bt::gemm_launch(L.y0, w->w1, w->b1, nullptr, L.h1, T, f, k, BT_EPI_BIAS_GELU, 0, s));
   count_gemm(2, T, f, k);
   BT_TRY(mark(s));
-  if (fused_ln_mode() >= 2 && gemm_ln_fits(T, k, f)) {  // x = LN((h1 W2 + y0) + b2), one kernel
+  if (fused_ffn2_ln(T, k, f) && final_out == nullptr) {  // x = LN((h1 W2 + y0) + b2), one kernel
     BT_TRY(gemm_ln_launch(L.h1, w->w2, w->b2, L.y0, w->ln1_g, w->ln1_b, w->ln1_eps, x, T, k, f, s));
     count_gemm(3, T, k, f);
     BT_TRY(mark(s));
@@ -207,6 +212,10 @@ extern "C" int bt_one_launch_ends(int k, int bs) { return bt::one_launch_ends(k,
 extern "C" int bt_fused_attn_out_ln(int T, int k) {
   return (bt::fused_ln_mode() >= 1 && bt::gemm_ln_fits(T, k, k)) ? 1 : 0;
 }
+
+// 1 when the forward fuses the FFN2 GEMM with add-bias + residual + LayerNorm
+// (every layer but a one-launch-ends forward's last) for T tokens.
+extern "C" int bt_fused_ffn2_ln(int T, int k, int f) { return bt::fused_ffn2_ln(T, k, f) ? 1 : 0; }
 
 extern "C" int bt_encoder_layer(const bt_layer_weights* w, const bt_layer_cfg* cfg, const int32_t* seq_starts, int bs,
                                 int T, void* x_inout, void* ws, size_t ws_bytes, bt_stream_t stream) {

@@ -126,7 +126,11 @@ def forward_sharded(weights, seqs, input_padded, config, *, group=None, gather: 
     on the partition when the forward runs the one-problem-per-tile MHA
     (max_seq_len > 256 or batch > 256; the segment kernel that groups short
     sequences for small batches shifts their keys inside a block, which
-    changes bf16 rounding only): tests/test_gpu_determinism.py."""
+    changes bf16 rounding only) and the shard and the full batch make the
+    same GEMM + LayerNorm fusion choice (the fused kernel runs when a batch's
+    128-row blocks fit one wave of clusters, ``bt_fused_attn_out_ln`` /
+    ``bt_fused_ffn2_ln``; it rounds the projection differently, within
+    tolerance): tests/test_gpu_determinism.py."""
     from dataclasses import replace
 
     import torch

@@ -25,7 +25,6 @@ METRICS = ("gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.
 # kernel-name prefix -> bench.py kernel-table name, in forward order per layer
 ROLES = (("forward_prologue", "prologue"), ("plan_scan", "plan"), ("pack_kernel", "pack"), ("mha_fwd", "mha"), ("gemm_ln_kernel", "gemm_attn_out_ln"),
          ("ln_bias_residual", "ln"), ("unpack_kernel", "unpack"))
-GEMM_ORDER = ("gemm_qkv", "gemm_attn_out", "gemm_ffn1_gelu", "gemm_ffn2")
 
 _SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
@@ -53,27 +52,27 @@ def read_report(path: Path) -> list[dict]:
 
 
 def roles(items: list[dict], tag: str) -> dict:
-    """Name each launch by its role in the layer (GEMMs in forward order)."""
-    named, g = {}, 0
-    ln_seen = 0
+    """Name each launch by its role in the layer, following the forward's
+    order: QKV GEMM, MHA, attn-out GEMM (+ LN0, or the fused GEMM+LN), FFN1
+    GEMM, FFN2 GEMM (+ LN1, or the fused GEMM+LN)."""
+    named = {}
+    nxt = "qkv"  # the next projection of the layer
     for it in items:
         k = it["kernel"]
         traffic = _bytes(it.get("dram__bytes_read.sum", "0 byte")) + _bytes(it.get("dram__bytes_write.sum", "0 byte"))
         name = None
         if k.startswith("void gemm_bf16") or k.startswith("gemm_bf16"):
-            # the fused attn-out GEMM+LN replaces the second plain GEMM
-            if g == 1 and any(x["kernel"].startswith("void gemm_ln") for x in items):
-                g = 2
-            name = GEMM_ORDER[g % 4]
-            g += 1
+            name, nxt = {"qkv": ("gemm_qkv", "attn_out"), "attn_out": ("gemm_attn_out", "ffn1"),
+                         "ffn1": ("gemm_ffn1_gelu", "ffn2"), "ffn2": ("gemm_ffn2", "qkv")}[nxt]
+        elif "gemm_ln_kernel" in k:
+            name, nxt = ("gemm_ffn2_ln", "qkv") if nxt == "ffn2" else ("gemm_attn_out_ln", "ffn1")
         else:
             for prefix, role in ROLES:
                 if prefix in k:
                     name = role
                     break
             if name == "ln":
-                name = "ln0" if (ln_seen == 0 and not any("gemm_ln" in x["kernel"] for x in items)) else "ln1"
-                ln_seen += 1
+                name = "ln0" if nxt == "ffn1" else "ln1"
         if name and f"{tag}:{name}" not in named:
             named[f"{tag}:{name}"] = int(traffic)
     return named
