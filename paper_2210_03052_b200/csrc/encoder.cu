@@ -46,7 +46,14 @@ static int fused_ln_mode() {
 }
 
 
-static bool fused_ffn2_ln(int T, int k, int f) { return fused_ln_mode() >= 2 && gemm_ln_fits(T, k, f); }
+// FFN2 + LN1 fusion: one wave of clusters, and at least 8 row blocks -- with
+// fewer, the 128 x 128 tiles over K = 4k leave most SMs idle and the plain
+// SM-pair GEMM + LN is as fast or faster (graph-captured BERT-base, same box:
+// bs 1 x mx 1024 (T 614) 0.667 vs 0.608 ms, bs 1 x 64 (T 38) 0.456 vs 0.437,
+// bs 16 x 64 (T 614) 0.493 vs 0.486; at C2 (T 2458) 0.685 vs 0.700).
+static bool fused_ffn2_ln(int T, int k, int f) {
+  return fused_ln_mode() >= 2 && T > 7 * 128 && gemm_ln_fits(T, k, f);
+}
 
 // Diagnostics only (results are wrong when set): BT_DEBUG_SKIP = a set of
 // letters naming launches of every layer to leave out -- q (QKV GEMM), m

@@ -66,9 +66,17 @@ def test_forward_c1_golden(bt, golden):
 
 @pytest.mark.parametrize("kind", ["init", "stress"])
 def test_forward_c2_vs_oracle(bt, kind):
-    """C2 geometry (BERT-base 12 layers, bs 16, mx 256) vs the fp32 oracle."""
+    """C2 geometry (BERT-base 12 layers, bs 16, mx 256) vs the fp32 oracle.
+    This is the shape where both projections run fused with their LayerNorm
+    (layers 1-11; the last layer's FFN2 + LN writes the fp32 output rows)."""
+    from paper_2210_03052_b200 import _lib
+
+    L = _lib.load()
+    assert L.bt_fused_attn_out_ln(2458, 768) == 1 and L.bt_fused_ffn2_ln(2458, 768, 3072) == 1
+    assert L.bt_fused_ffn2_ln(614, 768, 3072) == 0  # too few row blocks (encoder.cu fused_ffn2_ln)
     cfg = bt.preset_config("bert_base", 16, 256, bt.OptFlags.all_on())
     lens = orc.gen_lengths(16, 256, "fixed", seed=0, alpha=0.6)
+    assert sum(lens) == 2458
     x = orc.gen_input(lens, 256, 768, 0)
     w = _weights(bt, cfg, 0, kind)
     ocfg = orc.OracleConfig(12, 12, 64, 256, 16)
