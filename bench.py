@@ -222,6 +222,19 @@ def blas_threads() -> int:
         return int(os.environ.get("OPENBLAS_NUM_THREADS", os.cpu_count() or 1))
 
 
+def _all_blas_threads():
+    """Context raising the BLAS thread pool to every core this process may run on."""
+    import contextlib
+
+    try:
+        from threadpoolctl import threadpool_limits
+
+        ncores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+        return threadpool_limits(limits=ncores, user_api="blas")
+    except Exception:  # noqa: BLE001
+        return contextlib.nullcontext()
+
+
 def cpu_baseline_leg(cf: CpuForward, budget_s: float, runs: int = 3):
     """cpu_baseline: median of `runs` timed forwards on all host BLAS threads
     plus one run on a single thread (threadpoolctl), each on a bounded
@@ -694,18 +707,22 @@ def run_reference(args, wl):
     hidden = heads * 64
     x = harness.gen_input(seqs, hidden, 0)
     cf = CpuForward(heads, layers, mx, list(seqs.lengths), x)
-    # bound each step so that W + K steps fit cpu_budget_total
-    n = cf.size_for(args.cpu_budget_total / max(1, args.steps + args.warmup))
-    for _ in range(args.warmup):
-        cf.run(n)
-    times = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        cf.run(n)
-        times.append(time.perf_counter() - t0)
+    # every host thread this process may use: torchrun (N > 1) exports
+    # OMP_NUM_THREADS=1 to each rank, which would leave the reference's BLAS
+    # on one core; rank 0 alone runs this arm, so it raises the limit again
+    with _all_blas_threads():
+        # bound each step so that W + K steps fit cpu_budget_total
+        n = cf.size_for(args.cpu_budget_total / max(1, args.steps + args.warmup))
+        for _ in range(args.warmup):
+            cf.run(n)
+        times = []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            cf.run(n)
+            times.append(time.perf_counter() - t0)
+        cores = blas_threads()
     ms = sum(times) * 1e3 / len(times)
     v = n / (ms / 1e3)
-    cores = blas_threads()
     sample = (f"{cf.what} on the first {n} of {len(seqs.lengths)} sequences ({sum(seqs.lengths[:n])} tokens), "
               f"{layers} layers per step")
     return {"impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": "seq/s", "n_gpus": world,
