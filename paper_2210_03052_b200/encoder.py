@@ -613,10 +613,12 @@ class BertEncoderB200:
 
     def forward_host_pageable(self, seqs: SeqLengths, arr, out_pinned, config: ModelConfig | None = None):
         """forward_host_packed for a pageable host input (a reference-style
-        numpy ``Tensor``, fp32 [bs*mx, k]): only the valid rows are staged,
-        packed, into a write-combined page-locked buffer (host copies by a
-        small thread pool), which goes over PCIe as ONE contiguous DMA, then the cached
-        graph and the per-sequence D2H as forward_host_packed.  Synchronises."""
+        numpy ``Tensor``, fp32 [bs*mx, k]): only each sequence's valid rows
+        go over PCIe, copied straight from the pageable array into the packed
+        device buffer (the driver stages them page-locked and overlaps that
+        with the DMA; BT_PAGEABLE_STAGE=1: a write-combined staging buffer
+        filled by a thread pool, then one DMA), then the cached graph and the
+        per-sequence D2H as forward_host_packed.  Synchronises."""
         import concurrent.futures as cf
 
         with self._lock:
@@ -626,8 +628,8 @@ class BertEncoderB200:
             graph, run, xp, yp, _, _ = self._graph_entry(seqs, cfg, cfg_c)
             torch = self.torch
             T = seqs.total
-            stage = self._stage.get((T, k))
-            if stage is None:
+            stage = self._stage.get((T, k)) if _PAGEABLE_STAGE else None
+            if stage is None and _PAGEABLE_STAGE:
                 stage = _WcStage(T, k)
                 self._stage = {(T, k): stage}  # one shape kept
             if self._pool is None:
@@ -639,20 +641,28 @@ class BertEncoderB200:
             h2d.wait_stream(cur)
             comp.wait_stream(cur)
             lengths_h = np.ascontiguousarray(np.asarray(seqs.lengths, dtype=np.int32))
-            starts = np.concatenate([[0], np.cumsum(lengths_h)])
-            sn = stage.array
-            bounds = self.chunk_bounds(seqs.lengths, min(bs, 8))
+            if _PAGEABLE_STAGE:
+                starts = np.concatenate([[0], np.cumsum(lengths_h)])
+                sn = stage.array
+                bounds = self.chunk_bounds(seqs.lengths, min(bs, 8))
 
-            def copy_group(b0, b1):
-                for b in range(b0, b1):
-                    sn[starts[b]:starts[b + 1]] = arr[b * mx: b * mx + lengths_h[b]]
+                def copy_group(b0, b1):
+                    for b in range(b0, b1):
+                        sn[starts[b]:starts[b + 1]] = arr[b * mx: b * mx + lengths_h[b]]
 
-            for f in [self._pool.submit(copy_group, b0, b1) for b0, b1 in bounds]:
-                f.result()
-            one = np.asarray([T], dtype=np.int32)
-            with torch.cuda.stream(h2d):  # one contiguous DMA of the packed rows (a single T-row "sequence")
-                _lib.call("bt_copy_rows", xp.data_ptr(), stage.ptr, one.ctypes.data, 1, T, k * 4, 1,
-                          _lib.stream_ptr())
+                for f in [self._pool.submit(copy_group, b0, b1) for b0, b1 in bounds]:
+                    f.result()
+                one = np.asarray([T], dtype=np.int32)
+                with torch.cuda.stream(h2d):  # one contiguous DMA of the packed rows (a single T-row "sequence")
+                    _lib.call("bt_copy_rows", xp.data_ptr(), stage.ptr, one.ctypes.data, 1, T, k * 4, 1,
+                              _lib.stream_ptr())
+            else:
+                # each sequence's valid rows straight from the pageable array:
+                # the driver stages them through its own page-locked ring and
+                # overlaps that host copy with the DMA
+                with torch.cuda.stream(h2d):
+                    _lib.call("bt_copy_rows", xp.data_ptr(), arr.ctypes.data, lengths_h.ctypes.data, bs, mx, k * 4,
+                              1, _lib.stream_ptr())
             comp.wait_stream(h2d)
             with torch.cuda.stream(comp):
                 if graph is not None:
@@ -908,6 +918,16 @@ def forward_stream(weights, batches, config):
         items.append((sq, _pinned_f32(x, torch), out))
     eng.forward_host_stream(items, config=config)
     return [Tensor(out.numpy()) for _, _, out in items]
+
+
+# BT_PAGEABLE_STAGE=1: forward_host_pageable stages the valid rows into a
+# write-combined page-locked buffer with a 4-thread pool, then one DMA (the
+# earlier path); default 0: per-sequence copies straight from the pageable
+# array.  Measured at C2 (scripts/h2d_rate_probe.py): after a multi-threaded
+# host write the 7.5 MB DMA runs at 12 GB/s (0.61 ms; 47 GB/s after a
+# single-threaded write), while the driver-staged pageable copy moves the same
+# rows in 0.39 ms of host wall time, host copy included.
+_PAGEABLE_STAGE = os.environ.get("BT_PAGEABLE_STAGE", "0") == "1"
 
 
 class _WcStage:
