@@ -358,6 +358,7 @@ class BertEncoderB200:
         self._io_streams = None  # host-I/O pipeline: H2D, compute, D2H
         self._io_events = []
         self._stage = {}  # page-locked packed staging buffer for pageable inputs
+        self._stream_stage = {}  # forward_host_stream: two page-locked packed staging slots
         self._pool = None
 
     def layer(self, i: int) -> DeviceLayer:
@@ -684,7 +685,11 @@ class BertEncoderB200:
         batch is a whole forward_host_packed (valid rows DMA'd in, the cached
         graph, valid rows DMA'd out), but consecutive batches overlap on three
         streams -- H2D(i + 1) and D2H(i - 1) run under forward(i) -- with the
-        device buffers double-buffered (graph entries in two slots).
+        device buffers double-buffered (graph entries in two slots).  An
+        input may also be pageable (``_PageableRows``, a numpy caller's
+        array): its valid rows are packed into one of two page-locked
+        staging slots by the host thread pool while the GPU runs the
+        previous batch, then DMA'd as one copy.
         Synchronises once at the end; returns the out buffers."""
         with self._lock:
             cfg = config or self.config
@@ -712,12 +717,47 @@ class BertEncoderB200:
             ev_out = [torch.cuda.Event() for _ in range(n)]
             lens = [np.ascontiguousarray(np.asarray(sq.lengths, dtype=np.int32)) for sq, _, _ in items]
             whole = [np.asarray([sq.batch_size * sq.max_seq_len], dtype=np.int32) for sq, _, _ in items]
+            # pageable inputs (numpy): batch i's valid rows are packed into a
+            # page-locked staging slot (i % 2) by the host thread pool while
+            # the GPU runs batch i - 1, then cross PCIe as one DMA
+            staged = [isinstance(x, _PageableRows) and not pd for (_, x, _), pd in zip(items, padded)]
+            if any(staged):
+                import concurrent.futures as cf
+
+                if self._pool is None:
+                    self._pool = cf.ThreadPoolExecutor(max_workers=4, thread_name_prefix="bt200-host")
+                tmax = max(sq.total for (sq, _, _), st in zip(items, staged) if st)
+                slots = self._stream_stage.get((tmax, k))
+                if slots is None:
+                    slots = [torch.empty((tmax, k), dtype=torch.float32, pin_memory=True) for _ in range(2)]
+                    self._stream_stage = {(tmax, k): slots}
             for i, ((sq, x, out), e) in enumerate(zip(items, entries)):
                 bs, mx = sq.batch_size, sq.max_seq_len
+                if staged[i]:
+                    if i >= 2:
+                        ev_in[i - 2].synchronize()  # H2D(i - 2) has read this staging slot
+                    sn = slots[i % 2].numpy()
+                    arr = x.arr
+                    st = np.concatenate([[0], np.cumsum(lens[i])])
+                    bounds = self.chunk_bounds(sq.lengths, min(bs, _STAGE_CHUNKS))
+
+                    def copy_group(b0, b1, sn=sn, arr=arr, st=st, ln=lens[i], mx=mx):
+                        for b in range(b0, b1):
+                            sn[st[b]:st[b + 1]] = arr[b * mx: b * mx + ln[b]]
+
+                    if len(bounds) == 1:
+                        copy_group(*bounds[0])
+                    else:
+                        for f in [self._pool.submit(copy_group, b0, b1) for b0, b1 in bounds]:
+                            f.result()
                 if i >= 2:
                     h2d.wait_event(ev_done[i - 2])  # forward(i - 2) has read this slot's input
                 with torch.cuda.stream(h2d):
-                    if padded[i]:  # one contiguous copy of the padded input
+                    if staged[i]:  # the packed rows as one DMA (a single T-row "sequence")
+                        one = np.asarray([sq.total], dtype=np.int32)
+                        _lib.call("bt_copy_rows", e[2].data_ptr(), slots[i % 2].data_ptr(), one.ctypes.data, 1,
+                                  sq.total, row_b, 1, _lib.stream_ptr())
+                    elif padded[i]:  # one contiguous copy of the padded input
                         _lib.call("bt_copy_rows", e[2].data_ptr(), x.data_ptr(), whole[i].ctypes.data, 1, bs * mx,
                                   row_b, 1, _lib.stream_ptr())
                     else:
@@ -742,8 +782,10 @@ class BertEncoderB200:
                         _lib.call("bt_copy_rows", out.data_ptr(), e[3].data_ptr(), lens[i].ctypes.data, bs, mx, row_b,
                                   0, _lib.stream_ptr())
                     ev_out[i].record(d2h)
-            for (sq, _, out), pd in zip(items, padded):  # padded output rows are exact zeros (packing.py:158-159)
-                if not pd:
+                if staged[i]:  # (host paced by the GPU here: zero this batch's padded rows now)
+                    self._zero_padded_rows(out, sq, k)
+            for (sq, _, out), pd, sg in zip(items, padded, staged):  # padded output rows are exact zeros
+                if not pd and not sg:  # (packing.py:158-159)
                     self._zero_padded_rows(out, sq, k)
             d2h.synchronize()
             cur.wait_stream(d2h)
@@ -915,7 +957,7 @@ def forward_stream(weights, batches, config):
         if is_device(x):
             raise ShapeError("forward_stream takes host inputs (use forward for CUDA tensors)")
         out = torch.empty((rows, cols), dtype=torch.float32, pin_memory=True)
-        items.append((sq, _pinned_f32(x, torch), out))
+        items.append((sq, _host_source(x, torch), out))
     eng.forward_host_stream(items, config=config)
     return [Tensor(out.numpy()) for _, _, out in items]
 
@@ -928,6 +970,7 @@ def forward_stream(weights, batches, config):
 # single-threaded write), while the driver-staged pageable copy moves the same
 # rows in 0.39 ms of host wall time, host copy included.
 _PAGEABLE_STAGE = os.environ.get("BT_PAGEABLE_STAGE", "0") == "1"
+_STAGE_CHUNKS = int(os.environ.get("BT_STAGE_CHUNKS", "8"))
 
 
 class _WcStage:
@@ -954,6 +997,26 @@ class _WcStage:
 
 def _is_pinned_torch(x) -> bool:
     return type(x).__module__.startswith("torch") and not x.is_cuda and x.dtype.is_floating_point and x.is_pinned()
+
+
+class _PageableRows:
+    """A pageable fp32 host array as a copy source (``data_ptr``): the H2D
+    copies read it directly, staged page-locked by the driver."""
+
+    def __init__(self, arr: np.ndarray):
+        self.arr = arr
+
+    def data_ptr(self) -> int:
+        return self.arr.ctypes.data
+
+
+def _host_source(x, torch):
+    """forward_stream's input buffer: a page-locked fp32 torch tensor in
+    place, any other host input as its pageable fp32 array (no host-side
+    copy into pinned memory first; BT_PAGEABLE_STAGE=1 restores that copy)."""
+    if _PAGEABLE_STAGE or _is_pinned_torch(x) and x.dtype == torch.float32 and x.is_contiguous():
+        return _pinned_f32(x, torch)
+    return _PageableRows(np.ascontiguousarray(host_array(x), dtype=np.float32))
 
 
 def _pinned_f32(x, torch):
