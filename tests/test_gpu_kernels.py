@@ -90,6 +90,22 @@ def test_gemm_public_api(env):
         bt.gemm(bt.Tensor(a), bt.Tensor(b[:64]))
 
 
+@pytest.mark.parametrize("K,N", [(100, 50), (7, 3), (64, 130)])
+def test_gemm_public_api_any_shape(env, K, N):
+    """The reference gemm takes any shape (tensor.py:177-200); K and N that
+    are not multiples of 64 run zero-padded on the device."""
+    bt, torch = env
+    rng = np.random.default_rng(K * 1000 + N)
+    a = rng.standard_normal((45, K)).astype(np.float32)
+    b = (rng.standard_normal((K, N)) * 0.1).astype(np.float32)
+    bias = rng.standard_normal(N).astype(np.float32)
+    got = bt.gemm(bt.Tensor(a), bt.Tensor(b), bt.EpilogueHook.add_bias(bias))
+    assert got.array.shape == (45, N)
+    assert_close_bf16(got, a @ b + bias, rel_max=1e-2, what=f"gemm {K}x{N}")
+    got = bt.gemm(bt.Tensor(a), bt.Tensor(b))
+    assert_close_bf16(got, a @ b, rel_max=1e-2, what=f"gemm {K}x{N} no epilogue")
+
+
 @pytest.mark.parametrize("k", [768, 1024, 64, 2048])
 def test_layernorm(env, k):
     bt, torch = env
