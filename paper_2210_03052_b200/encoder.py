@@ -629,8 +629,11 @@ class BertEncoderB200:
             graph, run, xp, yp, _, _ = self._graph_entry(seqs, cfg, cfg_c)
             torch = self.torch
             T = seqs.total
-            stage = self._stage.get((T, k)) if _PAGEABLE_STAGE else None
-            if stage is None and _PAGEABLE_STAGE:
+            # thousands of per-sequence pageable copies (C5: 2048) cost more
+            # than staging: large batches keep the staged path
+            use_stage = _PAGEABLE_STAGE or bs > STREAM_ROW_COPIES_MAX
+            stage = self._stage.get((T, k)) if use_stage else None
+            if stage is None and use_stage:
                 stage = _WcStage(T, k)
                 self._stage = {(T, k): stage}  # one shape kept
             if self._pool is None:
@@ -642,7 +645,7 @@ class BertEncoderB200:
             h2d.wait_stream(cur)
             comp.wait_stream(cur)
             lengths_h = np.ascontiguousarray(np.asarray(seqs.lengths, dtype=np.int32))
-            if _PAGEABLE_STAGE:
+            if use_stage:
                 starts = np.concatenate([[0], np.cumsum(lengths_h)])
                 sn = stage.array
                 bounds = self.chunk_bounds(seqs.lengths, min(bs, 8))
