@@ -317,3 +317,35 @@ def test_forward_stream_padded_copies(bt, monkeypatch):
     outs = bt.forward_stream(w, batches, cfg)
     for (sq, x), y in zip(batches, outs):
         assert np.array_equal(y.array, bt.forward(w, sq, x, cfg).array)
+
+
+def test_forward_stream_mixed_host_inputs(bt):
+    """forward_stream over a mix of pageable numpy inputs (packed into the two
+    page-locked staging slots inside the pipeline), page-locked torch inputs
+    (DMA'd in place) and non-pinned torch CPU tensors, with batch totals that
+    differ from batch to batch (slots sized by the largest): every output
+    bitwise the per-call forward(), padded rows exactly zero."""
+    import torch
+
+    mx, layers, bs = 64, 1, 4
+    cfg = bt.ModelConfig(layers=layers, head_num=12, head_size=64, max_seq_len=mx, batch_size=bs,
+                         flags=bt.OptFlags.all_on())
+    w = bt.init_weights(cfg, seed=5)
+    lens_list = [[64, 1, 30, 7], [2, 3, 4, 5], [64, 64, 64, 64], [10, 64, 1, 33], [1, 1, 1, 1], [50, 20, 64, 9]]
+    batches, arrays = [], []
+    for i, lens in enumerate(lens_list):
+        x = orc.gen_input(lens, mx, 768, seed=40 + i).astype(np.float32)
+        if i % 3 == 0:
+            xin = bt.Tensor(x)
+        elif i % 3 == 1:
+            xin = torch.from_numpy(x.copy()).pin_memory()
+        else:
+            xin = torch.from_numpy(x.copy())
+        batches.append((bt.SeqLengths.of(lens, mx), xin))
+        arrays.append(x)
+    outs = bt.forward_stream(w, batches, cfg)
+    for (sq, _), x, y in zip(batches, arrays, outs):
+        single = bt.forward(w, sq, bt.Tensor(x), cfg).array
+        assert np.array_equal(y.array, single)
+        pad = ~orc.build_mask(list(sq.lengths), mx).reshape(-1).astype(bool)
+        assert not y.array[pad].any()
