@@ -617,9 +617,11 @@ class BertEncoderB200:
         numpy ``Tensor``, fp32 [bs*mx, k]): only each sequence's valid rows
         go over PCIe, copied straight from the pageable array into the packed
         device buffer (the driver stages them page-locked and overlaps that
-        with the DMA; BT_PAGEABLE_STAGE=1: a write-combined staging buffer
-        filled by a thread pool, then one DMA), then the cached graph and the
-        per-sequence D2H as forward_host_packed.  Synchronises."""
+        with the DMA).  Batches of more than STREAM_ROW_COPIES_MAX sequences
+        (or BT_PAGEABLE_STAGE=1) instead pack the valid rows into a
+        write-combined staging buffer with a thread pool, then one DMA.  Then
+        the cached graph and the per-sequence D2H as forward_host_packed.
+        Synchronises."""
         import concurrent.futures as cf
 
         with self._lock:
@@ -967,8 +969,11 @@ def forward_stream(weights, batches, config):
 
 # BT_PAGEABLE_STAGE=1: forward_host_pageable stages the valid rows into a
 # write-combined page-locked buffer with a 4-thread pool, then one DMA (the
-# earlier path); default 0: per-sequence copies straight from the pageable
-# array.  Measured at C2 (scripts/h2d_rate_probe.py): after a multi-threaded
+# earlier path, still used for batches of more than STREAM_ROW_COPIES_MAX
+# sequences: C5's 2048 per-sequence pageable copies measured slower, 3.0k vs
+# 3.4k seq/s per call); default 0: per-sequence copies straight from the
+# pageable array.  BT_STAGE_CHUNKS: how many host threads' worth of chunks
+# forward_host_stream packs a pageable batch in.  Measured at C2 (scripts/h2d_rate_probe.py): after a multi-threaded
 # host write the 7.5 MB DMA runs at 12 GB/s (0.61 ms; 47 GB/s after a
 # single-threaded write), while the driver-staged pageable copy moves the same
 # rows in 0.39 ms of host wall time, host copy included.
